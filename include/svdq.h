@@ -1,0 +1,185 @@
+/*
+ * svdq.h -- C ABI of libsvdq.so: SVDQuant's W4A4 linear with an absorbed
+ * 16-bit low-rank branch, B200 (sm_100a) native.
+ *
+ * The operation (PAPER.md, "P:n" = line n):
+ *   X in R^{b x m}, W in R^{m x n}
+ *   X_hat = X diag(lambda)^-1,  W_hat = diag(lambda) W               (reading Q1)
+ *   W_hat = L1 L2 + R  (truncated SVD, L1 = U Sigma_{:,:r}, L2 = V_{:r,:})
+ *   X W ~= X_hat L1 L2  +  Q(X_hat) Q(R)                             (Eq. 5)
+ *   Q(.) per-group symmetric: INT4 g64 16-bit scales, NVFP4 g16 E4M3 scales (Eq. 1)
+ * computed as two fused kernels (Fig. 5(b)):
+ *   K1 svdq_quantize_act_lowrank_down : one read of X -> Q(X_hat) codes + scales, and X L1
+ *   K2 svdq_gemm_w4a4_lowrank_up      : Q(X_hat) Q(R) + (X L1) L2 + bias into one output tile
+ * LoRA is attached by concatenation into L1 / L2 (svdq_lora_fuse).
+ *
+ * GEMM naming: M = b (tokens), K = m (input channels), N = n (output channels).
+ *
+ * Conventions (all entry points)
+ *  - Ownership: the caller allocates EVERY buffer (sizes from the *_sizes
+ *    queries); the library allocates nothing on the hot path and keeps no
+ *    per-layer state.  svdq_linear is a non-owning view that must stay valid
+ *    until enqueued work completes.
+ *  - Streams: `stream` is a cudaStream_t (NULL = legacy default stream).  Hot
+ *    path calls only enqueue work; they never synchronize.  Offline calls that
+ *    synchronize say so.
+ *  - Errors: a status code is returned; nothing aborts or throws across the ABI.
+ *    Arguments are validated on the host before any launch, so outputs are
+ *    untouched on error.  svdq_last_error() returns a thread-local detail string.
+ *  - Pointers marked [dev] are device pointers, [host] host pointers.
+ *  - Packing: 4-bit codes two per byte, low nibble = even K index.
+ *    NVFP4 codes are E2M1 (sign-magnitude; -0 = 0x8); INT4 codes are two's
+ *    complement in [-7, 7].
+ *  - NVFP4 scale factors: unsigned E4M3 bytes in the "128x4" tile layout over
+ *    rows padded to a multiple of 128:
+ *      off(row, c) = (row/128)*(K/64)*512 + (c/4)*512 + (row%32)*16 + ((row%128)/32)*4 + c%4
+ *    with c = k/16.  Padding rows hold 0x00.
+ *  - INT4 scales: [rows][K/64] row-major, bf16 or fp16 (reading Q8).
+ *  - Preconditions: K % 64 == 0; N % 16 == 0; M >= 1; rank % 16 == 0 and
+ *    0 <= rank <= 128; device pointers and row pitches 16-byte aligned.
+ */
+#ifndef SVDQ_H_
+#define SVDQ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SVDQ_OK = 0,
+  SVDQ_ERR_INVALID_ARGUMENT = 1, /* null pointer, bad enum                         */
+  SVDQ_ERR_SHAPE = 2,            /* K%64, N%16, M<1, dimension mismatch           */
+  SVDQ_ERR_RANK = 3,             /* rank%16 != 0 or out of [0, 128]               */
+  SVDQ_ERR_ALIGNMENT = 4,        /* pointer / pitch not 16-byte aligned           */
+  SVDQ_ERR_UNSUPPORTED = 5,      /* device is not sm_100, or format/dtype combo   */
+  SVDQ_ERR_NONFINITE = 6,        /* reserved (hot path never scans inputs)        */
+  SVDQ_ERR_CUDA = 7,             /* CUDA / cuBLAS / cuSOLVER failure              */
+  SVDQ_ERR_WORKSPACE = 8         /* workspace too small                          */
+} svdq_status;
+
+typedef enum { SVDQ_FMT_NVFP4 = 0, SVDQ_FMT_INT4 = 1 } svdq_format;
+typedef enum { SVDQ_BF16 = 0, SVDQ_FP16 = 1, SVDQ_FP32 = 2 } svdq_dtype;
+
+/* Quantized linear layer: non-owning view of caller-owned device buffers. */
+typedef struct svdq_linear {
+  int32_t fmt;              /* svdq_format                                              */
+  int32_t rank;             /* r (+ LoRA ranks), multiple of 16, <= 128                 */
+  int64_t K;                /* input channels  (paper m)                                */
+  int64_t N;                /* output channels (paper n)                                */
+  const uint8_t *w_codes;   /* [dev] [N][K/2]: Q(R)^T, K-major                          */
+  const uint8_t *w_scales;  /* [dev] NVFP4: 128x4 layout over (ceil(N/128)*128, K/16);  */
+                            /*       INT4 : [N][K/64] of scale_dtype                    */
+  const float *lambda_inv;  /* [dev] [K] fp32 = fl32(1 / lambda)                        */
+  const uint16_t *l1s;      /* [dev] [rank][K] bf16 = (diag(lambda)^-1 L1)^T             */
+  const uint16_t *l2s;      /* [dev] [N][rank] bf16 = L2^T / alpha                      */
+  const void *bias;         /* [dev] [N] of bias_dtype, or NULL                         */
+  int32_t scale_dtype;      /* INT4: SVDQ_BF16 | SVDQ_FP16 (weights AND activations)    */
+  int32_t bias_dtype;       /* SVDQ_BF16 | SVDQ_FP16 | SVDQ_FP32                        */
+  float gs_w;               /* NVFP4 per-tensor weight decode scale; INT4: 1            */
+  float gs_x;               /* NVFP4 static activation decode scale (default 1); INT4: 1 */
+} svdq_linear;
+/* alpha = fl32(gs_x * gs_w) for NVFP4, 1 for INT4; the GEMM epilogue computes
+ * Y = out_rn(fl32(alpha * acc) + bias).                                        */
+
+/* ---------------------------------------------------------------- sizes */
+/* Bytes of K1's outputs for M tokens: xq [M][K/2]; xs (NVFP4: 128x4 layout over
+ * ceil(M/128)*128 rows; INT4: [M][K/64] 16-bit); xl1 [M][rank] bf16.             */
+svdq_status svdq_act_buffer_sizes(int32_t fmt, int64_t M, int64_t K, int32_t rank,
+                                  size_t *xq_bytes, size_t *xs_bytes, size_t *xl1_bytes);
+/* Bytes of a layer's weight operands. */
+svdq_status svdq_weight_buffer_sizes(int32_t fmt, int64_t K, int64_t N, int32_t rank,
+                                     size_t *codes_bytes, size_t *scales_bytes,
+                                     size_t *l1s_bytes, size_t *l2s_bytes);
+
+/* ---------------------------------------------------------------- hot path */
+/* K1: smoothing + activation quantization + low-rank down-projection, one read of X.
+ *   x_hat[m,k] = fl32(x[m,k] * lambda_inv[k])                       (reading Q14)
+ *   NVFP4 per (m, 16-group): sf = e4m3(fl32(amax * fl32(fl32(1/gs_x) * fl32(1/6))));
+ *         qinv = sf==0 ? 0 : fl32(1/fl32(sf*gs_x)); code = e2m1_rn_sat(fl32(x_hat*qinv))
+ *   INT4  per (m, 64-group): s = to16(fl32(amax/7)); qinv = s==0 ? 0 : fl32(1/s);
+ *         code = clamp(rne(fl32(x_hat*qinv)), -7, 7)               (Eq. 1)
+ *   xl1[m,t] = bf16_rn(sum_k x[m,k] * l1s[t,k]), fp32 accumulation  (reading Q15/Q18)
+ * X: [dev] [M][ldx] of x_dtype (BF16 | FP16), ldx >= K elements, ldx % 8 == 0.
+ * xq: [dev] [M][K/2]; xs: [dev] (see sizes); xl1: [dev] [M][rank] (may be NULL if rank == 0).
+ * Bit-exact contract: xq and xs equal the oracle's codes / scales for the same X,
+ * lambda_inv and gs_x, including the 0x00 padding rows of the NVFP4 layout.      */
+svdq_status svdq_quantize_act_lowrank_down(const svdq_linear *L, const void *X, int32_t x_dtype,
+                                           int64_t M, int64_t ldx, uint8_t *xq, uint8_t *xs,
+                                           uint16_t *xl1, void *stream);
+
+/* K2: 4-bit GEMM with the low-rank up-projection folded into the same accumulator.
+ *   NVFP4: acc[m,n] = sum_g f(sfa[m,g]) f(sfb[n,g]) sum_{k in g} e2m1(qa) e2m1(qb)
+ *                     + sum_t xl1[m,t] l2s[n,t]          (tcgen05 kind::mxf4nvf4 + kind::f16)
+ *          Y = out_rn(fl32(alpha * acc) + bias[n])
+ *   INT4:  acc_g = sum_{k in g64} qa qb (exact int32, kind::i8);
+ *          Y = out_rn(sum_g fl32(fl32(float(acc_g) * sx[m,g]) * sw[n,g]) + sum_t xl1 l2s + bias)
+ * Y: [dev] [M][ldy] of y_dtype (BF16 | FP16 | FP32), ldy >= N, ldy % 8 == 0.       */
+svdq_status svdq_gemm_w4a4_lowrank_up(const svdq_linear *L, const uint8_t *xq, const uint8_t *xs,
+                                      const uint16_t *xl1, int64_t M, void *Y, int32_t y_dtype,
+                                      int64_t ldy, void *stream);
+
+/* Convenience: K1 then K2 on one stream.  ws: [dev] >= xq+xs+xl1 bytes (16-B aligned parts). */
+svdq_status svdq_linear_forward(const svdq_linear *L, const void *X, int32_t x_dtype, int64_t M,
+                                int64_t ldx, void *Y, int32_t y_dtype, int64_t ldy, void *ws,
+                                size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------- offline (weights) */
+/* Quantize a residual R (fp32, paper layout [K][N]) per output channel, groups along K.
+ *   NVFP4: gs_w = fl32(amax(|R|) / 2688) (or 1 if amax == 0) unless *gs_w > 0 on input;
+ *          codes / sf by the recipe of K1 with gs = gs_w.  INT4: 16-bit scales of scale_dtype.
+ * codes: [dev] [N][K/2]; scales: [dev] (svdq_weight_buffer_sizes); gs_w: [host] in/out.
+ * Synchronizes `stream` when it must compute gs_w.  Bit-exact against the oracle.   */
+svdq_status svdq_quantize_residual(const float *R, int64_t K, int64_t N, int32_t fmt,
+                                   int32_t scale_dtype, uint8_t *codes, uint8_t *scales,
+                                   float *gs_w, void *stream);
+
+/* Workspace bytes for svdq_quantize_weights. */
+svdq_status svdq_quantize_weights_workspace(int64_t K, int64_t N, int32_t rank, size_t *ws_bytes);
+
+/* Full offline weight preparation:
+ *   lambda_inv = fl32(1/lambda); W_hat = diag(lambda) W;  SVD of W_hat (cuBLAS/cuSOLVER fp64
+ *   Gram + eigensolver) unless L1_opt / L2_opt are given ([dev] fp32 [K][rank] / [rank][N]);
+ *   R = W_hat - L1 L2;  svdq_quantize_residual(R);  l1s = bf16(fl32(lambda_inv[k] * L1[k,t]))^T;
+ *   l2s = bf16(fl32(L2[t,n] / alpha))^T.
+ * W: [dev] [K][N] of w_dtype (paper layout).  lambda: [dev] [K] fp32 > 0.
+ * dst: fmt/rank/K/N set by the call; its buffer pointers (w_codes, w_scales,
+ * lambda_inv, l1s, l2s) must point to writable caller allocations; bias is left as is.
+ * Synchronizes `stream`.  Parity: L1 L2 within 1e-5 of the oracle's (relative to |W_hat|),
+ * codes bit-exact given R (see svdq_quantize_residual).                           */
+svdq_status svdq_quantize_weights(const void *W, int32_t w_dtype, const float *lambda, int64_t K,
+                                  int64_t N, int32_t rank, int32_t fmt, int32_t scale_dtype,
+                                  float gs_x, const float *L1_opt, const float *L2_opt,
+                                  svdq_linear *dst, void *ws, size_t ws_bytes, void *stream);
+
+/* LoRA fusion: dst->l1s = [src->l1s ; bf16(fl32(scale*A))^T] ([r+r_l][K]),
+ * dst->l2s = [src->l2s | bf16(fl32(B/alpha))^T] ([N][r+r_l]); codes / scales untouched
+ * (no re-quantization).  A: [dev] [K][r_l], B: [dev] [r_l][N] of ab_dtype
+ * (BF16 | FP16 | FP32).  dst must point to writable l1s / l2s of the new rank; all other
+ * fields are copied from src.  r_l % 16 == 0.  Enqueue only.                          */
+svdq_status svdq_lora_fuse(const svdq_linear *src, const void *A, const void *B, int32_t ab_dtype,
+                           int32_t r_l, float scale, svdq_linear *dst, void *stream);
+
+/* ---------------------------------------------------------------- test hooks */
+/* INT4 per-group exact accumulators: acc[g][m][n] = sum_{k in g64} qa[m,k] qb[n,k] (int32),
+ * computed on the same kind::i8 tensor-core path as K2.  xq [dev] [M][K/2], wq [dev] [N][K/2],
+ * acc [dev] [K/64][M][N].  Test hook for the bit-exact accumulator pin.               */
+svdq_status svdq_debug_int4_group_accum(const uint8_t *xq, const uint8_t *wq, int64_t M, int64_t N,
+                                        int64_t K, int32_t *acc, void *stream);
+/* Device codecs for the exhaustive format test: out[i] = e2m1x2 byte of (in[2i], in[2i+1])
+ * (cvt.rn.satfinite, low nibble = in[2i]) when kind == 0; e4m3 byte of in[i] when kind == 1. */
+svdq_status svdq_debug_codec(const float *in, uint8_t *out, int64_t n, int32_t kind, void *stream);
+
+/* ---------------------------------------------------------------- misc */
+const char *svdq_status_string(svdq_status s);
+const char *svdq_last_error(void);
+/* Number of this library's kernel launches issued by the calling thread (for bench claims). */
+uint64_t svdq_launch_count(void);
+int32_t svdq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVDQ_H_ */

@@ -1,0 +1,311 @@
+"""ctypes binding of libsvdq.so (include/svdq.h): argument marshalling only.
+
+Every function here has the name of the C entry point it calls.  Device
+buffers are torch CUDA tensors (PyTorch supplies memory and streams only);
+all arithmetic runs in the library's kernels.  There is no CPU fallback:
+importing this module without the built library raises ImportError, and
+every non-OK status raises SvdqError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsvdq.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} not found: build the CUDA library first "
+        "(python -m paper_2411_05007_b200.build or __graft_entry__.build()); "
+        "there is no CPU fallback")
+_lib = C.CDLL(LIB_PATH)
+
+# enums (svdq.h)
+SVDQ_OK = 0
+STATUS_NAMES = {0: "SVDQ_OK", 1: "SVDQ_ERR_INVALID_ARGUMENT", 2: "SVDQ_ERR_SHAPE", 3: "SVDQ_ERR_RANK",
+                4: "SVDQ_ERR_ALIGNMENT", 5: "SVDQ_ERR_UNSUPPORTED", 6: "SVDQ_ERR_NONFINITE",
+                7: "SVDQ_ERR_CUDA", 8: "SVDQ_ERR_WORKSPACE"}
+FMT = {"nvfp4": 0, "int4": 1}
+DTYPE = {"bf16": 0, "fp16": 1, "fp32": 2}
+TORCH_DTYPE = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}
+DTYPE_OF_TORCH = {torch.bfloat16: "bf16", torch.float16: "fp16", torch.float32: "fp32"}
+
+# Every symbol include/svdq.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "svdq_act_buffer_sizes", "svdq_weight_buffer_sizes", "svdq_quantize_act_lowrank_down",
+    "svdq_gemm_w4a4_lowrank_up", "svdq_linear_forward", "svdq_quantize_residual",
+    "svdq_quantize_weights_workspace", "svdq_quantize_weights", "svdq_lora_fuse",
+    "svdq_debug_int4_group_accum", "svdq_debug_codec", "svdq_status_string", "svdq_last_error",
+    "svdq_launch_count", "svdq_version",
+]
+
+
+class svdq_linear(C.Structure):
+    _fields_ = [
+        ("fmt", C.c_int32), ("rank", C.c_int32), ("K", C.c_int64), ("N", C.c_int64),
+        ("w_codes", C.c_void_p), ("w_scales", C.c_void_p), ("lambda_inv", C.c_void_p),
+        ("l1s", C.c_void_p), ("l2s", C.c_void_p), ("bias", C.c_void_p),
+        ("scale_dtype", C.c_int32), ("bias_dtype", C.c_int32),
+        ("gs_w", C.c_float), ("gs_x", C.c_float),
+    ]
+
+
+class SvdqError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        detail = _lib.svdq_last_error().decode()
+        super().__init__(f"{where}: {STATUS_NAMES.get(status, status)}: {detail}")
+
+
+_P = C.c_void_p
+_I32 = C.c_int32
+_I64 = C.c_int64
+_SZ = C.POINTER(C.c_size_t)
+_LP = C.POINTER(svdq_linear)
+_sig = {
+    "svdq_act_buffer_sizes": [_I32, _I64, _I64, _I32, _SZ, _SZ, _SZ],
+    "svdq_weight_buffer_sizes": [_I32, _I64, _I64, _I32, _SZ, _SZ, _SZ, _SZ],
+    "svdq_quantize_act_lowrank_down": [_LP, _P, _I32, _I64, _I64, _P, _P, _P, _P],
+    "svdq_gemm_w4a4_lowrank_up": [_LP, _P, _P, _P, _I64, _P, _I32, _I64, _P],
+    "svdq_linear_forward": [_LP, _P, _I32, _I64, _I64, _P, _I32, _I64, _P, C.c_size_t, _P],
+    "svdq_quantize_residual": [_P, _I64, _I64, _I32, _I32, _P, _P, C.POINTER(C.c_float), _P],
+    "svdq_quantize_weights_workspace": [_I64, _I64, _I32, _SZ],
+    "svdq_quantize_weights": [_P, _I32, _P, _I64, _I64, _I32, _I32, _I32, C.c_float, _P, _P, _LP,
+                              _P, C.c_size_t, _P],
+    "svdq_lora_fuse": [_LP, _P, _P, _I32, _I32, C.c_float, _LP, _P],
+    "svdq_debug_int4_group_accum": [_P, _P, _I64, _I64, _I64, _P, _P],
+    "svdq_debug_codec": [_P, _P, _I64, _I32, _P],
+}
+for _name, _args in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = C.c_int
+_lib.svdq_status_string.argtypes = [C.c_int]
+_lib.svdq_status_string.restype = C.c_char_p
+_lib.svdq_last_error.argtypes = []
+_lib.svdq_last_error.restype = C.c_char_p
+_lib.svdq_launch_count.argtypes = []
+_lib.svdq_launch_count.restype = C.c_uint64
+_lib.svdq_version.argtypes = []
+_lib.svdq_version.restype = C.c_int32
+
+
+def _check(status: int, where: str):
+    if status != SVDQ_OK:
+        raise SvdqError(status, where)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def lib():
+    return _lib
+
+
+# ---------------------------------------------------------------- misc
+def svdq_status_string(status: int) -> str:
+    return _lib.svdq_status_string(status).decode()
+
+
+def svdq_last_error() -> str:
+    return _lib.svdq_last_error().decode()
+
+
+def svdq_launch_count() -> int:
+    return int(_lib.svdq_launch_count())
+
+
+def svdq_version() -> int:
+    return int(_lib.svdq_version())
+
+
+def svdq_act_buffer_sizes(fmt: str, M: int, K: int, rank: int):
+    a, b, c = C.c_size_t(), C.c_size_t(), C.c_size_t()
+    _check(_lib.svdq_act_buffer_sizes(FMT[fmt], M, K, rank, C.byref(a), C.byref(b), C.byref(c)),
+           "svdq_act_buffer_sizes")
+    return a.value, b.value, c.value
+
+
+def svdq_weight_buffer_sizes(fmt: str, K: int, N: int, rank: int):
+    v = [C.c_size_t() for _ in range(4)]
+    _check(_lib.svdq_weight_buffer_sizes(FMT[fmt], K, N, rank, *[C.byref(x) for x in v]),
+           "svdq_weight_buffer_sizes")
+    return tuple(x.value for x in v)
+
+
+# ---------------------------------------------------------------- layer view
+class QuantizedLinear:
+    """Owns the device buffers of one layer and the svdq_linear view of them."""
+
+    def __init__(self, fmt: str, K: int, N: int, rank: int, w_codes, w_scales, lambda_inv, l1s, l2s,
+                 bias=None, scale_dtype: str = "bf16", gs_w: float = 1.0, gs_x: float = 1.0):
+        self.fmt, self.K, self.N, self.rank = fmt, K, N, rank
+        self.w_codes, self.w_scales, self.lambda_inv = w_codes, w_scales, lambda_inv
+        self.l1s, self.l2s, self.bias = l1s, l2s, bias
+        self.scale_dtype = scale_dtype
+        self.gs_w, self.gs_x = float(gs_w), float(gs_x)
+        self._sync_view()
+
+    def _sync_view(self):
+        bias_dt = DTYPE_OF_TORCH[self.bias.dtype] if self.bias is not None else "bf16"
+        self.view = svdq_linear(
+            FMT[self.fmt], self.rank, self.K, self.N, _ptr(self.w_codes), _ptr(self.w_scales),
+            _ptr(self.lambda_inv), _ptr(self.l1s), _ptr(self.l2s), _ptr(self.bias),
+            DTYPE[self.scale_dtype], DTYPE[bias_dt], self.gs_w, self.gs_x)
+
+    @property
+    def ref(self):
+        return C.byref(self.view)
+
+    @classmethod
+    def empty(cls, fmt, K, N, rank, device="cuda", scale_dtype="bf16", bias=None, gs_x=1.0):
+        codes_b, scales_b, l1s_b, l2s_b = svdq_weight_buffer_sizes(fmt, K, N, rank)
+        u8 = dict(dtype=torch.uint8, device=device)
+        return cls(fmt, K, N, rank,
+                   torch.empty(codes_b, **u8), torch.empty(scales_b, **u8),
+                   torch.empty(K, dtype=torch.float32, device=device),
+                   torch.empty(max(l1s_b // 2, 8), dtype=torch.int16, device=device),
+                   torch.empty(max(l2s_b // 2, 8), dtype=torch.int16, device=device),
+                   bias, scale_dtype, 1.0, gs_x)
+
+    def forward(self, X, out_dtype=None, stream=None):
+        return svdq_linear_forward(self, X, out_dtype=out_dtype, stream=stream)
+
+    __call__ = forward
+
+
+# ---------------------------------------------------------------- hot path
+def svdq_quantize_act_lowrank_down(layer: QuantizedLinear, X, xq=None, xs=None, xl1=None, stream=None):
+    """K1.  X: [M, K] bf16/fp16 CUDA tensor (row pitch X.stride(0))."""
+    M = X.shape[0]
+    bq, bs, bl = svdq_act_buffer_sizes(layer.fmt, M, layer.K, layer.rank)
+    dev = X.device
+    if xq is None:
+        xq = torch.empty(bq, dtype=torch.uint8, device=dev)
+    if xs is None:
+        xs = torch.empty(bs, dtype=torch.uint8, device=dev)
+    if xl1 is None and layer.rank:
+        xl1 = torch.empty(bl // 2, dtype=torch.int16, device=dev)
+    _check(_lib.svdq_quantize_act_lowrank_down(
+        layer.ref, _ptr(X), DTYPE[DTYPE_OF_TORCH[X.dtype]], M, X.stride(0), _ptr(xq), _ptr(xs),
+        _ptr(xl1), _stream(stream)), "svdq_quantize_act_lowrank_down")
+    return xq, xs, xl1
+
+
+def svdq_gemm_w4a4_lowrank_up(layer: QuantizedLinear, xq, xs, xl1, M: int, Y=None,
+                              out_dtype=torch.bfloat16, stream=None):
+    """K2.  Returns Y [M, N]."""
+    if Y is None:
+        Y = torch.empty(M, layer.N, dtype=out_dtype, device=xq.device)
+    _check(_lib.svdq_gemm_w4a4_lowrank_up(
+        layer.ref, _ptr(xq), _ptr(xs), _ptr(xl1), M, _ptr(Y), DTYPE[DTYPE_OF_TORCH[Y.dtype]],
+        Y.stride(0), _stream(stream)), "svdq_gemm_w4a4_lowrank_up")
+    return Y
+
+
+def forward_workspace_bytes(layer: QuantizedLinear, M: int) -> int:
+    up = lambda b: (b + 255) // 256 * 256
+    return sum(up(b) for b in svdq_act_buffer_sizes(layer.fmt, M, layer.K, layer.rank))
+
+
+def svdq_linear_forward(layer: QuantizedLinear, X, Y=None, out_dtype=None, ws=None, stream=None):
+    M = X.shape[0]
+    if Y is None:
+        Y = torch.empty(M, layer.N, dtype=out_dtype or X.dtype, device=X.device)
+    need = forward_workspace_bytes(layer, M)
+    if ws is None:
+        ws = torch.empty(need, dtype=torch.uint8, device=X.device)
+    _check(_lib.svdq_linear_forward(
+        layer.ref, _ptr(X), DTYPE[DTYPE_OF_TORCH[X.dtype]], M, X.stride(0), _ptr(Y),
+        DTYPE[DTYPE_OF_TORCH[Y.dtype]], Y.stride(0), _ptr(ws), ws.numel(), _stream(stream)),
+        "svdq_linear_forward")
+    return Y
+
+
+# ---------------------------------------------------------------- offline
+def svdq_quantize_residual(R, fmt: str, scale_dtype: str = "bf16", gs_w: float = 0.0,
+                           codes=None, scales=None, stream=None):
+    """R: [K, N] fp32 CUDA tensor (paper layout).  Returns (codes, scales, gs_w)."""
+    K, N = R.shape
+    cb, sb, _, _ = svdq_weight_buffer_sizes(fmt, K, N, 0)
+    if codes is None:
+        codes = torch.empty(cb, dtype=torch.uint8, device=R.device)
+    if scales is None:
+        scales = torch.empty(sb, dtype=torch.uint8, device=R.device)
+    g = C.c_float(gs_w)
+    _check(_lib.svdq_quantize_residual(_ptr(R), K, N, FMT[fmt], DTYPE[scale_dtype], _ptr(codes),
+                                       _ptr(scales), C.byref(g), _stream(stream)),
+           "svdq_quantize_residual")
+    return codes, scales, g.value
+
+
+def svdq_quantize_weights_workspace(K: int, N: int, rank: int) -> int:
+    wsb = C.c_size_t()
+    _check(_lib.svdq_quantize_weights_workspace(K, N, rank, C.byref(wsb)),
+           "svdq_quantize_weights_workspace")
+    return wsb.value
+
+
+def svdq_quantize_weights(W, lam, rank: int, fmt: str, scale_dtype: str = "bf16", gs_x: float = 1.0,
+                          L1=None, L2=None, bias=None, stream=None) -> QuantizedLinear:
+    """W: [K, N] CUDA tensor (bf16/fp16/fp32), lam: [K] fp32."""
+    K, N = W.shape
+    layer = QuantizedLinear.empty(fmt, K, N, rank, device=W.device, scale_dtype=scale_dtype,
+                                  bias=bias, gs_x=gs_x)
+    ws = torch.empty(svdq_quantize_weights_workspace(K, N, rank), dtype=torch.uint8, device=W.device)
+    W = W.contiguous()
+    lam = lam.contiguous().float()
+    _check(_lib.svdq_quantize_weights(
+        _ptr(W), DTYPE[DTYPE_OF_TORCH[W.dtype]], _ptr(lam), K, N, rank, FMT[fmt], DTYPE[scale_dtype],
+        gs_x, _ptr(L1), _ptr(L2), layer.ref, _ptr(ws), ws.numel(), _stream(stream)),
+        "svdq_quantize_weights")
+    layer.gs_w = layer.view.gs_w
+    layer.gs_x = layer.view.gs_x
+    del ws
+    return layer
+
+
+def svdq_lora_fuse(layer: QuantizedLinear, A, B, scale: float = 1.0, stream=None) -> QuantizedLinear:
+    """A: [K, r_l], B: [r_l, N] CUDA tensors (bf16/fp16/fp32).  Returns a new layer of rank r + r_l
+    sharing the residual codes / scales / lambda with `layer`."""
+    r_l = A.shape[1]
+    r1 = layer.rank + r_l
+    out = QuantizedLinear(layer.fmt, layer.K, layer.N, r1, layer.w_codes, layer.w_scales,
+                          layer.lambda_inv,
+                          torch.empty(r1 * layer.K, dtype=torch.int16, device=A.device),
+                          torch.empty(layer.N * r1, dtype=torch.int16, device=A.device),
+                          layer.bias, layer.scale_dtype, layer.gs_w, layer.gs_x)
+    A = A.contiguous()
+    B = B.contiguous()
+    if B.dtype != A.dtype:
+        raise ValueError("A and B must share a dtype")
+    _check(_lib.svdq_lora_fuse(layer.ref, _ptr(A), _ptr(B), DTYPE[DTYPE_OF_TORCH[A.dtype]], r_l,
+                               scale, out.ref, _stream(stream)), "svdq_lora_fuse")
+    return out
+
+
+# ---------------------------------------------------------------- test hooks
+def svdq_debug_int4_group_accum(xq, wq, M: int, N: int, K: int, stream=None):
+    acc = torch.empty((K // 64, M, N), dtype=torch.int32, device=xq.device)
+    _check(_lib.svdq_debug_int4_group_accum(_ptr(xq), _ptr(wq), M, N, K, _ptr(acc), _stream(stream)),
+           "svdq_debug_int4_group_accum")
+    return acc
+
+
+def svdq_debug_codec(x, kind: int, stream=None):
+    """kind 0: E2M1x2 bytes of consecutive pairs; kind 1: E4M3 byte per value."""
+    x = x.contiguous().float()
+    n = x.numel() // 2 if kind == 0 else x.numel()
+    out = torch.empty(n, dtype=torch.uint8, device=x.device)
+    _check(_lib.svdq_debug_codec(_ptr(x), _ptr(out), n, kind, _stream(stream)), "svdq_debug_codec")
+    return out

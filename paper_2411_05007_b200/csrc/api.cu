@@ -1,0 +1,556 @@
+// api.cu -- the extern "C" boundary declared in include/svdq.h: host-side
+// validation, TMA descriptor construction, dispatch, error reporting.
+#include <cublas_v2.h>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cusolverDn.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/svdq.h"
+#include "formats.cuh"
+#include "k1_launch.h"
+
+using namespace svdq;
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local uint64_t g_launches = 0;
+
+svdq_status fail(svdq_status s, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+svdq_status cuda_fail(cudaError_t e, const char *where) {
+  return fail(SVDQ_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define SVDQ_CUDA(call, where)                         \
+  do {                                                 \
+    cudaError_t e_ = (call);                           \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+svdq_status check_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(SVDQ_ERR_UNSUPPORTED, "no CUDA device");
+  static int cached[64];   // 0 unknown, 1 ok, 2 bad
+  if (dev < 64 && cached[dev] == 1) return SVDQ_OK;
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0)
+    return fail(SVDQ_ERR_UNSUPPORTED, "device %d is sm_%d%d; libsvdq is built for sm_100a", dev,
+                major, minor);
+  if (dev < 64) cached[dev] = 1;
+  return SVDQ_OK;
+}
+
+int64_t sf_bytes(int64_t rows, int64_t K) { return ((rows + 127) / 128) * 128 * (K / 16); }
+
+svdq_status check_linear(const svdq_linear *L, bool need_weights) {
+  if (!L) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null svdq_linear");
+  if (L->fmt != SVDQ_FMT_NVFP4 && L->fmt != SVDQ_FMT_INT4)
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad format %d", L->fmt);
+  if (L->K <= 0 || L->K % 64) return fail(SVDQ_ERR_SHAPE, "K=%lld must be a positive multiple of 64", (long long)L->K);
+  if (L->N <= 0 || L->N % 16) return fail(SVDQ_ERR_SHAPE, "N=%lld must be a positive multiple of 16", (long long)L->N);
+  if (L->rank < 0 || L->rank > 128 || L->rank % 16)
+    return fail(SVDQ_ERR_RANK, "rank=%d must be a multiple of 16 in [0, 128]", L->rank);
+  if (L->fmt == SVDQ_FMT_INT4 && L->scale_dtype != SVDQ_BF16 && L->scale_dtype != SVDQ_FP16)
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "INT4 scale_dtype must be BF16 or FP16");
+  if (L->fmt == SVDQ_FMT_NVFP4 && !(L->gs_x > 0.f))
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "gs_x must be > 0");
+  if (!L->lambda_inv) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null lambda_inv");
+  if (L->rank > 0 && (!L->l1s || !L->l2s)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null l1s/l2s with rank > 0");
+  if (!aligned16(L->lambda_inv) || !aligned16(L->l1s) || !aligned16(L->l2s))
+    return fail(SVDQ_ERR_ALIGNMENT, "lambda_inv / l1s / l2s must be 16-byte aligned");
+  if (need_weights) {
+    if (!L->w_codes || !L->w_scales) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null weight codes/scales");
+    if (!aligned16(L->w_codes) || !aligned16(L->w_scales))
+      return fail(SVDQ_ERR_ALIGNMENT, "weight codes/scales must be 16-byte aligned");
+    if (L->bias && L->bias_dtype != SVDQ_BF16 && L->bias_dtype != SVDQ_FP16 && L->bias_dtype != SVDQ_FP32)
+      return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad bias dtype");
+    if (L->fmt == SVDQ_FMT_NVFP4 && !(L->gs_w > 0.f))
+      return fail(SVDQ_ERR_INVALID_ARGUMENT, "gs_w must be > 0");
+  }
+  return SVDQ_OK;
+}
+
+// ---------------------------------------------------------------- TMA descriptors
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2D row-major tensor [rows][cols] of `dt`, row pitch `pitch_bytes`, box {box_cols, box_rows},
+// 128-byte swizzle.
+svdq_status make_map(CUtensorMap *map, const void *base, CUtensorMapDataType dt, int64_t cols,
+                     int64_t rows, int64_t pitch_bytes, uint32_t box_cols, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(SVDQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch_bytes)};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, dt, 2, const_cast<void *>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SVDQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return SVDQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *svdq_status_string(svdq_status s) {
+  switch (s) {
+    case SVDQ_OK: return "SVDQ_OK";
+    case SVDQ_ERR_INVALID_ARGUMENT: return "SVDQ_ERR_INVALID_ARGUMENT";
+    case SVDQ_ERR_SHAPE: return "SVDQ_ERR_SHAPE";
+    case SVDQ_ERR_RANK: return "SVDQ_ERR_RANK";
+    case SVDQ_ERR_ALIGNMENT: return "SVDQ_ERR_ALIGNMENT";
+    case SVDQ_ERR_UNSUPPORTED: return "SVDQ_ERR_UNSUPPORTED";
+    case SVDQ_ERR_NONFINITE: return "SVDQ_ERR_NONFINITE";
+    case SVDQ_ERR_CUDA: return "SVDQ_ERR_CUDA";
+    case SVDQ_ERR_WORKSPACE: return "SVDQ_ERR_WORKSPACE";
+  }
+  return "SVDQ_ERR_UNKNOWN";
+}
+
+const char *svdq_last_error(void) { return g_err; }
+uint64_t svdq_launch_count(void) { return g_launches; }
+int32_t svdq_version(void) { return 1; }
+
+svdq_status svdq_act_buffer_sizes(int32_t fmt, int64_t M, int64_t K, int32_t rank, size_t *xq,
+                                  size_t *xs, size_t *xl1) {
+  if (!xq || !xs || !xl1) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null output");
+  if (fmt != SVDQ_FMT_NVFP4 && fmt != SVDQ_FMT_INT4) return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad format");
+  if (M < 1) return fail(SVDQ_ERR_SHAPE, "M must be >= 1");
+  if (K <= 0 || K % 64) return fail(SVDQ_ERR_SHAPE, "K must be a positive multiple of 64");
+  if (rank < 0 || rank > 128 || rank % 16) return fail(SVDQ_ERR_RANK, "bad rank");
+  *xq = static_cast<size_t>(M * K / 2);
+  *xs = fmt == SVDQ_FMT_NVFP4 ? static_cast<size_t>(sf_bytes(M, K)) : static_cast<size_t>(M * (K / 64) * 2);
+  *xl1 = static_cast<size_t>(M) * rank * 2;
+  return SVDQ_OK;
+}
+
+svdq_status svdq_weight_buffer_sizes(int32_t fmt, int64_t K, int64_t N, int32_t rank, size_t *codes,
+                                     size_t *scales, size_t *l1s, size_t *l2s) {
+  if (!codes || !scales || !l1s || !l2s) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null output");
+  if (fmt != SVDQ_FMT_NVFP4 && fmt != SVDQ_FMT_INT4) return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad format");
+  if (K <= 0 || K % 64) return fail(SVDQ_ERR_SHAPE, "K must be a positive multiple of 64");
+  if (N <= 0 || N % 16) return fail(SVDQ_ERR_SHAPE, "N must be a positive multiple of 16");
+  if (rank < 0 || rank > 128 || rank % 16) return fail(SVDQ_ERR_RANK, "bad rank");
+  *codes = static_cast<size_t>(N * K / 2);
+  *scales = fmt == SVDQ_FMT_NVFP4 ? static_cast<size_t>(sf_bytes(N, K)) : static_cast<size_t>(N * (K / 64) * 2);
+  *l1s = static_cast<size_t>(rank) * K * 2;
+  *l2s = static_cast<size_t>(N) * rank * 2;
+  return SVDQ_OK;
+}
+
+svdq_status svdq_quantize_act_lowrank_down(const svdq_linear *L, const void *X, int32_t x_dtype,
+                                           int64_t M, int64_t ldx, uint8_t *xq, uint8_t *xs,
+                                           uint16_t *xl1, void *stream) {
+  svdq_status st = check_linear(L, false);
+  if (st != SVDQ_OK) return st;
+  if (!X || !xq || !xs || (L->rank > 0 && !xl1)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null buffer");
+  if (x_dtype != SVDQ_BF16 && x_dtype != SVDQ_FP16)
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "X dtype must be BF16 or FP16");
+  if (M < 1) return fail(SVDQ_ERR_SHAPE, "M must be >= 1");
+  if (ldx < L->K) return fail(SVDQ_ERR_SHAPE, "ldx < K");
+  if (ldx % 8 || !aligned16(X) || !aligned16(xq) || !aligned16(xs) || (xl1 && !aligned16(xl1)))
+    return fail(SVDQ_ERR_ALIGNMENT, "X / ldx / outputs must be 16-byte aligned");
+  if ((st = check_device()) != SVDQ_OK) return st;
+  K1Params p{};
+  p.fmt = L->fmt == SVDQ_FMT_NVFP4 ? 0 : 1;
+  p.x_bf16 = x_dtype == SVDQ_BF16;
+  p.scale_bf16 = L->scale_dtype == SVDQ_BF16;
+  p.X = X;
+  p.ldx = ldx;
+  p.M = M;
+  p.Mpad = ((M + 127) / 128) * 128;
+  p.K = L->K;
+  p.lam_inv = L->lambda_inv;
+  p.l1s = L->l1s;
+  p.rank = L->rank;
+  p.gs_x = L->fmt == SVDQ_FMT_NVFP4 ? L->gs_x : 1.0f;
+  p.xq = xq;
+  p.xs = xs;
+  p.xl1 = xl1;
+  cudaError_t e = launch_k1(p, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "K1 launch");
+  ++g_launches;
+  return SVDQ_OK;
+}
+
+svdq_status svdq_gemm_w4a4_lowrank_up(const svdq_linear *L, const uint8_t *xq, const uint8_t *xs,
+                                      const uint16_t *xl1, int64_t M, void *Y, int32_t y_dtype,
+                                      int64_t ldy, void *stream) {
+  svdq_status st = check_linear(L, true);
+  if (st != SVDQ_OK) return st;
+  if (!xq || !xs || !Y || (L->rank > 0 && !xl1)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null buffer");
+  if (y_dtype != SVDQ_BF16 && y_dtype != SVDQ_FP16 && y_dtype != SVDQ_FP32)
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad Y dtype");
+  if (M < 1) return fail(SVDQ_ERR_SHAPE, "M must be >= 1");
+  if (ldy < L->N) return fail(SVDQ_ERR_SHAPE, "ldy < N");
+  if (ldy % 8 || !aligned16(Y) || !aligned16(xq) || !aligned16(xs) || (xl1 && !aligned16(xl1)))
+    return fail(SVDQ_ERR_ALIGNMENT, "Y / ldy / inputs must be 16-byte aligned");
+  if ((st = check_device()) != SVDQ_OK) return st;
+  const int64_t K = L->K, N = L->N;
+  K2Params p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.Npad = ((N + 127) / 128) * 128;
+  p.rank = L->rank;
+  p.sfa = xs;
+  p.sfb = L->w_scales;
+  p.xq = xq;
+  p.wq = L->w_codes;
+  p.bias = L->bias;
+  p.bias_dtype = L->bias_dtype;
+  p.Y = Y;
+  p.y_dtype = y_dtype;
+  p.ldy = ldy;
+  p.scale_bf16 = L->scale_dtype == SVDQ_BF16;
+  p.alpha = L->fmt == SVDQ_FMT_NVFP4 ? L->gs_x * L->gs_w : 1.0f;
+  K2Maps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  const int BN = L->fmt == SVDQ_FMT_NVFP4 ? k2_nvfp4_bn(M, N) : kInt4BN;
+  if (L->fmt == SVDQ_FMT_NVFP4) {
+    if ((st = make_map(&maps.a, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, M, K / 2, 128, 128)) != SVDQ_OK) return st;
+    if ((st = make_map(&maps.b, L->w_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, N, K / 2, 128, BN)) != SVDQ_OK) return st;
+  }
+  if (L->rank > 0) {
+    if ((st = make_map(&maps.xl1, xl1, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->rank, M, L->rank * 2, 64, 128)) != SVDQ_OK) return st;
+    if ((st = make_map(&maps.l2, L->l2s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->rank, N, L->rank * 2, 64, BN)) != SVDQ_OK) return st;
+  }
+  cudaError_t e = L->fmt == SVDQ_FMT_NVFP4 ? launch_k2_nvfp4(maps, p, static_cast<cudaStream_t>(stream))
+                                           : launch_k2_int4(maps, p, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported) return fail(SVDQ_ERR_UNSUPPORTED, "INT4 GEMM not built");
+  if (e != cudaSuccess) return cuda_fail(e, "K2 launch");
+  ++g_launches;
+  return SVDQ_OK;
+}
+
+svdq_status svdq_linear_forward(const svdq_linear *L, const void *X, int32_t x_dtype, int64_t M,
+                                int64_t ldx, void *Y, int32_t y_dtype, int64_t ldy, void *ws,
+                                size_t ws_bytes, void *stream) {
+  svdq_status st = check_linear(L, true);
+  if (st != SVDQ_OK) return st;
+  size_t bq, bs, bl;
+  if ((st = svdq_act_buffer_sizes(L->fmt, M, L->K, L->rank, &bq, &bs, &bl)) != SVDQ_OK) return st;
+  auto up = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
+  if (!ws || ws_bytes < up(bq) + up(bs) + up(bl)) return fail(SVDQ_ERR_WORKSPACE, "workspace too small");
+  uint8_t *xq = static_cast<uint8_t *>(ws);
+  uint8_t *xs = xq + up(bq);
+  uint16_t *xl1 = reinterpret_cast<uint16_t *>(xs + up(bs));
+  if ((st = svdq_quantize_act_lowrank_down(L, X, x_dtype, M, ldx, xq, xs, L->rank ? xl1 : nullptr, stream)) != SVDQ_OK)
+    return st;
+  return svdq_gemm_w4a4_lowrank_up(L, xq, xs, L->rank ? xl1 : nullptr, M, Y, y_dtype, ldy, stream);
+}
+
+svdq_status svdq_quantize_residual(const float *R, int64_t K, int64_t N, int32_t fmt, int32_t scale_dtype,
+                                   uint8_t *codes, uint8_t *scales, float *gs_w, void *stream) {
+  if (!R || !codes || !scales || !gs_w) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null pointer");
+  if (fmt != SVDQ_FMT_NVFP4 && fmt != SVDQ_FMT_INT4) return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad format");
+  if (K <= 0 || K % 64) return fail(SVDQ_ERR_SHAPE, "K must be a positive multiple of 64");
+  if (N <= 0 || N % 16) return fail(SVDQ_ERR_SHAPE, "N must be a positive multiple of 16");
+  if (fmt == SVDQ_FMT_INT4 && scale_dtype != SVDQ_BF16 && scale_dtype != SVDQ_FP16)
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "INT4 scale dtype must be BF16 or FP16");
+  if (!aligned16(codes) || !aligned16(scales) || !aligned16(R)) return fail(SVDQ_ERR_ALIGNMENT, "unaligned");
+  svdq_status st = check_device();
+  if (st != SVDQ_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  float gs = 1.0f;
+  if (fmt == SVDQ_FMT_NVFP4) {
+    if (*gs_w > 0.f) {
+      gs = *gs_w;
+    } else {
+      unsigned int *d_amax = nullptr;
+      SVDQ_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&d_amax), sizeof(unsigned int), s), "alloc");
+      SVDQ_CUDA(launch_absmax(R, K * N, d_amax, s), "absmax");
+      ++g_launches;
+      unsigned int bits = 0;
+      SVDQ_CUDA(cudaMemcpyAsync(&bits, d_amax, sizeof(bits), cudaMemcpyDeviceToHost, s), "copy");
+      SVDQ_CUDA(cudaFreeAsync(d_amax, s), "free");
+      SVDQ_CUDA(cudaStreamSynchronize(s), "sync");
+      float amax;
+      std::memcpy(&amax, &bits, sizeof(amax));
+      volatile float div = 2688.0f;   // fl32(amax / 2688): one IEEE single division
+      gs = amax == 0.f ? 1.0f : amax / div;
+      *gs_w = gs;
+    }
+  } else {
+    *gs_w = 1.0f;
+  }
+  SVDQ_CUDA(launch_quantize_residual(R, K, N, fmt == SVDQ_FMT_NVFP4 ? 0 : 1, scale_dtype == SVDQ_BF16,
+                                     gs, codes, scales, s),
+            "quantize residual");
+  ++g_launches;
+  return SVDQ_OK;
+}
+
+// ---------------------------------------------------------------- offline weights
+namespace {
+struct WsLayout {
+  size_t what, gram, evals, E, sigma, l1_64, l2_64, r32, l1_32, l2_32, work, info, total;
+  int lwork;
+};
+size_t up256(size_t b) { return (b + 255) & ~static_cast<size_t>(255); }
+
+svdq_status ws_layout(int64_t K, int64_t N, int32_t rank, int lwork, WsLayout *w) {
+  const int64_t P = K < N ? K : N;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += up256(bytes); return o; };
+  w->what = take(static_cast<size_t>(K) * N * 8);
+  w->gram = take(static_cast<size_t>(P) * P * 8);
+  w->evals = take(static_cast<size_t>(P) * 8);
+  w->E = take(static_cast<size_t>(P) * (rank > 0 ? rank : 1) * 8);
+  w->sigma = take(static_cast<size_t>(rank > 0 ? rank : 1) * 8);
+  w->l1_64 = take(static_cast<size_t>(K) * (rank > 0 ? rank : 1) * 8);
+  w->l2_64 = take(static_cast<size_t>(N) * (rank > 0 ? rank : 1) * 8);
+  w->r32 = take(static_cast<size_t>(K) * N * 4);
+  w->l1_32 = take(static_cast<size_t>(K) * (rank > 0 ? rank : 1) * 4);
+  w->l2_32 = take(static_cast<size_t>(N) * (rank > 0 ? rank : 1) * 4);
+  w->work = take(static_cast<size_t>(lwork > 0 ? lwork : 1) * 8);
+  w->info = take(16);
+  w->total = off;
+  w->lwork = lwork;
+  return SVDQ_OK;
+}
+
+int syevd_lwork(int64_t P) {
+  cusolverDnHandle_t h;
+  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) return -1;
+  int lwork = 0;
+  cusolverStatus_t r = cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                                   static_cast<int>(P), nullptr, static_cast<int>(P),
+                                                   nullptr, &lwork);
+  cusolverDnDestroy(h);
+  return r == CUSOLVER_STATUS_SUCCESS ? lwork : -1;
+}
+}  // namespace
+
+svdq_status svdq_quantize_weights_workspace(int64_t K, int64_t N, int32_t rank, size_t *ws_bytes) {
+  if (!ws_bytes) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null output");
+  if (K <= 0 || K % 64 || N <= 0 || N % 16) return fail(SVDQ_ERR_SHAPE, "bad K/N");
+  if (rank < 0 || rank > 128 || rank % 16) return fail(SVDQ_ERR_RANK, "bad rank");
+  svdq_status st = check_device();
+  if (st != SVDQ_OK) return st;
+  const int64_t P = K < N ? K : N;
+  const int lwork = rank > 0 ? syevd_lwork(P) : 1;
+  if (lwork < 0) return fail(SVDQ_ERR_CUDA, "cusolver bufferSize failed");
+  WsLayout w;
+  ws_layout(K, N, rank, lwork, &w);
+  *ws_bytes = w.total;
+  return SVDQ_OK;
+}
+
+svdq_status svdq_quantize_weights(const void *W, int32_t w_dtype, const float *lambda, int64_t K,
+                                  int64_t N, int32_t rank, int32_t fmt, int32_t scale_dtype,
+                                  float gs_x, const float *L1_opt, const float *L2_opt,
+                                  svdq_linear *dst, void *ws, size_t ws_bytes, void *stream) {
+  if (!W || !lambda || !dst || !ws) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null pointer");
+  if (w_dtype != SVDQ_BF16 && w_dtype != SVDQ_FP16 && w_dtype != SVDQ_FP32)
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad W dtype");
+  if (fmt != SVDQ_FMT_NVFP4 && fmt != SVDQ_FMT_INT4) return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad format");
+  if (K <= 0 || K % 64 || N <= 0 || N % 16) return fail(SVDQ_ERR_SHAPE, "bad K/N");
+  if (rank < 0 || rank > 128 || rank % 16 || rank > (K < N ? K : N)) return fail(SVDQ_ERR_RANK, "bad rank");
+  if ((L1_opt == nullptr) != (L2_opt == nullptr)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "L1_opt and L2_opt go together");
+  if (!dst->w_codes || !dst->w_scales || !dst->lambda_inv || (rank > 0 && (!dst->l1s || !dst->l2s)))
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "dst buffers must be set");
+  if (fmt == SVDQ_FMT_NVFP4 && !(gs_x > 0.f)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "gs_x must be > 0");
+  svdq_status st = check_device();
+  if (st != SVDQ_OK) return st;
+  const int64_t P = K < N ? K : N;
+  const int lwork = (rank > 0 && !L1_opt) ? syevd_lwork(P) : 1;
+  if (lwork < 0) return fail(SVDQ_ERR_CUDA, "cusolver bufferSize failed");
+  WsLayout w;
+  ws_layout(K, N, rank, lwork, &w);
+  if (ws_bytes < w.total) return fail(SVDQ_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, w.total);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t *base = static_cast<uint8_t *>(ws);
+  double *What = reinterpret_cast<double *>(base + w.what);
+  double *G = reinterpret_cast<double *>(base + w.gram);
+  double *evals = reinterpret_cast<double *>(base + w.evals);
+  double *E = reinterpret_cast<double *>(base + w.E);
+  double *sigma = reinterpret_cast<double *>(base + w.sigma);
+  double *L1d = reinterpret_cast<double *>(base + w.l1_64);
+  double *L2d = reinterpret_cast<double *>(base + w.l2_64);
+  float *R32 = reinterpret_cast<float *>(base + w.r32);
+  float *L1f = reinterpret_cast<float *>(base + w.l1_32);
+  float *L2f = reinterpret_cast<float *>(base + w.l2_32);
+  double *work = reinterpret_cast<double *>(base + w.work);
+  int *info = reinterpret_cast<int *>(base + w.info);
+
+  float *lam_inv = const_cast<float *>(dst->lambda_inv);
+  SVDQ_CUDA(launch_lambda_inv(lambda, lam_inv, K, s), "lambda_inv");
+  SVDQ_CUDA(launch_smooth_weight64(W, w_dtype, lambda, K, N, What, s), "smooth W");
+  g_launches += 2;
+
+  cublasHandle_t hb = nullptr;
+  if (cublasCreate(&hb) != CUBLAS_STATUS_SUCCESS) return fail(SVDQ_ERR_CUDA, "cublasCreate");
+  cublasSetStream(hb, s);
+  cublasSetMathMode(hb, CUBLAS_DEFAULT_MATH);
+  svdq_status result = SVDQ_OK;
+  const double one = 1.0, zero = 0.0, mone = -1.0;
+  do {
+    if (rank > 0) {
+      if (L1_opt) {
+        if (launch_f32_to_f64(L1_opt, L1d, K * rank, s) != cudaSuccess ||
+            launch_f32_to_f64(L2_opt, L2d, static_cast<int64_t>(rank) * N, s) != cudaSuccess) {
+          result = fail(SVDQ_ERR_CUDA, "convert L1/L2");
+          break;
+        }
+      } else {
+        // Gram matrix of the smaller side (column-major view of row-major What is What^T, N x K)
+        if (N <= K) {
+          if (cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, (int)N, (int)K, &one, What, (int)N, &zero, G, (int)N) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "syrk"); break; }
+        } else {
+          if (cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, (int)K, (int)N, &one, What, (int)N, &zero, G, (int)K) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "syrk"); break; }
+        }
+        cusolverDnHandle_t hs = nullptr;
+        if (cusolverDnCreate(&hs) != CUSOLVER_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "cusolverDnCreate"); break; }
+        cusolverDnSetStream(hs, s);
+        cusolverStatus_t cs = cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)P, G, (int)P, evals, work, lwork, info);
+        cusolverDnDestroy(hs);
+        if (cs != CUSOLVER_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "syevd"); break; }
+        if (launch_eig_to_factors(G, evals, P, rank, E, sigma, s) != cudaSuccess) { result = fail(SVDQ_ERR_CUDA, "eig"); break; }
+        if (N <= K) {
+          // L2 = E^T (rows = right singular vectors); L1 = What E  (= U_r Sigma_r)
+          if (cublasDgeam(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)N, rank, &one, E, rank, &zero, E, (int)N, L2d, (int)N) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "geam"); break; }
+          if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, rank, (int)K, (int)N, &one, E, rank, What, (int)N, &zero, L1d, rank) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "gemm L1"); break; }
+        } else {
+          // L1 = E diag(sigma); L2 = diag(sigma)^-1 E^T What
+          if (cudaMemcpyAsync(L1d, E, static_cast<size_t>(K) * rank * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess) { result = fail(SVDQ_ERR_CUDA, "copy"); break; }
+          if (launch_scale_cols(L1d, K, rank, sigma, 0, 0, s) != cudaSuccess) { result = fail(SVDQ_ERR_CUDA, "scale"); break; }
+          if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, (int)N, rank, (int)K, &one, What, (int)N, E, rank, &zero, L2d, (int)N) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "gemm L2"); break; }
+          if (launch_scale_cols(L2d, rank, N, sigma, 1, 1, s) != cudaSuccess) { result = fail(SVDQ_ERR_CUDA, "scale"); break; }
+        }
+        g_launches += 3;
+      }
+      // R = W_hat - L1 L2  (in place on What; column-major: What^T -= L2^T L1^T)
+      if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)N, (int)K, rank, &mone, L2d, (int)N, L1d, rank, &one, What, (int)N) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "gemm R"); break; }
+    }
+    if (launch_f64_to_f32(What, R32, K * N, s) != cudaSuccess) { result = fail(SVDQ_ERR_CUDA, "R32"); break; }
+    ++g_launches;
+    float gs_w = 0.f;
+    if ((result = svdq_quantize_residual(R32, K, N, fmt, scale_dtype, const_cast<uint8_t *>(dst->w_codes),
+                                         const_cast<uint8_t *>(dst->w_scales), &gs_w, stream)) != SVDQ_OK)
+      break;
+    const float gx = fmt == SVDQ_FMT_NVFP4 ? gs_x : 1.0f;
+    const float alpha = fmt == SVDQ_FMT_NVFP4 ? gx * gs_w : 1.0f;
+    if (rank > 0) {
+      if (launch_f64_to_f32(L1d, L1f, K * rank, s) != cudaSuccess ||
+          launch_f64_to_f32(L2d, L2f, static_cast<int64_t>(rank) * N, s) != cudaSuccess ||
+          launch_derive_l1s(L1f, 2, lam_inv, 1.0f, K, rank, 0, const_cast<uint16_t *>(dst->l1s), s) != cudaSuccess ||
+          launch_derive_l2s(L2f, 2, N, rank, 0, rank, alpha, const_cast<uint16_t *>(dst->l2s), s) != cudaSuccess) {
+        result = fail(SVDQ_ERR_CUDA, "derive l1s/l2s");
+        break;
+      }
+      g_launches += 4;
+    }
+    dst->fmt = fmt;
+    dst->rank = rank;
+    dst->K = K;
+    dst->N = N;
+    dst->scale_dtype = fmt == SVDQ_FMT_INT4 ? scale_dtype : SVDQ_BF16;
+    dst->gs_w = gs_w;
+    dst->gs_x = gx;
+  } while (false);
+  cublasDestroy(hb);
+  if (result != SVDQ_OK) return result;
+  SVDQ_CUDA(cudaStreamSynchronize(s), "sync");
+  return SVDQ_OK;
+}
+
+svdq_status svdq_lora_fuse(const svdq_linear *src, const void *A, const void *B, int32_t ab_dtype,
+                           int32_t r_l, float scale, svdq_linear *dst, void *stream) {
+  svdq_status st = check_linear(src, false);
+  if (st != SVDQ_OK) return st;
+  if (!A || !B || !dst || !dst->l1s || !dst->l2s) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null pointer");
+  if (ab_dtype != SVDQ_BF16 && ab_dtype != SVDQ_FP16 && ab_dtype != SVDQ_FP32)
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad A/B dtype");
+  if (r_l <= 0 || r_l % 16 || src->rank + r_l > 128) return fail(SVDQ_ERR_RANK, "bad LoRA rank");
+  if (dst->l1s == src->l1s || dst->l2s == src->l2s)
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "dst l1s/l2s must not alias src");
+  if ((st = check_device()) != SVDQ_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int r0 = src->rank, r1 = src->rank + r_l;
+  const float alpha = src->fmt == SVDQ_FMT_NVFP4 ? src->gs_x * src->gs_w : 1.0f;
+  uint16_t *l1s = const_cast<uint16_t *>(dst->l1s);
+  uint16_t *l2s = const_cast<uint16_t *>(dst->l2s);
+  if (r0 > 0) {
+    SVDQ_CUDA(launch_copy_l1s_rows(src->l1s, src->K, r0, l1s, s), "copy l1s");
+    SVDQ_CUDA(launch_copy_l2s_cols(src->l2s, src->N, r0, r1, l2s, s), "copy l2s");
+    ++g_launches;
+  }
+  SVDQ_CUDA(launch_derive_l1s(A, ab_dtype, nullptr, scale, src->K, r_l, r0, l1s, s), "lora l1s");
+  SVDQ_CUDA(launch_derive_l2s(B, ab_dtype, src->N, r_l, r0, r1, alpha, l2s, s), "lora l2s");
+  g_launches += 2;
+  const uint16_t *nl1 = dst->l1s, *nl2 = dst->l2s;
+  *dst = *src;
+  dst->rank = r1;
+  dst->l1s = nl1;
+  dst->l2s = nl2;
+  return SVDQ_OK;
+}
+
+svdq_status svdq_debug_int4_group_accum(const uint8_t *xq, const uint8_t *wq, int64_t M, int64_t N,
+                                        int64_t K, int32_t *acc, void *stream) {
+  if (!xq || !wq || !acc) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null pointer");
+  if (M < 1 || K <= 0 || K % 64 || N <= 0 || N % 16) return fail(SVDQ_ERR_SHAPE, "bad shape");
+  svdq_status st = check_device();
+  if (st != SVDQ_OK) return st;
+  K2Params p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.Npad = N;
+  p.xq = xq;
+  p.wq = wq;
+  p.dbg_acc = acc;
+  p.alpha = 1.0f;
+  K2Maps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  cudaError_t e = launch_k2_int4(maps, p, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported) return fail(SVDQ_ERR_UNSUPPORTED, "INT4 GEMM not built");
+  if (e != cudaSuccess) return cuda_fail(e, "int4 debug launch");
+  ++g_launches;
+  return SVDQ_OK;
+}
+
+svdq_status svdq_debug_codec(const float *in, uint8_t *out, int64_t n, int32_t kind, void *stream) {
+  if (!in || !out) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null pointer");
+  if (n < 0 || (kind != 0 && kind != 1)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad n / kind");
+  svdq_status st = check_device();
+  if (st != SVDQ_OK) return st;
+  if (n == 0) return SVDQ_OK;
+  cudaError_t e = launch_codec(in, out, n, kind, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "codec launch");
+  ++g_launches;
+  return SVDQ_OK;
+}
+
+}  // extern "C"

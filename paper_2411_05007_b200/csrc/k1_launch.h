@@ -1,0 +1,73 @@
+// Internal launch interfaces between api.cu and the kernel translation units.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace svdq {
+
+struct K1Params {
+  int fmt;            // 0 NVFP4, 1 INT4
+  bool x_bf16;        // X dtype bf16 (else fp16)
+  bool scale_bf16;    // INT4 scale dtype bf16 (else fp16)
+  const void *X;
+  int64_t ldx, M, Mpad, K;
+  const float *lam_inv;
+  const uint16_t *l1s;
+  int rank;
+  float gs_x;
+  uint8_t *xq;
+  uint8_t *xs;
+  uint16_t *xl1;
+};
+cudaError_t launch_k1(const K1Params &p, cudaStream_t s);
+
+struct K2Params {
+  int64_t M, N, K, Npad;
+  int rank;
+  const uint8_t *sfa;     // NVFP4: activation scale factors (128x4 layout); INT4: [M][K/64]
+  const uint8_t *sfb;     // NVFP4: weight scale factors; INT4: [N][K/64]
+  const uint8_t *xq;      // INT4 path (cp.async staging)
+  const uint8_t *wq;
+  const void *bias;
+  int bias_dtype;         // 0 bf16, 1 fp16, 2 fp32
+  void *Y;
+  int y_dtype;            // 0 bf16, 1 fp16, 2 fp32
+  int64_t ldy;
+  float alpha;
+  int scale_bf16;         // INT4 scales
+  int32_t *dbg_acc;       // INT4 debug: per-group int32 accumulators [K/64][M][N]
+};
+struct K2Maps {
+  CUtensorMap a, b, xl1, l2;
+};
+cudaError_t launch_k2_nvfp4(const K2Maps &maps, const K2Params &p, cudaStream_t s);
+int k2_nvfp4_bn(int64_t M, int64_t N);   // N tile the NVFP4 GEMM will use
+constexpr int kInt4BN = 128;             // N tile of the INT4 GEMM
+cudaError_t launch_k2_int4(const K2Maps &maps, const K2Params &p, cudaStream_t s);
+
+// weight-side kernels (wprep.cu)
+cudaError_t launch_absmax(const float *R, int64_t n, unsigned int *out_bits, cudaStream_t s);
+cudaError_t launch_quantize_residual(const float *R, int64_t K, int64_t N, int fmt, bool scale_bf16,
+                                     float gs_w, uint8_t *codes, uint8_t *scales, cudaStream_t s);
+cudaError_t launch_codec(const float *in, uint8_t *out, int64_t n, int kind, cudaStream_t s);
+cudaError_t launch_lambda_inv(const float *lam, float *lam_inv, int64_t K, cudaStream_t s);
+cudaError_t launch_smooth_weight64(const void *W, int w_dtype, const float *lam, int64_t K, int64_t N,
+                                   double *What, cudaStream_t s);
+cudaError_t launch_f32_to_f64(const float *in, double *out, int64_t n, cudaStream_t s);
+cudaError_t launch_f64_to_f32(const double *in, float *out, int64_t n, cudaStream_t s);
+// l1s[row_offset + t][k] = bf16(fl32(m_k * v[k][t])), m_k = lam_inv[k] if given else `scale`
+cudaError_t launch_derive_l1s(const void *src, int src_dtype, const float *lam_inv, float scale,
+                              int64_t K, int r_src, int row_offset, uint16_t *l1s, cudaStream_t s);
+// l2s[n][col_offset + t] = bf16(fl32(v[t][n] / alpha)), l2s row pitch total_rank
+cudaError_t launch_derive_l2s(const void *src, int src_dtype, int64_t N, int r_src, int col_offset,
+                              int total_rank, float alpha, uint16_t *l2s, cudaStream_t s);
+cudaError_t launch_copy_l1s_rows(const uint16_t *src, int64_t K, int rows, uint16_t *dst, cudaStream_t s);
+cudaError_t launch_copy_l2s_cols(const uint16_t *src, int64_t N, int r_src, int r_dst, uint16_t *dst,
+                                 cudaStream_t s);
+cudaError_t launch_eig_to_factors(const double *V, const double *evals, int64_t P, int rank,
+                                  double *out_vecs, double *out_sigma, cudaStream_t s);
+cudaError_t launch_scale_cols(double *A, int64_t rows, int64_t cols, const double *sig, int invert,
+                              int by_row, cudaStream_t s);
+
+}  // namespace svdq

@@ -1,0 +1,80 @@
+"""K1 parity (svdq_quantize_act_lowrank_down through the C ABI) against the
+oracle: codes and scales bit-exact (including the 0x00 padding rows of the
+NVFP4 128x4 layout), xl1 within 1e-3 relative Frobenius of the oracle's fp64
+X L1s^T rounded to bf16."""
+import numpy as np
+import pytest
+
+from helpers import layer_from_ops, make_case, need_cuda, pack_act, rel_fro
+from oracle import formats as F
+from oracle import svdquant as S
+
+pytestmark = pytest.mark.gpu
+
+
+def run_k1(fmt, M, K, N, r, dt="bf16", seed=0, ldx_pad=0, gs_x=1.0):
+    need_cuda()
+    import torch
+    import paper_2411_05007_b200 as P
+    x, w, lam, ops = make_case(fmt, M, K, N, r, dt=dt, seed=seed, gs_x=gs_x)
+    dev = torch.device("cuda")
+    layer = layer_from_ops(P, ops, dev)
+    tdt = P.TORCH_DTYPE[dt]
+    Xfull = torch.zeros(M, K + ldx_pad, dtype=tdt, device=dev)
+    Xfull[:, :K] = torch.from_numpy(x).to(dev).to(tdt)
+    X = Xfull[:, :K]
+    xs_size = P.svdq_act_buffer_sizes(fmt, M, K, r)[1]
+    xs = torch.full((xs_size,), 0xEE, dtype=torch.uint8, device=dev)     # poison: padding must be written
+    xq, xs, xl1 = P.svdq_quantize_act_lowrank_down(layer, X, xs=xs)
+    torch.cuda.synchronize()
+    qa = S.quantize_activation(x, ops)
+    ref_xq, ref_xs = pack_act(fmt, qa, K)
+    got_xq = xq.cpu().numpy().reshape(M, K // 2)
+    got_xs = xs.cpu().numpy()
+    bad = np.argwhere(got_xq != ref_xq)
+    assert bad.size == 0, f"{len(bad)} code bytes differ, first at {bad[0]}"
+    bad = np.flatnonzero(got_xs != ref_xs.reshape(-1))
+    assert bad.size == 0, f"{bad.size} scale bytes differ, first at {bad[0]}"
+    if r:
+        got = F.bf16_from_bits(xl1.cpu().numpy().view(np.uint16).reshape(M, r))
+        ref = F.bf16_from_bits(qa.xl1_bits)
+        err = rel_fro(got, ref)
+        assert err <= 1e-3, err
+        assert rel_fro(got, qa.xl1_exact) <= 5e-3      # bf16 storage rounding only
+    return ops, qa
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+def test_k1_c1(fmt):
+    run_k1(fmt, 256, 512, 512, 16)
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+@pytest.mark.parametrize("M", [1, 127, 129, 300])
+def test_k1_ragged_rows(fmt, M):
+    run_k1(fmt, M, 256, 64, 16, seed=M)
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+@pytest.mark.parametrize("r", [0, 32, 48, 64, 80, 128])
+def test_k1_ranks(fmt, r):
+    run_k1(fmt, 160, 1152, 128 if r <= 128 else r, r, seed=r)
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+def test_k1_fp16_and_pitch(fmt):
+    run_k1(fmt, 200, 640, 128, 32, dt="fp16", ldx_pad=64, seed=3)
+
+
+def test_k1_k64_minimal():
+    run_k1("nvfp4", 33, 64, 16, 16)
+
+
+def test_k1_nvfp4_static_gs():
+    run_k1("nvfp4", 128, 512, 64, 16, gs_x=0.125, seed=9)
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+def test_k1_flux_qkv_full(fmt):
+    """BASELINE config C4 activation shape (M=4608, K=3072, r=32), bit-exact at full size."""
+    run_k1(fmt, 4608, 3072, 64, 32, seed=4)

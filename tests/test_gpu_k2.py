@@ -1,0 +1,116 @@
+"""K2 parity (svdq_gemm_w4a4_lowrank_up through the C ABI) given the
+oracle's quantized operands: Y within 1e-3 relative Frobenius of the oracle's
+fp64 result rounded to the output dtype (reading Q17).
+Full-size shapes compare sampled rows the oracle computes one by one."""
+import numpy as np
+import pytest
+
+from helpers import layer_from_ops, make_case, need_cuda, pack_act, rel_fro, to_dev
+from oracle import svdquant as S
+
+pytestmark = pytest.mark.gpu
+
+
+def _subset(qa, rows):
+    return S.QuantAct(qa.codes[rows], qa.scales[rows], qa.xl1_bits[rows], qa.xl1_exact[rows])
+
+
+def run_k2(fmt, M, K, N, r, dt="bf16", out="bf16", seed=0, with_bias=True, sample=None, tol=1e-3):
+    need_cuda()
+    import torch
+    import paper_2411_05007_b200 as P
+    x, w, lam, ops = make_case(fmt, M, K, N, r, dt=dt, seed=seed, with_bias=with_bias)
+    dev = torch.device("cuda")
+    layer = layer_from_ops(P, ops, dev, bias_dtype=dt)
+    qa = S.quantize_activation(x, ops)
+    xq, xs = pack_act(fmt, qa, K)
+    xl1 = to_dev(qa.xl1_bits.view(np.int16).reshape(-1), dev) if r else None
+    try:
+        Y = P.svdq_gemm_w4a4_lowrank_up(layer, to_dev(xq.reshape(-1), dev), to_dev(xs.reshape(-1), dev),
+                                        xl1, M, out_dtype=P.TORCH_DTYPE[out])
+    except P.SvdqError as e:
+        if e.status == 5 and fmt == "int4":
+            pytest.skip("INT4 GEMM not built")
+        raise
+    torch.cuda.synchronize()
+    y = Y.float().cpu().numpy()
+    assert np.all(np.isfinite(y))
+    rows = np.arange(M) if sample is None else np.unique(np.concatenate(
+        [np.random.default_rng(seed).choice(M, sample, replace=False), [0, M - 1]]))
+    y_ref = S.round_output(S.gemm_reference(_subset(qa, rows), ops), out)
+    err = rel_fro(y[rows], y_ref)
+    assert err <= tol, f"rel fro err {err:.3e}"
+    exact = np.mean(y[rows] == y_ref)
+    return err, exact
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+def test_k2_c1(fmt):
+    err, exact = run_k2(fmt, 256, 512, 512, 16)
+    assert exact > 0.9         # fp32 accumulation order only flips rare output roundings
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+@pytest.mark.parametrize("M,N", [(1, 64), (129, 144), (300, 400), (127, 16)])
+def test_k2_ragged(fmt, M, N):
+    run_k2(fmt, M, 256, N, 16, seed=M + N)
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+@pytest.mark.parametrize("r", [0, 48, 64, 128])
+def test_k2_ranks(fmt, r):
+    run_k2(fmt, 200, 512, 256, r, seed=r)
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+@pytest.mark.parametrize("K", [64, 192, 1152])
+def test_k2_k_tails(fmt, K):
+    run_k2(fmt, 130, K, 128 if K > 64 else 64, 16, seed=K)
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+@pytest.mark.parametrize("out", ["fp16", "fp32"])
+def test_k2_out_dtypes(fmt, out):
+    run_k2(fmt, 256, 640, 192, 32, dt="fp16", out=out, seed=5)
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+def test_k2_no_bias(fmt):
+    run_k2(fmt, 96, 256, 128, 16, with_bias=False, seed=6)
+
+
+def test_k2_nvfp4_wide_tiles():
+    """Enough 128x256 tiles to select the BN = 256 kernel."""
+    run_k2("nvfp4", 2048, 512, 2560, 32, seed=7, sample=96)
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+def test_k2_flux_qkv_full(fmt):
+    """BASELINE config C4, FLUX.1 qkv: M=4608, K=3072, N=9216, r=32 (sampled rows)."""
+    run_k2(fmt, 4608, 3072, 9216, 32, seed=8, sample=48)
+
+
+def test_int4_group_accumulators_bit_exact():
+    """svdq_debug_int4_group_accum (same kind::i8 path as K2) vs the oracle's exact int64."""
+    need_cuda()
+    import torch
+    import paper_2411_05007_b200 as P
+    from oracle import formats as F
+    rng = np.random.default_rng(3)
+    M, N, K = 200, 144, 384
+    qa = rng.integers(-7, 8, (M, K))
+    qb = rng.integers(-7, 8, (N, K))
+    qa[0, :] = 7
+    qb[0, :] = 7                # extreme group sums: 64 * 49
+    qb[1, :] = -7
+    dev = torch.device("cuda")
+    try:
+        acc = P.svdq_debug_int4_group_accum(to_dev(F.pack_nibbles(F.int4_to_nibble(qa)).reshape(-1), dev),
+                                            to_dev(F.pack_nibbles(F.int4_to_nibble(qb)).reshape(-1), dev),
+                                            M, N, K)
+    except P.SvdqError as e:
+        if e.status == 5:
+            pytest.skip("INT4 GEMM not built")
+        raise
+    ref = S.int4_group_accum(qa, qb)
+    np.testing.assert_array_equal(acc.cpu().numpy(), ref)
