@@ -1,0 +1,433 @@
+"""Benchmark of the fused W4A4 + low-rank linear (BASELINE.json metric:
+"fused W4A4+low-rank linear TFLOPS (% FP4 peak); FLUX.1 block latency").
+
+A step = the W4A4 linears of one FLUX.1-dev double block (image stream at
+4096 tokens, text stream at 512 tokens: qkv, proj, MLP up, MLP down) and one
+single block (4608 tokens: linear1 3072->21504, linear2 15360->3072), rank
+32, NVFP4, bf16 activations -- BASELINE config C4.  Each linear is K1
+(svdq_quantize_act_lowrank_down) followed by K2 (svdq_gemm_w4a4_lowrank_up).
+TFLOPS counts 2*M*N*K per linear (the low-rank FLOPs are overhead).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl svdq|reference]
+
+N > 1 (torchrun): every rank runs the same step on its own GPU (replicas,
+weak scaling, no collective on the data path); value = all ranks' FLOPs /
+max-over-ranks time.  Prints one JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "fused W4A4+low-rank linear TFLOPS (% FP4 peak); FLUX.1 block latency"
+UNIT = "TFLOP/s"
+
+
+def flux_block_layers(batch=1):
+    return synth.flux_double_block(batch) + synth.flux_single_block(batch)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        p = json.load(open(path))
+        return p, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks (NVML)
+class ClockSampler:
+    def __init__(self, index):
+        self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
+        }
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in names.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self.stop_ev.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ svdq arm
+def build_layers(P, torch, layers, fmt, dev):
+    """Synthetic FLUX-shaped layers (DESIGN.md input recipe), weights prepared on the GPU
+    by svdq_quantize_weights (fp64 Gram + eigensolver SVD, residual quantization)."""
+    out = []
+    for i, L in enumerate(layers):
+        g = torch.Generator(device="cpu").manual_seed(4000 + i)
+        w = synth.gen_w(L.K, L.N, synth.rng(4, i, 1))
+        xcal = synth.gen_x(256, L.K, synth.rng(4, i, 2))
+        lam = (np.max(np.abs(xcal), 0) ** 0.5 / np.max(np.abs(w), 1) ** 0.5).clip(1e-5, 1e5)
+        lam = lam.astype(np.float32)
+        bias = torch.from_numpy(synth.gen_bias(L.N, synth.rng(4, i, 3))).to(dev).to(torch.bfloat16)
+        layer = P.svdq_quantize_weights(torch.from_numpy(w).to(dev), torch.from_numpy(lam).to(dev), L.r,
+                                        fmt, "bf16", 1.0, bias=bias)
+        x = torch.from_numpy(synth.gen_x(L.M, L.K, synth.rng(4, i, 0))).to(dev).to(torch.bfloat16)
+        bq, bs, bl = P.svdq_act_buffer_sizes(fmt, L.M, L.K, L.r)
+        bufs = dict(
+            x=x,
+            xq=torch.empty(bq, dtype=torch.uint8, device=dev),
+            xs=torch.empty(bs, dtype=torch.uint8, device=dev),
+            xl1=torch.empty(max(bl // 2, 8), dtype=torch.int16, device=dev),
+            y=torch.empty(L.M, L.N, dtype=torch.bfloat16, device=dev),
+        )
+        out.append((L, layer, bufs))
+        del w, g
+    torch.cuda.synchronize()
+    return out
+
+
+def run_svdq(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2411_05007_b200 as P
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    layers = flux_block_layers(args.batch)
+    built = build_layers(P, torch, layers, args.fmt, dev)
+    flops = sum(2.0 * L.M * L.N * L.K for L in layers)
+    k1_bytes = sum(L.M * L.K * 2 + L.M * L.K * (0.5625 if args.fmt == "nvfp4" else 0.53125)
+                   + L.M * L.r * 2 for L in layers)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step(st, k1_events=None, k2_events=None, only=None):
+        for j, (L, layer, b) in enumerate(built):
+            if only == "k1":
+                P.svdq_quantize_act_lowrank_down(layer, b["x"], b["xq"], b["xs"], b["xl1"], stream=st)
+                continue
+            if only == "k2":
+                P.svdq_gemm_w4a4_lowrank_up(layer, b["xq"], b["xs"], b["xl1"], L.M, Y=b["y"], stream=st)
+                continue
+            if k1_events is not None:
+                k1_events[j][0].record(st)
+            P.svdq_quantize_act_lowrank_down(layer, b["x"], b["xq"], b["xs"], b["xl1"], stream=st)
+            if k1_events is not None:
+                k1_events[j][1].record(st)
+                k2_events[j][0].record(st)
+            P.svdq_gemm_w4a4_lowrank_up(layer, b["xq"], b["xs"], b["xl1"], L.M, Y=b["y"], stream=st)
+            if k2_events is not None:
+                k2_events[j][1].record(st)
+
+    # eager warm-up (also sets kernel attributes), then capture the step as CUDA graphs:
+    # one plain (timed region) and one with external timing events around every launch.
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step(stream)
+    torch.cuda.synchronize()
+    ext = lambda: torch.cuda.Event(enable_timing=True, external=True)
+    k1_ev = [(ext(), ext()) for _ in built]
+    k2_ev = [(ext(), ext()) for _ in built]
+    g_plain, g_ev = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    n0 = P.svdq_launch_count()
+    with torch.cuda.graph(g_plain, stream=stream):
+        step(stream)
+    launches_per_step = P.svdq_launch_count() - n0
+    with torch.cuda.graph(g_ev, stream=stream):
+        step(stream, k1_ev, k2_ev)
+    g_k1, g_k2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_k1, stream=stream):
+        step(stream, only="k1")
+    with torch.cuda.graph(g_k2, stream=stream):
+        step(stream, only="k2")
+    torch.cuda.synchronize()
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            g_plain.replay()
+    torch.cuda.synchronize()
+
+    step_ev = [(ev(), ev()) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        with torch.cuda.stream(stream):
+            for s in range(args.steps):
+                flush.zero_()                       # L2 flush (outside the per-step events)
+                step_ev[s][0].record(stream)
+                g_plain.replay()
+                step_ev[s][1].record(stream)
+        torch.cuda.synchronize()
+    launches = launches_per_step * args.steps
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in step_ev]
+    total_ms = float(sum(step_ms))
+    # per-kernel durations: replay the event graph (same inputs, L2 flushed before each)
+    k1_rows, k2_rows = [], []
+    for s in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            g_ev.replay()
+        torch.cuda.synchronize()
+        k1_rows.append([a.elapsed_time(b) for a, b in k1_ev])
+        k2_rows.append([a.elapsed_time(b) for a, b in k2_ev])
+    k1_ms = np.array(k1_rows)
+    k2_ms = np.array(k2_rows)
+    # K1-only / K2-only graphs: the same launches back to back, no K1<->K2 alternation
+    only_ms = {}
+    for name, g in (("k1", g_k1), ("k2", g_k2)):
+        tot = 0.0
+        for s in range(args.steps):
+            a, b = ev(), ev()
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                a.record(stream)
+                g.replay()
+                b.record(stream)
+            torch.cuda.synchronize()
+            tot += a.elapsed_time(b)
+        only_ms[name] = tot / args.steps
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # ---------------- end to end through the public API with host buffers
+    hx = [b["x"].cpu().pin_memory() for (_, _, b) in built]
+    hy = [torch.empty(b["y"].shape, dtype=b["y"].dtype, pin_memory=True) for (_, _, b) in built]
+    ws = [torch.empty(P.abi.forward_workspace_bytes(layer, L.M), dtype=torch.uint8, device=dev)
+          for (L, layer, _) in built]
+    h2d = sum(x.numel() * x.element_size() for x in hx)
+    d2h = sum(y.numel() * y.element_size() for y in hy)
+
+    def e2e_step():
+        with torch.cuda.stream(stream):
+            for j, (L, layer, b) in enumerate(built):
+                b["x"].copy_(hx[j], non_blocking=True)
+                P.svdq_linear_forward(layer, b["x"], Y=b["y"], ws=ws[j], stream=stream)
+                hy[j].copy_(b["y"], non_blocking=True)
+        stream.synchronize()
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = ev(), ev()
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    if rank != 0:
+        return None
+    pk, pk_kind = peaks()
+    fp4_peak = 4.0 * pk.get("bf16_tflops_sustained", pk["bf16_tflops"])     # guide: fp4 = 4 x bf16 nominal
+    k2_flops = np.array([2.0 * L.M * L.N * L.K for L in layers])
+    k2_avg_s = k2_ms.mean(axis=0) / 1e3
+    k2_achieved = float(k2_flops.sum() / k2_avg_s.sum() / 1e12)
+    k1_avg_s = k1_ms.mean(axis=0) / 1e3
+    k1_gbs = float(k1_bytes / k1_avg_s.sum() / 1e9)
+    value = world * flops * args.steps / (total_ms / 1e3) / 1e12
+    per_layer = {L.name: {"M": L.M, "K": L.K, "N": L.N,
+                          "k1_us": round(float(k1_avg_s[j] * 1e6), 2),
+                          "k2_us": round(float(k2_avg_s[j] * 1e6), 2),
+                          "k2_tflops": round(float(k2_flops[j] / k2_avg_s[j] / 1e12), 1)}
+                 for j, L in enumerate(layers)}
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k2_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("bytes_per_launch")
+    clocks = clk.summary()
+    return {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "e2m1 x e2m1 -> f32 (NVFP4 g16 e4m3 scales) + bf16 low-rank",
+        "data": "synthetic (seeded; DESIGN.md input recipe), weights prepared on GPU by svdq_quantize_weights",
+        "config": {"workload": "flux1-dev block linears: 1 double block (img 4096 tok + txt 512 tok: "
+                               "qkv, proj, mlp_up, mlp_down) + 1 single block (4608 tok: linear1, linear2)",
+                   "batch": args.batch, "hidden": 3072, "mlp": 12288, "rank": 32, "format": args.fmt,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "flushed between steps (512 MiB write outside the per-step events)",
+                   "block_latency_ms": round(total_ms / args.steps, 4)},
+        "roofline": {"bound": "tensor", "achieved": round(k2_achieved, 1), "peak": round(fp4_peak, 1),
+                     "unit": "TFLOP/s", "frac": round(k2_achieved / fp4_peak, 4), "traffic": traffic,
+                     "kernel": "svdq_gemm_w4a4_lowrank_up (K2, NVFP4)",
+                     "peak_source": f"4 x {pk_kind} sustained bf16 (MEASURED_PEAKS.json), guide fp4:bf16 = 9:2.25",
+                     "achieved_def": "sum 2*M*N*K over the step's linears / sum of K2 CUDA-event durations"},
+        "k1": {"bound": "hbm", "achieved": round(k1_gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+               "frac": round(k1_gbs / pk["hbm_gbs"], 4),
+               "achieved_def": "sum (2MK + 0.5625MK + 2Mr) / sum of K1 durations"},
+        "per_layer": per_layer,
+        "e2e": {"value": round(world * flops * args.steps / (e2e_ms / 1e3) / 1e12, 3), "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": round(e2e_ms / args.steps, 3),
+                "path": "svdq_linear_forward (C ABI) per linear; pinned host X in, Y out"},
+        "graph_only_ms": {"k1_all_layers": round(only_ms["k1"], 4), "k2_all_layers": round(only_ms["k2"], 4),
+                          "note": "each kernel's launches replayed back to back as one graph (L2 flushed before)"},
+        "gpu_launches": int(launches),
+        "timing": "step captured once as a CUDA graph (20 launches), replayed per step; per-kernel "
+                  "times from a second graph with external timing events around each launch",
+        "clocks": clocks,
+    }
+
+
+# ------------------------------------------------------------------ oracle timings
+def oracle_sample_tflops(layers, rows, budget_s=None):
+    """Oracle forward (K1 + K2 semantics) on `rows` tokens of each layer.  Operands come
+    from the oracle's own prepare_operands with a cheap (randomized) decomposition of
+    W_hat -- weight preparation is offline on both arms and untimed."""
+    from oracle import svdquant as S
+    from oracle import formats as F
+    t_total, flops = 0.0, 0.0
+    for i, L in enumerate(layers):
+        w = synth.gen_w(L.K, L.N, synth.rng(4, i, 1))
+        xcal = synth.gen_x(256, L.K, synth.rng(4, i, 2))
+        lam = S.compute_smoothing(xcal, w, 0.5)
+        w_hat = S.smooth_weight(w, lam)
+        g = np.random.default_rng(i).standard_normal((L.N, L.r + 8))
+        q, _ = np.linalg.qr(w_hat @ g)
+        u, s, vt = np.linalg.svd(q.T @ w_hat, full_matrices=False)
+        L1 = (q @ u[:, :L.r]) * s[:L.r]
+        L2 = vt[:L.r]
+        d = S.Decomposition(w_hat, L1, L2, w_hat - L1 @ L2, s)
+        ops = S.prepare_operands(w, lam, L.r, "nvfp4", decomp=d,
+                                 bias=F.bf16_round(synth.gen_bias(L.N, synth.rng(4, i, 3))))
+        x = F.bf16_round(synth.gen_x(rows, L.K, synth.rng(4, i, 0)))
+        t0 = time.perf_counter()
+        S.forward(x, ops)
+        t_total += time.perf_counter() - t0
+        flops += 2.0 * rows * L.N * L.K
+    return flops / t_total / 1e12, t_total
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:
+        return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+def run_reference(args):
+    layers = flux_block_layers(args.batch)
+    rows = args.ref_rows
+    for _ in range(args.warmup):
+        oracle_sample_tflops(layers[:1], 8)
+    vals, ts = [], []
+    for _ in range(args.steps):
+        v, t = oracle_sample_tflops(layers, rows)
+        vals.append(v)
+        ts.append(t)
+    value = float(np.mean(vals))
+    cores = blas_threads()
+    sample = f"{rows} tokens of each of the step's {len(layers)} linears per step (oracle forward, fp64)"
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * float(np.mean(ts)), 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle)",
+        "data": "synthetic (seeded)",
+        "config": {"workload": "flux1-dev block linears (row sample)", "rank": 32, "format": args.fmt},
+        "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="svdq", choices=["svdq", "reference"])
+    ap.add_argument("--fmt", default="nvfp4", choices=["nvfp4", "int4"])
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--ref-rows", type=int, default=32)
+    ap.add_argument("--cpu-rows", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "svdq":
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)))
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_svdq(args, rank, world, local_rank)
+    if rank == 0:
+        if not args.no_cpu_baseline and world == 1:
+            v, t = oracle_sample_tflops(flux_block_layers(args.batch)[:2], args.cpu_rows)
+            out["cpu_baseline"] = {"value": round(v, 6), "unit": UNIT, "cores": blas_threads(),
+                                   "kind": "oracle",
+                                   "sample": f"{args.cpu_rows} tokens of the img qkv + proj linears "
+                                             f"(oracle forward, {t:.1f} s)"}
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -14,7 +14,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsvdq.so")
+LIB_PATH = os.environ.get("SVDQ_LIB") or os.path.join(_HERE, "libsvdq.so")   # SVDQ_LIB: debug builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

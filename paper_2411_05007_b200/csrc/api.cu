@@ -104,7 +104,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 2D row-major tensor [rows][cols] of `dt`, row pitch `pitch_bytes`, box {box_cols, box_rows},
 // 128-byte swizzle.
 svdq_status make_map(CUtensorMap *map, const void *base, CUtensorMapDataType dt, int64_t cols,
-                     int64_t rows, int64_t pitch_bytes, uint32_t box_cols, uint32_t box_rows) {
+                     int64_t rows, int64_t pitch_bytes, uint32_t box_cols, uint32_t box_rows,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return fail(SVDQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -112,7 +113,7 @@ svdq_status make_map(CUtensorMap *map, const void *base, CUtensorMapDataType dt,
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, dt, 2, const_cast<void *>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SVDQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return SVDQ_OK;
@@ -197,7 +198,21 @@ svdq_status svdq_quantize_act_lowrank_down(const svdq_linear *L, const void *X, 
   p.xq = xq;
   p.xs = xs;
   p.xl1 = xl1;
-  cudaError_t e = launch_k1(p, static_cast<cudaStream_t>(stream));
+  cudaError_t e;
+  if (p.x_bf16) {
+    // TMA + tcgen05 path: X tiles [128 x 64] and L1s tiles [rank x 64], 128-B swizzle
+    K1Maps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    if ((st = make_map(&maps.x, X, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->K, M, ldx * 2, 64, 128)) != SVDQ_OK)
+      return st;
+    if (L->rank > 0 &&
+        (st = make_map(&maps.l1s, L->l1s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->K, L->rank, L->K * 2, 64,
+                       static_cast<uint32_t>(L->rank))) != SVDQ_OK)
+      return st;
+    e = launch_k1_tc(maps, p, static_cast<cudaStream_t>(stream));
+  } else {
+    e = launch_k1(p, static_cast<cudaStream_t>(stream));
+  }
   if (e != cudaSuccess) return cuda_fail(e, "K1 launch");
   ++g_launches;
   return SVDQ_OK;
@@ -240,6 +255,12 @@ svdq_status svdq_gemm_w4a4_lowrank_up(const svdq_linear *L, const uint8_t *xq, c
   if (L->fmt == SVDQ_FMT_NVFP4) {
     if ((st = make_map(&maps.a, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, M, K / 2, 128, 128)) != SVDQ_OK) return st;
     if ((st = make_map(&maps.b, L->w_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, N, K / 2, 128, BN)) != SVDQ_OK) return st;
+  } else {
+    // packed int4 tiles [rows x 64 B] (two K groups), dense (no swizzle): unpacked in smem
+    if ((st = make_map(&maps.a, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, M, K / 2, 64, 128,
+                       CU_TENSOR_MAP_SWIZZLE_NONE)) != SVDQ_OK) return st;
+    if ((st = make_map(&maps.b, L->w_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, N, K / 2, 64, BN,
+                       CU_TENSOR_MAP_SWIZZLE_NONE)) != SVDQ_OK) return st;
   }
   if (L->rank > 0) {
     if ((st = make_map(&maps.xl1, xl1, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->rank, M, L->rank * 2, 64, 128)) != SVDQ_OK) return st;
@@ -532,10 +553,14 @@ svdq_status svdq_debug_int4_group_accum(const uint8_t *xq, const uint8_t *wq, in
   p.wq = wq;
   p.dbg_acc = acc;
   p.alpha = 1.0f;
+  if (!aligned16(xq) || !aligned16(wq) || !aligned16(acc)) return fail(SVDQ_ERR_ALIGNMENT, "unaligned");
   K2Maps maps;
   std::memset(&maps, 0, sizeof(maps));
+  if ((st = make_map(&maps.a, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, M, K / 2, 64, 128,
+                     CU_TENSOR_MAP_SWIZZLE_NONE)) != SVDQ_OK) return st;
+  if ((st = make_map(&maps.b, wq, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, N, K / 2, 64, kInt4BN,
+                     CU_TENSOR_MAP_SWIZZLE_NONE)) != SVDQ_OK) return st;
   cudaError_t e = launch_k2_int4(maps, p, static_cast<cudaStream_t>(stream));
-  if (e == cudaErrorNotSupported) return fail(SVDQ_ERR_UNSUPPORTED, "INT4 GEMM not built");
   if (e != cudaSuccess) return cuda_fail(e, "int4 debug launch");
   ++g_launches;
   return SVDQ_OK;

@@ -20,7 +20,12 @@ struct K1Params {
   uint8_t *xs;
   uint16_t *xl1;
 };
-cudaError_t launch_k1(const K1Params &p, cudaStream_t s);
+cudaError_t launch_k1(const K1Params &p, cudaStream_t s);       // mma.sync path (fp16 X)
+struct K1Maps {
+  CUtensorMap x, l1s;
+};
+cudaError_t launch_k1_tc(const K1Maps &maps, const K1Params &p, cudaStream_t s);   // bf16 X
+int k1_tc_ksplit(int64_t Mpad, int64_t K);
 
 struct K2Params {
   int64_t M, N, K, Npad;

@@ -1,0 +1,367 @@
+// K1 for bf16 activations, Blackwell-native: TMA-streamed X tiles, the
+// low-rank down-projection on tcgen05 tensor cores, quantization on CUDA cores
+// from the same shared-memory tile ("Fused Quantize + Down Projection",
+// Fig. 5(b)).
+//
+// One CTA = 128 rows x a contiguous K range; the ks CTAs of a cluster split K.
+//   warp 0      TMA producer: X tile [128 rows x 64] (bf16, 128-B swizzle), the
+//               matching L1s tile [r x 64] and 64 lambda_inv values into a smem ring.
+//   warp 1      TMEM allocator + MMA issuer: xl1_partial[128 x r] += X_tile . L1s_tile^T
+//               (tcgen05.mma kind::f16, fp32 accumulation in TMEM).
+//   warps 2..17 quantizers, 8 rows each: x_hat = fl32(x * lambda_inv), NVFP4 / INT4
+//               codes + scales (App. B recipe, bit-exact) straight from smem.  NVFP4
+//               qinv = fl32(1 / fl32(f32(sf) * gs_x)) comes from a 256-entry table built
+//               per CTA with that exact recipe.
+// The cluster then reduces the ks partial xl1 tiles through distributed shared
+// memory in fixed rank order (deterministic), rounds to bf16 and stores.
+// X rows >= M are zero-filled by TMA, so the NVFP4 padding rows get sf = 0x00.
+#include <cstdint>
+#include <cuda_bf16.h>
+
+#include "formats.cuh"
+#include "k1_launch.h"
+#include "sm100.cuh"
+
+#ifdef SVDQ_TRACE
+namespace svdq { __device__ unsigned long long g_k1_trace[256]; __device__ unsigned long long g_k1_cta[1024][3]; }
+extern "C" int svdq_k1_cta_read(unsigned long long *host) {
+  return cudaMemcpyFromSymbol(host, svdq::g_k1_cta, sizeof(unsigned long long) * 1024 * 3) == cudaSuccess ? 0 : 1;
+}
+extern "C" int svdq_k1_trace_read(unsigned long long *host) {
+  return cudaMemcpyFromSymbol(host, svdq::g_k1_trace, sizeof(unsigned long long) * 256) == cudaSuccess ? 0 : 1;
+}
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(slot) \
+  do { if (blockIdx.x == 0 && blockIdx.y == 0) svdq::g_k1_trace[(slot)] = gtime(); } while (0)
+#else
+#define TRACE(slot) do {} while (0)
+#endif
+
+namespace svdq {
+
+namespace {
+
+constexpr int kQuantWarps = 16;   // 8 rows each
+constexpr int kThreads = 32 * (2 + kQuantWarps);
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  return static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(lo))) |
+         (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(hi))) << 16);
+}
+
+struct K1Layout {
+  int stage_bytes, stages, red_stride;
+  size_t red_off, bar_off, smem;
+};
+
+__host__ __device__ inline K1Layout k1_layout(int rank) {
+  K1Layout L;
+  L.stage_bytes = ((16384 + rank * 128 + 256) + 1023) / 1024 * 1024;
+  L.red_stride = rank + 2;                       // padded row stride (floats, even: float2 reads)
+  const size_t red = rank ? static_cast<size_t>(128) * L.red_stride * 4 : 0;
+  int s = static_cast<int>((150 * 1024 - red) / L.stage_bytes);
+  L.stages = s > 8 ? 8 : (s < 2 ? 2 : s);
+  L.red_off = static_cast<size_t>(L.stages) * L.stage_bytes;
+  L.bar_off = (L.red_off + red + 15) / 16 * 16;
+  L.smem = L.bar_off + 256 + 1024 + 1024;     // + 256-entry qinv table
+  return L;
+}
+
+template <int kFmt, bool kScaleBf16>
+__global__ void __launch_bounds__(kThreads, 1)
+    k1_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmL,
+                 const K1Params p, int ks) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~static_cast<uintptr_t>(1023));
+  const int r = p.rank;
+  const K1Layout Ly = k1_layout(r);
+  const int S = Ly.stages;
+  float *red = reinterpret_cast<float *>(smem + Ly.red_off);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + Ly.bar_off);
+  uint64_t *empty = full + 8;
+  uint64_t *dfull = empty + 8;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dfull + 1);
+  float *qinv_lut = reinterpret_cast<float *>(smem + Ly.bar_off + 256);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t K = p.K;
+  const int nkb = static_cast<int>(K / 64);
+  const int crank = static_cast<int>(blockIdx.x);          // rank in the K-split cluster
+  const int kb_begin = crank * nkb / ks;
+  const int nsteps = (crank + 1) * nkb / ks - kb_begin;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.y) * 128;
+  const uint32_t tcols = r <= 32 ? 32 : (r <= 64 ? 64 : 128);
+
+  if (threadIdx.x == 0) TRACE(0);
+#ifdef SVDQ_TRACE
+  const int cta_id = blockIdx.y * gridDim.x + blockIdx.x;
+  if (threadIdx.x == 0 && cta_id < 1024) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    svdq::g_k1_cta[cta_id][0] = gtime();
+    svdq::g_k1_cta[cta_id][2] = smid;
+  }
+#endif
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kQuantWarps + (r ? 1 : 0));
+    }
+    mbar_init(dfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmX);
+    if (r) tma_prefetch(&tmL);
+  }
+  if (warp == 1 && r) tmem_alloc_n(tmem_slot, tcols);
+  if (kFmt == 0 && threadIdx.x >= 64 && threadIdx.x < 64 + 256) {
+    const uint32_t code = threadIdx.x - 64;            // UE4M3 byte; 0x7F.. are never produced
+    const float sfd = e4m3_to_f32(code & 0x7F);
+    qinv_lut[code] = sfd == 0.f ? 0.f : __frcp_rn(__fmul_rn(sfd, p.gs_x));
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = r ? *tmem_slot : 0;
+  if (threadIdx.x == 0) TRACE(1);
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- producer
+    if (elect_one()) {
+      const uint32_t bytes = 16384 + r * 128 + 256;
+      // warm L2 with the first ring's worth of X tiles beyond what the smem ring holds
+      for (int i = S; i < nsteps && i < 2 * S; ++i)
+        tma_prefetch_2d(&tmX, (kb_begin + i) * 64, static_cast<int32_t>(row0));
+      for (int i = 0; i < nsteps; ++i) {
+        const int s = i % S;
+        const uint32_t ph = (i / S) & 1;
+        const int kb = kb_begin + i;
+        mbar_wait_spin(&empty[s], ph ^ 1);
+        TRACE(2 + i);                                     // producer issues stage i
+        if (i + 2 * S < nsteps) tma_prefetch_2d(&tmX, (kb_begin + i + 2 * S) * 64, static_cast<int32_t>(row0));
+        uint8_t *st = smem + s * Ly.stage_bytes;
+        mbar_arrive_expect_tx(&full[s], bytes);
+        tma_load_2d(st, &tmX, &full[s], kb * 64, static_cast<int32_t>(row0));
+        if (r) tma_load_2d(st + 16384, &tmL, &full[s], kb * 64, 0);
+        bulk_load(st + 16384 + r * 128, p.lam_inv + kb * 64, 256, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (r) {
+      const uint32_t idesc = idesc_bf16(128, static_cast<uint32_t>(r));
+      for (int i = 0; i < nsteps; ++i) {
+        const int s = i % S;
+        const uint32_t ph = (i / S) & 1;
+        mbar_wait_spin(&full[s], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t xa = smem_u32(smem + s * Ly.stage_bytes);
+          const uint32_t la = xa + 16384;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            mma_bf16(tmem, sdesc_kmajor_sw128(xa + 32 * j), sdesc_kmajor_sw128(la + 32 * j), idesc,
+                     (i | j) != 0);
+          tc_commit(&empty[s]);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) tc_commit(dfull);
+      __syncwarp();
+    }
+  } else {
+    // ---------------------------------------------------------------- quantizers
+    const int qw = warp - 2;
+    const int g = lane >> 2;
+    const int q = lane & 3;
+    const int rl = qw * 8 + g;                          // this lane's row within the tile
+    const int64_t row = row0 + rl;
+    const bool rvalid = row < p.M;
+    const float t6 = __fmul_rn(__frcp_rn(p.gs_x), __frcp_rn(6.0f));
+    uint8_t *xq_row = p.xq + row * (K / 2);
+    uint8_t *sf_row = p.xs + sf_offset(row, 0, K);        // + kb * 512 per 64-wide block
+    uint16_t *s16_row = reinterpret_cast<uint16_t *>(p.xs) + row * (K / 64);
+    const uint32_t swz = static_cast<uint32_t>(rl & 7);
+    for (int i = 0; i < nsteps; ++i) {
+      const int s = i % S;
+      const uint32_t ph = (i / S) & 1;
+      const int kb = kb_begin + i;
+      mbar_wait(&full[s], ph);                            // suspend (do not hammer the barrier)
+      if (qw == 0 && lane == 0) TRACE(66 + i);            // first quantizer sees stage i
+      const uint32_t xa = smem_u32(smem + s * Ly.stage_bytes) + rl * 128;
+      const float *lam = reinterpret_cast<const float *>(smem + s * Ly.stage_bytes + 16384 + r * 128);
+      float xh[2][8];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const float4 la = *reinterpret_cast<const float4 *>(lam + c * 32 + q * 8);
+        const float4 lb = *reinterpret_cast<const float4 *>(lam + c * 32 + q * 8 + 4);
+        const float lm[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+        const uint4 v = lds128(xa + ((static_cast<uint32_t>(c * 4 + q) ^ swz) * 16));
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          xh[c][2 * j] = __fmul_rn(__uint_as_float(w4[j] << 16), lm[2 * j]);
+          xh[c][2 * j + 1] = __fmul_rn(__uint_as_float(w4[j] & 0xFFFF0000u), lm[2 * j + 1]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);       // tile consumed: values are in registers
+      if (qw == 15 && lane == 0) TRACE(130 + i);          // last quantizer released stage i
+      if constexpr (kFmt == 0) {
+        uint32_t sfb[2], codes[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          float amax = 0.f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) amax = fmaxf(amax, fabsf(xh[c][j]));
+          amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+          const uint32_t sf = e4m3_rn_sat(__fmul_rn(amax, t6));
+          const float qinv = qinv_lut[sf];
+          float v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = __fmul_rn(xh[c][j], qinv);
+          codes[c] = e2m1x8(v);
+          sfb[c] = sf;
+        }
+        const uint32_t o0 = __shfl_down_sync(0xffffffffu, sfb[0], 2);
+        const uint32_t o1 = __shfl_down_sync(0xffffffffu, sfb[1], 2);
+        if (rvalid) {
+          *reinterpret_cast<uint32_t *>(xq_row + kb * 32 + q * 4) = codes[0];
+          *reinterpret_cast<uint32_t *>(xq_row + kb * 32 + 16 + q * 4) = codes[1];
+        }
+        if (q == 0)
+          *reinterpret_cast<uint32_t *>(sf_row + kb * 512) = sfb[0] | (o0 << 8) | (sfb[1] << 16) | (o1 << 24);
+      } else {
+        float amax = 0.f;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) amax = fmaxf(amax, fabsf(xh[c][j]));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+        const uint16_t sc = scale16_rn_sat<kScaleBf16>(__fdiv_rn(amax, 7.0f));
+        const float sd = scale16_to_f32<kScaleBf16>(sc);
+        const float qinv = sd == 0.f ? 0.f : __frcp_rn(sd);
+        if (rvalid) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              int v = __float2int_rn(__fmul_rn(xh[c][j], qinv));
+              v = max(-7, min(7, v));
+              word |= (static_cast<uint32_t>(v) & 0xFu) << (4 * j);
+            }
+            *reinterpret_cast<uint32_t *>(xq_row + kb * 32 + c * 16 + q * 4) = word;
+          }
+          if (q == 0) s16_row[kb] = sc;
+        }
+      }
+    }
+  }
+
+  if (threadIdx.x == 64) TRACE(194);                      // quantizer 0 done
+#ifdef SVDQ_TRACE
+  if (threadIdx.x == 64 && cta_id < 1024) svdq::g_k1_cta[cta_id][1] = gtime();
+#endif
+  if (r == 0) return;
+  // -------------------------------------------------------------------- xl1 reduction
+  if (warp >= 2 && warp < 6) {
+    const int quad = warp & 3;
+    const int rl = quad * 32 + lane;
+    mbar_wait_spin(dfull, 0);
+    tc_fence_after();
+    for (int c16 = 0; c16 < r / 16; ++c16) {
+      uint32_t v[16];
+      tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(quad * 32) << 16) + c16 * 16, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) red[rl * Ly.red_stride + c16 * 16 + j] = __uint_as_float(v[j]);
+    }
+  }
+  tc_fence_before();
+  if (threadIdx.x == 64) TRACE(195);                      // TMEM drained
+  cluster_sync();                                    // every partial tile is in smem
+  if (threadIdx.x == 64) TRACE(196);
+  {
+    const int rows_lo = crank * 128 / ks;
+    const int rows_hi = (crank + 1) * 128 / ks;
+    const int pairs = (rows_hi - rows_lo) * (r / 2);
+    for (int idx = threadIdx.x; idx < pairs; idx += kThreads) {
+      const int rl = rows_lo + idx / (r / 2);
+      const int col = 2 * (idx % (r / 2));
+      const float *src = red + rl * Ly.red_stride + col;
+      float2 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)                    // all remote loads in flight at once
+        v[j] = j < ks ? ld_dsmem_f32x2(src, static_cast<uint32_t>(j)) : make_float2(0.f, 0.f);
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {                  // fixed rank order: deterministic
+        s0 += v[j].x;
+        s1 += v[j].y;
+      }
+      const int64_t row = row0 + rl;
+      if (row < p.M) *reinterpret_cast<uint32_t *>(p.xl1 + row * r + col) = pack_bf16x2(s0, s1);
+    }
+  }
+  if (threadIdx.x == 64) TRACE(197);
+  cluster_sync();                                    // peers finished reading my smem
+  if (threadIdx.x == 64) TRACE(198);
+  if (warp == 1) tmem_dealloc_n(tmem, tcols);
+}
+
+template <int kFmt, bool kScaleBf16>
+cudaError_t launch_t(const K1Maps &maps, const K1Params &p, int ks, cudaStream_t s) {
+  auto kern = k1_tc_kernel<kFmt, kScaleBf16>;
+  const K1Layout Ly = k1_layout(p.rank);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(Ly.smem));
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(ks), static_cast<unsigned>(p.Mpad / 128), 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = Ly.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(ks);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, maps.x, maps.l1s, p, ks);
+}
+
+}  // namespace
+
+int k1_tc_ksplit(int64_t Mpad, int64_t K) {
+  const int64_t tiles = Mpad / 128;
+  const int64_t nkb = K / 64;
+  int ks = 1;
+  while (ks * 2 <= 8 && tiles * ks * 2 <= 160 && nkb >= ks * 2) ks *= 2;
+  return ks;
+}
+
+cudaError_t launch_k1_tc(const K1Maps &maps, const K1Params &p, cudaStream_t s) {
+  const int ks = k1_tc_ksplit(p.Mpad, p.K);
+  if (p.fmt == 0) return launch_t<0, true>(maps, p, ks, s);
+  return p.scale_bf16 ? launch_t<1, true>(maps, p, ks, s) : launch_t<1, false>(maps, p, ks, s);
+}
+
+}  // namespace svdq

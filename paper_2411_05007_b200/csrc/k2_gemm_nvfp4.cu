@@ -8,14 +8,19 @@
 //                the up-projection is one extra K-slab, so Y is written once)
 //   Y[m,n]    = out_rn(fl32(alpha * acc) + bias[n]),  alpha = gs_x * gs_w
 //
-// Structure: one 128 x BN output tile per CTA, warp-specialized.
-//   warp 0      TMA producer: A/B code tiles (128-B swizzle), SFA/SFB chunks (bulk copy),
-//               then ceil(rank/64) low-rank slabs (xl1 / l2s tiles, zero-filled past rank)
-//               into the same smem ring.
-//   warp 1      TMEM allocator + single-thread MMA issuer: tcgen05.cp of the scale
-//               factors smem -> TMEM, tcgen05.mma, tcgen05.commit releases smem stages.
-//   warps 2..5  epilogue: tcgen05.ld -> alpha, bias -> 16-bit -> global.
-// TMEM (512 columns): accumulator [0, BN); per-stage scale-factor columns after it.
+// Persistent, warp-specialized; one CTA per SM walks 128 x BN output tiles.
+//   warp 0      TMA producer: A/B code tiles (128-B swizzle) and SFA/SFB 512-B chunks
+//               (bulk copies) into a kStages ring, then ceil(rank/64) low-rank slabs
+//               (xl1 / l2s tiles, zero-filled past rank) into the same ring.
+//   warp 1      TMEM allocator + single-thread MMA issuer.  Scale factors go
+//               smem -> TMEM (tcgen05.cp) into one of two SF slots; a slot is reused
+//               only after the MMAs that read it completed.  The accumulator is double
+//               buffered so the epilogue of tile i overlaps the main loop of tile i+1.
+//   warps 2..5  epilogue: tcgen05.ld -> alpha, bias -> 16-bit -> global; releases the
+//               accumulator buffer to the MMA warp.
+// TMEM columns: acc0 [0,BN), acc1 [BN,2BN), SF slots after.  BN = 192 keeps
+// 2*192 + 2*48 <= 512; N tiles that start mid scale-factor atom (n0 % 128 == 64)
+// read SFB from a TMEM address 2 columns (64 rows) into the loaded atom pair.
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -29,18 +34,34 @@ namespace svdq {
 template <int BN>
 struct NvCfg {
   static constexpr int BM = 128;
-  static constexpr int BKB = 128;                       // bytes of K per stage (256 fp4)
-  static constexpr int kStages = BN == 256 ? 4 : 6;
-  static constexpr int A_BYTES = BM * BKB;              // 16 KB
+  static constexpr int BKB = 128;                        // bytes of K per stage (256 fp4)
+  static constexpr int A_BYTES = BM * BKB;               // 16 KB
   static constexpr int B_BYTES = BN * BKB;
-  static constexpr int SFA_BYTES = 4 * 512;             // 128 rows x 16 sf
-  static constexpr int SFB_BYTES = (BN / 128) * 4 * 512;
+  static constexpr int SFA_BYTES = 4 * 512;              // 128 rows x 16 sf
+  static constexpr int SFB_BYTES = 2 * 4 * 512;          // two 128-row atoms x 16 sf
   static constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
-  static constexpr int SF_COLS = 16 + BN / 8;           // TMEM columns per stage
-  static constexpr int SMEM = kStages * STAGE + 1024 + 256;
+  static constexpr int kStages = (200 * 1024) / STAGE;
+  static constexpr int SF_COLS = 16 + 32;                // TMEM columns per SF slot
+  static constexpr int SF_BASE = 2 * BN;
+  static constexpr int BAR_BYTES = 256;
+  static constexpr int SMEM = kStages * STAGE + BAR_BYTES + BN * 4 + 1024;
   static_assert(STAGE % 1024 == 0, "stage must keep 1024-B alignment");
-  static_assert(BN + kStages * SF_COLS <= 512, "TMEM budget");
+  static_assert(SF_BASE + 2 * SF_COLS <= 512, "TMEM budget");
+  static_assert(kStages >= 3, "pipeline depth");
 };
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ float to_f32(T v);
+template <>
+__device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <>
+__device__ __forceinline__ float to_f32<__half>(__half v) { return __half2float(v); }
+template <>
+__device__ __forceinline__ float to_f32<float>(float v) { return v; }
 
 __device__ __forceinline__ float load_bias(const void *b, int dt, int64_t i) {
   if (dt == 0) return __bfloat162float(static_cast<const __nv_bfloat16 *>(b)[i]);
@@ -78,28 +99,35 @@ __global__ void __launch_bounds__(192, 1)
                     const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmL,
                     const K2Params p) {
   using C = NvCfg<BN>;
+  constexpr int S = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~static_cast<uintptr_t>(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::kStages * C::STAGE);
-  uint64_t *empty = full + C::kStages;
-  uint64_t *accum_full = empty + C::kStages;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accum_full + 1);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * C::STAGE);
+  uint64_t *empty = full + S;
+  uint64_t *acc_full = empty + S;      // [2]
+  uint64_t *acc_empty = acc_full + 2;  // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+  float *bias_s = reinterpret_cast<float *>(smem + S * C::STAGE + C::BAR_BYTES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * C::BM;
-  const int64_t n0 = static_cast<int64_t>(blockIdx.y) * BN;
-  const int nkb64 = static_cast<int>(p.K / 64);        // 64-wide K blocks
-  const int nkt = (nkb64 + 3) / 4;                     // pipeline K steps
+  const int nkb64 = static_cast<int>(p.K / 64);          // 64-wide K blocks
+  const int nkt = (nkb64 + 3) / 4;                       // FP4 pipeline steps per tile
   const int nslab = (p.rank + 63) / 64;
+  const int mt_count = static_cast<int>((p.M + 127) / 128);
+  const int nt_count = static_cast<int>((p.N + BN - 1) / BN);
+  const int tiles = mt_count * nt_count;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::kStages; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accum_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);
+    }
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -121,31 +149,34 @@ __global__ void __launch_bounds__(192, 1)
     if (elect_one()) {
       int s = 0;
       uint32_t ph = 0;
-      const int64_t mt = m0 / 128;
-      for (int kt = 0; kt < nkt; ++kt) {
-        const int nsub = min(4, nkb64 - kt * 4);
-        int nsfb = 0;
-        for (int h = 0; h < BN / 128; ++h)
-          if (n0 + h * 128 < p.Npad) ++nsfb;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t *st = smem + s * C::STAGE;
-        mbar_arrive_expect_tx(&full[s], C::A_BYTES + C::B_BYTES + nsub * 512 * (1 + nsfb));
-        tma_load_2d(st, &tmA, &full[s], kt * C::BKB, static_cast<int32_t>(m0));
-        tma_load_2d(st + C::A_BYTES, &tmB, &full[s], kt * C::BKB, static_cast<int32_t>(n0));
-        bulk_load(st + C::A_BYTES + C::B_BYTES, p.sfa + (mt * nkb64 + kt * 4) * 512, nsub * 512,
-                  &full[s]);
-        for (int h = 0; h < nsfb; ++h)
-          bulk_load(st + C::A_BYTES + C::B_BYTES + C::SFA_BYTES + h * 2048,
-                    p.sfb + ((n0 / 128 + h) * nkb64 + kt * 4) * 512, nsub * 512, &full[s]);
-        if (++s == C::kStages) { s = 0; ph ^= 1; }
-      }
-      for (int j = 0; j < nslab; ++j) {
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t *st = smem + s * C::STAGE;
-        mbar_arrive_expect_tx(&full[s], C::BM * 128 + BN * 128);
-        tma_load_2d(st, &tmX, &full[s], j * 64, static_cast<int32_t>(m0));
-        tma_load_2d(st + C::A_BYTES, &tmL, &full[s], j * 64, static_cast<int32_t>(n0));
-        if (++s == C::kStages) { s = 0; ph ^= 1; }
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t m0 = static_cast<int64_t>(t % mt_count) * 128;
+        const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
+        const int64_t atom0 = n0 / 128;                  // first SFB atom of the tile
+        const int64_t atom_last = min((n0 + BN - 1) / 128, p.Npad / 128 - 1);
+        const int natom = static_cast<int>(atom_last - atom0 + 1);   // 1 or 2 atoms cover the tile
+        for (int kt = 0; kt < nkt; ++kt) {
+          const int nsub = min(4, nkb64 - kt * 4);
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t *st = smem + s * C::STAGE;
+          mbar_arrive_expect_tx(&full[s], C::A_BYTES + C::B_BYTES + nsub * 512 * (1 + natom));
+          tma_load_2d(st, &tmA, &full[s], kt * C::BKB, static_cast<int32_t>(m0));
+          tma_load_2d(st + C::A_BYTES, &tmB, &full[s], kt * C::BKB, static_cast<int32_t>(n0));
+          bulk_load(st + C::A_BYTES + C::B_BYTES, p.sfa + ((m0 / 128) * nkb64 + kt * 4) * 512,
+                    nsub * 512, &full[s]);
+          for (int h = 0; h < natom; ++h)
+            bulk_load(st + C::A_BYTES + C::B_BYTES + C::SFA_BYTES + h * 2048,
+                      p.sfb + ((atom0 + h) * nkb64 + kt * 4) * 512, nsub * 512, &full[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        for (int j = 0; j < nslab; ++j) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t *st = smem + s * C::STAGE;
+          mbar_arrive_expect_tx(&full[s], C::BM * 128 + BN * 128);
+          tma_load_2d(st, &tmX, &full[s], j * 64, static_cast<int32_t>(m0));
+          tma_load_2d(st + C::A_BYTES, &tmL, &full[s], j * 64, static_cast<int32_t>(n0));
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
       }
     }
   } else if (warp == 1) {
@@ -154,81 +185,110 @@ __global__ void __launch_bounds__(192, 1)
     constexpr uint32_t idesc_h = idesc_bf16(128, BN);
     int s = 0;
     uint32_t ph = 0;
-    for (int kt = 0; kt < nkt; ++kt) {
-      const int nsub = min(4, nkb64 - kt * 4);
-      mbar_wait(&full[s], ph);
+    int acc_i = 0;
+    // SF slot bookkeeping: the pipeline stage / phase whose MMAs last read each slot
+    int slot_stage[2] = {-1, -1};
+    uint32_t slot_phase[2] = {0, 0};
+    int sf_i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++acc_i) {
+      const int b = acc_i & 1;
+      const uint32_t acc_ph = (acc_i >> 1) & 1;
+      const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
+      const uint32_t sfb_off = static_cast<uint32_t>((n0 % 128) / 32);
+      const uint32_t d_tmem = tmem + b * BN;
+      mbar_wait(&acc_empty[b], acc_ph ^ 1);             // epilogue drained this buffer
       tc_fence_after();
-      if (elect_one()) {
-        uint8_t *st = smem + s * C::STAGE;
-        const uint32_t a_addr = smem_u32(st);
-        const uint32_t b_addr = smem_u32(st + C::A_BYTES);
-        const uint32_t sfa_addr = smem_u32(st + C::A_BYTES + C::B_BYTES);
-        const uint32_t sfb_addr = sfa_addr + C::SFA_BYTES;
-        const uint32_t sf_col = tmem + BN + s * C::SF_COLS;
-        const uint32_t sfa_col = sf_col;
-        const uint32_t sfb_col = sf_col + 16;
-        for (int i = 0; i < nsub; ++i) {
-          tmem_cp_32x128b_warpx4(sfa_col + 4 * i, sdesc_cp_32x128b(sfa_addr + i * 512));
-#pragma unroll
-          for (int h = 0; h < BN / 128; ++h)
-            tmem_cp_32x128b_warpx4(sfb_col + i * (BN / 32) + 4 * h,
-                                   sdesc_cp_32x128b(sfb_addr + h * 2048 + i * 512));
+      for (int kt = 0; kt < nkt; ++kt) {
+        const int nsub = min(4, nkb64 - kt * 4);
+        const int slot = sf_i & 1;
+        if (slot_stage[slot] >= 0) mbar_wait(&empty[slot_stage[slot]], slot_phase[slot]);
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          uint8_t *st = smem + s * C::STAGE;
+          const uint32_t a_addr = smem_u32(st);
+          const uint32_t b_addr = smem_u32(st + C::A_BYTES);
+          const uint32_t sfa_addr = smem_u32(st + C::A_BYTES + C::B_BYTES);
+          const uint32_t sfb_addr = sfa_addr + C::SFA_BYTES;
+          const uint32_t sfa_col = tmem + C::SF_BASE + slot * C::SF_COLS;
+          const uint32_t sfb_col = sfa_col + 16;
+          for (int i = 0; i < nsub; ++i) {
+            tmem_cp_32x128b_warpx4(sfa_col + 4 * i, sdesc_cp_32x128b(sfa_addr + i * 512));
+            tmem_cp_32x128b_warpx4(sfb_col + 8 * i, sdesc_cp_32x128b(sfb_addr + i * 512));
+            tmem_cp_32x128b_warpx4(sfb_col + 8 * i + 4, sdesc_cp_32x128b(sfb_addr + 2048 + i * 512));
+          }
+          for (int i = 0; i < nsub; ++i)
+            mma_nvfp4(d_tmem, sdesc_kmajor_sw128(a_addr + 32 * i), sdesc_kmajor_sw128(b_addr + 32 * i),
+                      idesc_q, sfa_col + 4 * i, sfb_col + 8 * i + sfb_off, (kt | i) != 0);
+          tc_commit(&empty[s]);
         }
-        for (int i = 0; i < nsub; ++i) {
-          mma_nvfp4(tmem, sdesc_kmajor_sw128(a_addr + 32 * i), sdesc_kmajor_sw128(b_addr + 32 * i),
-                    idesc_q, sfa_col + 4 * i, sfb_col + i * (BN / 32), (kt | i) != 0);
+        __syncwarp();
+        slot_stage[slot] = s;
+        slot_phase[slot] = ph;
+        ++sf_i;
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+      for (int j = 0; j < nslab; ++j) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          uint8_t *st = smem + s * C::STAGE;
+          const uint32_t a_addr = smem_u32(st);
+          const uint32_t b_addr = smem_u32(st + C::A_BYTES);
+          const int nk16 = min(4, (p.rank - j * 64) / 16);
+          for (int i = 0; i < nk16; ++i)
+            mma_bf16(d_tmem, sdesc_kmajor_sw128(a_addr + 32 * i), sdesc_kmajor_sw128(b_addr + 32 * i),
+                     idesc_h, (nkt > 0 || j > 0 || i > 0) ? 1u : 0u);
+          tc_commit(&empty[s]);
         }
-        tc_commit(&empty[s]);
+        __syncwarp();
+        if (++s == S) { s = 0; ph ^= 1; }
       }
+      if (elect_one()) tc_commit(&acc_full[b]);
       __syncwarp();
-      if (++s == C::kStages) { s = 0; ph ^= 1; }
     }
-    for (int j = 0; j < nslab; ++j) {
-      mbar_wait(&full[s], ph);
-      tc_fence_after();
-      if (elect_one()) {
-        uint8_t *st = smem + s * C::STAGE;
-        const uint32_t a_addr = smem_u32(st);
-        const uint32_t b_addr = smem_u32(st + C::A_BYTES);
-        const int nk16 = min(4, (p.rank - j * 64) / 16);
-        for (int i = 0; i < nk16; ++i)
-          mma_bf16(tmem, sdesc_kmajor_sw128(a_addr + 32 * i), sdesc_kmajor_sw128(b_addr + 32 * i),
-                   idesc_h, (nkt > 0 || j > 0 || i > 0) ? 1u : 0u);
-        tc_commit(&empty[s]);
-      }
-      __syncwarp();
-      if (++s == C::kStages) { s = 0; ph ^= 1; }
-    }
-    if (elect_one()) tc_commit(accum_full);
-    __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue
     const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
     const int row = quad * 32 + lane;
-    const int64_t grow = m0 + row;
-    mbar_wait(accum_full, 0);
-    tc_fence_after();
+    const int et = threadIdx.x - 64;           // 0..127
+    int acc_i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++acc_i) {
+      const int b = acc_i & 1;
+      const uint32_t acc_ph = (acc_i >> 1) & 1;
+      const int64_t m0 = static_cast<int64_t>(t % mt_count) * 128;
+      const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
+      const int64_t grow = m0 + row;
+      // stage this tile's bias (fp32) in smem
+      named_bar(1, 128);                        // previous tile's readers are done
+      for (int c = et; c < BN; c += 128)
+        bias_s[c] = (p.bias && n0 + c < p.N) ? load_bias(p.bias, p.bias_dtype, n0 + c) : 0.f;
+      named_bar(1, 128);
+      mbar_wait(&acc_full[b], acc_ph);
+      tc_fence_after();
 #pragma unroll 1
-    for (int cc = 0; cc < BN / 32; ++cc) {
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + cc * 32, r);
-      tmem_ld_wait();
-      if (grow < p.M) {
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16) + cc * 32, r);
+        tmem_ld_wait();
+        if (grow < p.M) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int64_t col = n0 + cc * 32 + j * 8;
-          if (col < p.N) {
-            float v[8];
+          for (int j = 0; j < 4; ++j) {
+            const int64_t col = n0 + cc * 32 + j * 8;
+            if (col < p.N) {
+              float v[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              float y = __fmul_rn(p.alpha, __uint_as_float(r[j * 8 + e]));
-              if (p.bias) y = __fadd_rn(y, load_bias(p.bias, p.bias_dtype, col + e));
-              v[e] = y;
+              for (int e = 0; e < 8; ++e)
+                v[e] = __fadd_rn(__fmul_rn(p.alpha, __uint_as_float(r[j * 8 + e])),
+                                 bias_s[cc * 32 + j * 8 + e]);
+              store8(p.Y, p.y_dtype, p.ldy, grow, col, v);
             }
-            store8(p.Y, p.y_dtype, p.ldy, grow, col, v);
           }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
     }
   }
   tc_fence_before();
@@ -242,19 +302,27 @@ static cudaError_t launch_bn(const K2Maps &maps, const K2Params &p, cudaStream_t
   auto kern = k2_nvfp4_kernel<BN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>((p.M + 127) / 128), static_cast<unsigned>((p.N + BN - 1) / BN));
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t tiles = ((p.M + 127) / 128) * ((p.N + BN - 1) / BN);
+  const unsigned grid = static_cast<unsigned>(tiles < num_sms ? tiles : num_sms);
   kern<<<grid, 192, C::SMEM, s>>>(maps.a, maps.b, maps.xl1, maps.l2, p);
   return cudaGetLastError();
 }
 
 int k2_nvfp4_bn(int64_t M, int64_t N) {
-  // 256-wide tiles when there are enough of them to fill the machine.
-  const int64_t tiles256 = ((M + 127) / 128) * ((N + 255) / 256);
-  return tiles256 >= 148 ? 256 : 128;
+  (void)M;
+  if (N % 192 == 0) return 192;
+  if (N % 128 == 0) return 128;
+  return N > 1024 ? 192 : 128;
 }
 
 cudaError_t launch_k2_nvfp4(const K2Maps &maps, const K2Params &p, cudaStream_t s) {
-  return k2_nvfp4_bn(p.M, p.N) == 256 ? launch_bn<256>(maps, p, s) : launch_bn<128>(maps, p, s);
+  return k2_nvfp4_bn(p.M, p.N) == 192 ? launch_bn<192>(maps, p, s) : launch_bn<128>(maps, p, s);
 }
 
 }  // namespace svdq
