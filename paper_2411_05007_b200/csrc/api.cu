@@ -7,6 +7,7 @@
 #include <cusolverDn.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -117,6 +118,35 @@ svdq_status make_map(CUtensorMap *map, const void *base, CUtensorMapDataType dt,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SVDQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return SVDQ_OK;
+}
+
+// 3-D uint64 view of a 128x4 scale-factor buffer: [rows/128][K/64][512 B], box {64, 4, atoms}.
+svdq_status make_sf_map(CUtensorMap *map, const void *base, int64_t rows, int64_t K, uint32_t atoms) {
+  auto fn = encode_fn();
+  if (!fn) return fail(SVDQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int64_t nkb = K / 64;
+  cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(nkb), static_cast<cuuint64_t>((rows + 127) / 128)};
+  cuuint64_t strides[2] = {512, static_cast<cuuint64_t>(nkb * 512)};
+  cuuint32_t box[3] = {64, 4, atoms};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void *>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SVDQ_ERR_CUDA, "cuTensorMapEncodeTiled (sf) failed (%d)", (int)r);
+  return SVDQ_OK;
+}
+
+// CTA-pair kernel for long reductions (measured on B200: K = 12288 / 15360 layers run
+// 13-15 % faster as pairs; K = 3072 layers 5 % faster on the 1-CTA kernel).
+// SVDQ_K2_PAIR=0 / 1 forces one kernel (testing / comparison).
+bool use_pair_kernel(int64_t M, int64_t K) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char *e = getenv("SVDQ_K2_PAIR");
+    mode = e ? atoi(e) : 2;
+  }
+  if (M <= 128 || mode == 0) return false;
+  return mode == 1 || K >= 6144;
 }
 
 }  // namespace
@@ -251,10 +281,23 @@ svdq_status svdq_gemm_w4a4_lowrank_up(const svdq_linear *L, const uint8_t *xq, c
   p.alpha = L->fmt == SVDQ_FMT_NVFP4 ? L->gs_x * L->gs_w : 1.0f;
   K2Maps maps;
   std::memset(&maps, 0, sizeof(maps));
-  const int BN = L->fmt == SVDQ_FMT_NVFP4 ? k2_nvfp4_bn(M, N) : kInt4BN;
+  const bool pair = L->fmt == SVDQ_FMT_NVFP4 && use_pair_kernel(M, K);
+  const int BN = L->fmt == SVDQ_FMT_NVFP4 ? (pair ? kNvfp4PairBN : k2_nvfp4_bn(M, N)) : kInt4BN;
+  const uint32_t b_rows = pair ? kNvfp4PairBN / 2 : static_cast<uint32_t>(BN);   // B rows staged per CTA
+  CUtensorMap sfa_map, sfb_map;
   if (L->fmt == SVDQ_FMT_NVFP4) {
+    const CUtensorMapDataType ydt = y_dtype == SVDQ_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                    : y_dtype == SVDQ_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                           : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const int64_t ysz = y_dtype == SVDQ_FP32 ? 4 : 2;
+    if ((st = make_map(&maps.y, Y, ydt, N, M, ldy * ysz, static_cast<uint32_t>(128 / ysz), 32)) != SVDQ_OK)
+      return st;
     if ((st = make_map(&maps.a, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, M, K / 2, 128, 128)) != SVDQ_OK) return st;
-    if ((st = make_map(&maps.b, L->w_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, N, K / 2, 128, BN)) != SVDQ_OK) return st;
+    if ((st = make_map(&maps.b, L->w_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, N, K / 2, 128, b_rows)) != SVDQ_OK) return st;
+    if (pair) {
+      if ((st = make_sf_map(&sfa_map, xs, M, K, 1)) != SVDQ_OK) return st;
+      if ((st = make_sf_map(&sfb_map, L->w_scales, N, K, 2)) != SVDQ_OK) return st;
+    }
   } else {
     // packed int4 tiles [rows x 64 B] (two K groups), dense (no swizzle): unpacked in smem
     if ((st = make_map(&maps.a, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, M, K / 2, 64, 128,
@@ -264,10 +307,12 @@ svdq_status svdq_gemm_w4a4_lowrank_up(const svdq_linear *L, const uint8_t *xq, c
   }
   if (L->rank > 0) {
     if ((st = make_map(&maps.xl1, xl1, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->rank, M, L->rank * 2, 64, 128)) != SVDQ_OK) return st;
-    if ((st = make_map(&maps.l2, L->l2s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->rank, N, L->rank * 2, 64, BN)) != SVDQ_OK) return st;
+    if ((st = make_map(&maps.l2, L->l2s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->rank, N, L->rank * 2, 64, b_rows)) != SVDQ_OK) return st;
   }
-  cudaError_t e = L->fmt == SVDQ_FMT_NVFP4 ? launch_k2_nvfp4(maps, p, static_cast<cudaStream_t>(stream))
-                                           : launch_k2_int4(maps, p, static_cast<cudaStream_t>(stream));
+  cudaError_t e = L->fmt == SVDQ_FMT_NVFP4
+                      ? (pair ? launch_k2_nvfp4_2sm(maps, sfa_map, sfb_map, p, static_cast<cudaStream_t>(stream))
+                              : launch_k2_nvfp4(maps, p, static_cast<cudaStream_t>(stream)))
+                      : launch_k2_int4(maps, p, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported) return fail(SVDQ_ERR_UNSUPPORTED, "INT4 GEMM not built");
   if (e != cudaSuccess) return cuda_fail(e, "K2 launch");
   ++g_launches;

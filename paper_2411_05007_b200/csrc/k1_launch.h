@@ -44,10 +44,15 @@ struct K2Params {
   int32_t *dbg_acc;       // INT4 debug: per-group int32 accumulators [K/64][M][N]
 };
 struct K2Maps {
-  CUtensorMap a, b, xl1, l2;
+  CUtensorMap a, b, xl1, l2, y;   // y: output store map, box {128 B of columns, 32 rows}, SW128
 };
 cudaError_t launch_k2_nvfp4(const K2Maps &maps, const K2Params &p, cudaStream_t s);
-int k2_nvfp4_bn(int64_t M, int64_t N);   // N tile the NVFP4 GEMM will use
+int k2_nvfp4_bn(int64_t M, int64_t N);   // N tile the 1-CTA NVFP4 GEMM will use
+// CTA-pair NVFP4 GEMM (256 x 192 tiles, each CTA stages 96 rows of B); SF tensor maps are
+// 3-D uint64 views [tiles128][K/64][64] of the 128x4 scale-factor layout.
+cudaError_t launch_k2_nvfp4_2sm(const K2Maps &maps, const CUtensorMap &sfa, const CUtensorMap &sfb,
+                                const K2Params &p, cudaStream_t s);
+constexpr int kNvfp4PairBN = 192;
 constexpr int kInt4BN = 128;             // N tile of the INT4 GEMM
 cudaError_t launch_k2_int4(const K2Maps &maps, const K2Params &p, cudaStream_t s);
 

@@ -28,6 +28,22 @@
 #include "formats.cuh"
 #include "k1_launch.h"
 #include "sm100.cuh"
+#include "k2_epilogue.cuh"
+#ifndef SVDQ_EXP
+#define SVDQ_EXP 0
+#endif
+
+#ifdef SVDQ_TRACE
+namespace svdq { __device__ unsigned long long g_k2_trace[148][8]; }
+extern "C" int svdq_k2_trace_read(unsigned long long *host) {
+  return cudaMemcpyFromSymbol(host, svdq::g_k2_trace, sizeof(unsigned long long) * 148 * 8) == cudaSuccess ? 0 : 1;
+}
+#define K2T_BEGIN() long long _t0 = clock64()
+#define K2T_ACC(v) (v) += clock64() - _t0
+#else
+#define K2T_BEGIN() do {} while (0)
+#define K2T_ACC(v) do {} while (0)
+#endif
 
 namespace svdq {
 
@@ -40,11 +56,12 @@ struct NvCfg {
   static constexpr int SFA_BYTES = 4 * 512;              // 128 rows x 16 sf
   static constexpr int SFB_BYTES = 2 * 4 * 512;          // two 128-row atoms x 16 sf
   static constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
-  static constexpr int kStages = (200 * 1024) / STAGE;
+  static constexpr int EPI_BYTES = 4 * 2 * 4096;          // per epilogue warp: two 4 KB staging buffers
+  static constexpr int kStages = (225 * 1024 - EPI_BYTES - 2048) / STAGE;
   static constexpr int SF_COLS = 16 + 32;                // TMEM columns per SF slot
   static constexpr int SF_BASE = 2 * BN;
   static constexpr int BAR_BYTES = 256;
-  static constexpr int SMEM = kStages * STAGE + BAR_BYTES + BN * 4 + 1024;
+  static constexpr int SMEM = kStages * STAGE + EPI_BYTES + BAR_BYTES + BN * 4 + 1024;
   static_assert(STAGE % 1024 == 0, "stage must keep 1024-B alignment");
   static_assert(SF_BASE + 2 * SF_COLS <= 512, "TMEM budget");
   static_assert(kStages >= 3, "pipeline depth");
@@ -97,18 +114,19 @@ template <int BN>
 __global__ void __launch_bounds__(192, 1)
     k2_nvfp4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmL,
-                    const K2Params p) {
+                    const __grid_constant__ CUtensorMap tmY, const K2Params p) {
   using C = NvCfg<BN>;
   constexpr int S = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~static_cast<uintptr_t>(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * C::STAGE);
+  uint8_t *epi_stage = smem + S * C::STAGE;             // 1024-aligned TMA-store staging
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * C::STAGE + C::EPI_BYTES);
   uint64_t *empty = full + S;
   uint64_t *acc_full = empty + S;      // [2]
   uint64_t *acc_empty = acc_full + 2;  // [2]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
-  float *bias_s = reinterpret_cast<float *>(smem + S * C::STAGE + C::BAR_BYTES);
+  float *bias_s = reinterpret_cast<float *>(smem + S * C::STAGE + C::EPI_BYTES + C::BAR_BYTES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -147,6 +165,10 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
+#ifdef SVDQ_TRACE
+      long long t_prod_wait = 0;
+      const long long t_start = clock64();
+#endif
       int s = 0;
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -157,7 +179,7 @@ __global__ void __launch_bounds__(192, 1)
         const int natom = static_cast<int>(atom_last - atom0 + 1);   // 1 or 2 atoms cover the tile
         for (int kt = 0; kt < nkt; ++kt) {
           const int nsub = min(4, nkb64 - kt * 4);
-          mbar_wait(&empty[s], ph ^ 1);
+          { K2T_BEGIN(); mbar_wait(&empty[s], ph ^ 1); K2T_ACC(t_prod_wait); }
           uint8_t *st = smem + s * C::STAGE;
           mbar_arrive_expect_tx(&full[s], C::A_BYTES + C::B_BYTES + nsub * 512 * (1 + natom));
           tma_load_2d(st, &tmA, &full[s], kt * C::BKB, static_cast<int32_t>(m0));
@@ -178,6 +200,9 @@ __global__ void __launch_bounds__(192, 1)
           if (++s == S) { s = 0; ph ^= 1; }
         }
       }
+#ifdef SVDQ_TRACE
+      if (blockIdx.x < 148) { g_k2_trace[blockIdx.x][0] = t_prod_wait; g_k2_trace[blockIdx.x][1] = clock64() - t_start; }
+#endif
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -186,23 +211,23 @@ __global__ void __launch_bounds__(192, 1)
     int s = 0;
     uint32_t ph = 0;
     int acc_i = 0;
-    // SF slot bookkeeping: the pipeline stage / phase whose MMAs last read each slot
-    int slot_stage[2] = {-1, -1};
-    uint32_t slot_phase[2] = {0, 0};
     int sf_i = 0;
+#ifdef SVDQ_TRACE
+    long long t_acc = 0, t_slot = 0, t_full = 0;
+    const long long t_start = clock64();
+#endif
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++acc_i) {
       const int b = acc_i & 1;
       const uint32_t acc_ph = (acc_i >> 1) & 1;
       const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
       const uint32_t sfb_off = static_cast<uint32_t>((n0 % 128) / 32);
       const uint32_t d_tmem = tmem + b * BN;
-      mbar_wait(&acc_empty[b], acc_ph ^ 1);             // epilogue drained this buffer
+      { K2T_BEGIN(); mbar_wait(&acc_empty[b], acc_ph ^ 1); K2T_ACC(t_acc); }   // epilogue drained this buffer
       tc_fence_after();
       for (int kt = 0; kt < nkt; ++kt) {
         const int nsub = min(4, nkb64 - kt * 4);
         const int slot = sf_i & 1;
-        if (slot_stage[slot] >= 0) mbar_wait(&empty[slot_stage[slot]], slot_phase[slot]);
-        mbar_wait(&full[s], ph);
+        { K2T_BEGIN(); mbar_wait(&full[s], ph); K2T_ACC(t_full); }
         tc_fence_after();
         if (elect_one()) {
           uint8_t *st = smem + s * C::STAGE;
@@ -212,19 +237,45 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t sfb_addr = sfa_addr + C::SFA_BYTES;
           const uint32_t sfa_col = tmem + C::SF_BASE + slot * C::SF_COLS;
           const uint32_t sfb_col = sfa_col + 16;
-          for (int i = 0; i < nsub; ++i) {
-            tmem_cp_32x128b_warpx4(sfa_col + 4 * i, sdesc_cp_32x128b(sfa_addr + i * 512));
-            tmem_cp_32x128b_warpx4(sfb_col + 8 * i, sdesc_cp_32x128b(sfb_addr + i * 512));
-            tmem_cp_32x128b_warpx4(sfb_col + 8 * i + 4, sdesc_cp_32x128b(sfb_addr + 2048 + i * 512));
-          }
-          for (int i = 0; i < nsub; ++i)
-            mma_nvfp4(d_tmem, sdesc_kmajor_sw128(a_addr + 32 * i), sdesc_kmajor_sw128(b_addr + 32 * i),
-                      idesc_q, sfa_col + 4 * i, sfb_col + 8 * i + sfb_off, (kt | i) != 0);
+            // descriptors: +16 B in smem = +1 in the start-address field (no carry: smem < 256 KB)
+            const uint64_t sfa_d = sdesc_cp_32x128b(sfa_addr), sfb_d = sdesc_cp_32x128b(sfb_addr);
+            const uint64_t a_d = sdesc_kmajor_sw128(a_addr), b_d = sdesc_kmajor_sw128(b_addr);
+            if (nsub == 4) {
+            #pragma unroll
+              for (int i = 0; i < 4; ++i) {
+#if SVDQ_EXP < 2
+                tmem_cp_32x128b_warpx4(sfa_col + 4 * i, sfa_d + 32 * i);
+#endif
+#if SVDQ_EXP < 1
+                tmem_cp_32x128b_warpx4(sfb_col + 8 * i, sfb_d + 32 * i);
+#endif
+#if SVDQ_EXP < 1
+                tmem_cp_32x128b_warpx4(sfb_col + 8 * i + 4, sfb_d + 128 + 32 * i);
+#endif
+              }
+            #pragma unroll
+              for (int i = 0; i < 4; ++i)
+                mma_nvfp4(d_tmem, a_d + 2 * i, b_d + 2 * i, idesc_q, sfa_col + 4 * i, sfb_col + 8 * i + sfb_off,
+                      (kt | i) != 0);
+            } else {
+              for (int i = 0; i < nsub; ++i) {
+#if SVDQ_EXP < 2
+                tmem_cp_32x128b_warpx4(sfa_col + 4 * i, sfa_d + 32 * i);
+#endif
+#if SVDQ_EXP < 1
+                tmem_cp_32x128b_warpx4(sfb_col + 8 * i, sfb_d + 32 * i);
+#endif
+#if SVDQ_EXP < 1
+                tmem_cp_32x128b_warpx4(sfb_col + 8 * i + 4, sfb_d + 128 + 32 * i);
+#endif
+              }
+              for (int i = 0; i < nsub; ++i)
+                mma_nvfp4(d_tmem, a_d + 2 * i, b_d + 2 * i, idesc_q, sfa_col + 4 * i, sfb_col + 8 * i + sfb_off,
+                      (kt | i) != 0);
+            }
           tc_commit(&empty[s]);
         }
         __syncwarp();
-        slot_stage[slot] = s;
-        slot_phase[slot] = ph;
         ++sf_i;
         if (++s == S) { s = 0; ph ^= 1; }
       }
@@ -247,12 +298,19 @@ __global__ void __launch_bounds__(192, 1)
       if (elect_one()) tc_commit(&acc_full[b]);
       __syncwarp();
     }
+#ifdef SVDQ_TRACE
+    if (lane == 0 && blockIdx.x < 148) {
+      g_k2_trace[blockIdx.x][2] = t_acc; g_k2_trace[blockIdx.x][3] = t_slot; g_k2_trace[blockIdx.x][4] = t_full;
+      g_k2_trace[blockIdx.x][5] = clock64() - t_start;
+    }
+#endif
   } else {
     // ------------------------------------------------------------ epilogue
     const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
     const int row = quad * 32 + lane;
     const int et = threadIdx.x - 64;           // 0..127
     int acc_i = 0;
+    int ebuf = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++acc_i) {
       const int b = acc_i & 1;
       const uint32_t acc_ph = (acc_i >> 1) & 1;
@@ -266,31 +324,16 @@ __global__ void __launch_bounds__(192, 1)
       named_bar(1, 128);
       mbar_wait(&acc_full[b], acc_ph);
       tc_fence_after();
-#pragma unroll 1
-      for (int cc = 0; cc < BN / 32; ++cc) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16) + cc * 32, r);
-        tmem_ld_wait();
-        if (grow < p.M) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int64_t col = n0 + cc * 32 + j * 8;
-            if (col < p.N) {
-              float v[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e)
-                v[e] = __fadd_rn(__fmul_rn(p.alpha, __uint_as_float(r[j * 8 + e])),
-                                 bias_s[cc * 32 + j * 8 + e]);
-              store8(p.Y, p.y_dtype, p.ldy, grow, col, v);
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[b]);
+      epilogue_tile<BN>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype, &tmY,
+                        static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0),
+                        epi_stage + (warp - 2) * 8192, ebuf, lane, [&]() {
+                          tc_fence_before();
+                          __syncwarp();
+                          if (lane == 0) mbar_arrive(&acc_empty[b]);
+                        });
     }
   }
+  if (warp >= 2 && lane == 0) bulk_wait_group<0>();    // outstanding TMA stores done
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
@@ -310,7 +353,7 @@ static cudaError_t launch_bn(const K2Maps &maps, const K2Params &p, cudaStream_t
   }
   const int64_t tiles = ((p.M + 127) / 128) * ((p.N + BN - 1) / BN);
   const unsigned grid = static_cast<unsigned>(tiles < num_sms ? tiles : num_sms);
-  kern<<<grid, 192, C::SMEM, s>>>(maps.a, maps.b, maps.xl1, maps.l2, p);
+  kern<<<grid, 192, C::SMEM, s>>>(maps.a, maps.b, maps.xl1, maps.l2, maps.y, p);
   return cudaGetLastError();
 }
 

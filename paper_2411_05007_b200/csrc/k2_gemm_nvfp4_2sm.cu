@@ -1,0 +1,344 @@
+// K2 (NVFP4), CTA-pair version: the same fused GEMM as k2_gemm_nvfp4.cu
+// ("Fused 4-Bit Compute + Up Projection", Fig. 5(b); Eq. 5), run on
+// a cluster of two CTAs with tcgen05 cta_group::2 so that a 256 x 192 output tile
+// is computed by two SMs that each stage only HALF of the B (weight) tile:
+//   CTA rank c of the pair holds A rows [m0 + 128c, +128) and B rows [n0 + 96c, +96)
+//   in its shared memory, its own SFA rows and a full copy of the tile's SFB; the
+//   leader (rank 0) alone issues tcgen05.cp / tcgen05.mma .cta_group::2, which read
+//   both CTAs' shared memory at the same offsets and write each CTA's TMEM
+//   (D rows of that CTA's A half, all 192 columns).
+// Why: the 1-CTA kernel is bounded by operand delivery into each SM (ncu: ~9.5 TB/s
+// of TMA loads at 33 % tensor-pipe activity); halving B per SM raises the FLOP per
+// byte each SM ingests from ~300 to ~370 (and halves B reads from L2).
+//
+// Warp roles per CTA (192 threads): warp 0 TMA producer (both CTAs; bytes land on the
+// leader's full barrier), warp 1 TMEM allocator (both) + MMA issuer (leader), warps
+// 2..5 epilogue (both; release the accumulator buffer to the leader's barrier).
+// TMEM per CTA: acc0 [0,192), acc1 [192,384), two SF slots of 48 columns.
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "formats.cuh"
+#include "k1_launch.h"
+#include "sm100.cuh"
+#include "k2_epilogue.cuh"
+#ifndef SVDQ_EXP
+#define SVDQ_EXP 0
+#endif
+
+#ifdef SVDQ_TRACE
+namespace svdq { __device__ unsigned long long g_k2p_trace[148][8]; }
+extern "C" int svdq_k2p_trace_read(unsigned long long *host) {
+  return cudaMemcpyFromSymbol(host, svdq::g_k2p_trace, sizeof(unsigned long long) * 148 * 8) == cudaSuccess ? 0 : 1;
+}
+#define K2T_BEGIN() long long _t0 = clock64()
+#define K2T_ACC(v) (v) += clock64() - _t0
+#else
+#define K2T_BEGIN() do {} while (0)
+#define K2T_ACC(v) do {} while (0)
+#endif
+
+namespace svdq {
+
+namespace {
+
+constexpr int BN = 192;                       // pair tile N
+constexpr int BNH = BN / 2;                   // B rows per CTA
+constexpr int A_BYTES = 128 * 128;            // 16 KB
+constexpr int B_BYTES = BNH * 128;            // 12 KB
+constexpr int SFA_BYTES = 2048;
+constexpr int SFB_BYTES = 4096;               // two 128-row atoms x 4 K-blocks
+constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;   // 34 KB
+constexpr int kStages = 5;
+constexpr int SF_COLS = 48;
+constexpr int SF_BASE = 2 * BN;
+constexpr int EPI_OFF = kStages * STAGE;                 // 4 epilogue warps x two 4 KB staging buffers
+constexpr int BAR_OFF = EPI_OFF + 4 * 8192;
+constexpr int SMEM = BAR_OFF + 256 + BN * 4 + 1024;
+static_assert(STAGE % 1024 == 0, "stage alignment");
+static_assert(SF_BASE + 2 * SF_COLS <= 512, "TMEM budget");
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ float load_bias(const void *b, int dt, int64_t i) {
+  if (dt == 0) return __bfloat162float(static_cast<const __nv_bfloat16 *>(b)[i]);
+  if (dt == 1) return __half2float(static_cast<const __half *>(b)[i]);
+  return static_cast<const float *>(b)[i];
+}
+__device__ __forceinline__ void store8(void *Y, int dt, int64_t ldy, int64_t row, int64_t col, const float (&v)[8]) {
+  if (dt == 2) {
+    float4 *p = reinterpret_cast<float4 *>(static_cast<float *>(Y) + row * ldy + col);
+    p[0] = make_float4(v[0], v[1], v[2], v[3]);
+    p[1] = make_float4(v[4], v[5], v[6], v[7]);
+    return;
+  }
+  uint32_t w[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (dt == 0)
+      w[j] = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(v[2 * j]))) |
+             (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(v[2 * j + 1]))) << 16);
+    else
+      w[j] = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(v[2 * j]))) |
+             (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(v[2 * j + 1]))) << 16);
+  }
+  *reinterpret_cast<uint4 *>(static_cast<uint16_t *>(Y) + row * ldy + col) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__global__ void __launch_bounds__(192, 1)
+    k2_nvfp4_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmL,
+                        const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
+                        const __grid_constant__ CUtensorMap tmY, const K2Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~static_cast<uintptr_t>(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + BAR_OFF);
+  uint64_t *empty = full + kStages;
+  uint64_t *acc_full = empty + kStages;   // [2]
+  uint64_t *acc_empty = acc_full + 2;     // [2] (leader's copy is the one used)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+  float *bias_s = reinterpret_cast<float *>(smem + BAR_OFF + 256);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();             // 0 leader, 1 peer
+  const int pair = static_cast<int>(blockIdx.x >> 1);
+  const int npairs = static_cast<int>(gridDim.x >> 1);
+  const int nkb64 = static_cast<int>(p.K / 64);
+  const int nkt = (nkb64 + 3) / 4;
+  const int nslab = (p.rank + 63) / 64;
+  const int mt_count = static_cast<int>((p.M + 255) / 256);
+  const int nt_count = static_cast<int>((p.N + BN - 1) / BN);
+  const int tiles = mt_count * nt_count;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 8);                       // 4 epilogue warps x 2 CTAs
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    tma_prefetch(&tmSFA);
+    tma_prefetch(&tmSFB);
+    if (nslab) {
+      tma_prefetch(&tmX);
+      tma_prefetch(&tmL);
+    }
+  }
+  if (warp == 1) tmem_alloc_cg2(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();                                        // barriers of both CTAs initialised
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (elect_one()) {
+      const uint32_t full0 = mapa_u32(&full[0], 0);      // leader's barriers
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = pair; t < tiles; t += npairs) {
+        const int64_t m0 = static_cast<int64_t>(t % mt_count) * 256;
+        const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
+        const int32_t ma = static_cast<int32_t>(m0 + 128 * crank);
+        const int32_t nb = static_cast<int32_t>(n0 + BNH * crank);
+        for (int kt = 0; kt < nkt; ++kt) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t *st = smem + s * STAGE;
+          const uint32_t fb = full0 + s * 8;
+          if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE);
+          tma_load_2d_cg2(st, &tmA, fb, kt * 128, ma);
+          tma_load_2d_cg2(st + A_BYTES, &tmB, fb, kt * 128, nb);
+          tma_load_3d_cg2(st + A_BYTES + B_BYTES, &tmSFA, fb, 0, kt * 4, static_cast<int32_t>(m0 / 128 + crank));
+          tma_load_3d_cg2(st + A_BYTES + B_BYTES + SFA_BYTES, &tmSFB, fb, 0, kt * 4,
+                          static_cast<int32_t>(n0 / 128));
+          if (++s == kStages) { s = 0; ph ^= 1; }
+        }
+        for (int j = 0; j < nslab; ++j) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t *st = smem + s * STAGE;
+          const uint32_t fb = full0 + s * 8;
+          if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
+          tma_load_2d_cg2(st, &tmX, fb, j * 64, ma);
+          tma_load_2d_cg2(st + A_BYTES, &tmL, fb, j * 64, nb);
+          if (++s == kStages) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader)
+    if (crank == 0) {
+      constexpr uint32_t idesc_q = idesc_nvfp4(256, BN);
+      constexpr uint32_t idesc_h = idesc_bf16(256, BN);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc_i = 0;
+      int sf_i = 0;
+#ifdef SVDQ_TRACE
+      long long t_acc = 0, t_full = 0;
+      const long long t_start = clock64();
+#endif
+      for (int t = pair; t < tiles; t += npairs, ++acc_i) {
+        const int b = acc_i & 1;
+        const uint32_t acc_ph = (acc_i >> 1) & 1;
+        const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
+        const uint32_t sfb_off = static_cast<uint32_t>((n0 % 128) / 32);
+        const uint32_t d_tmem = tmem + b * BN;
+        { K2T_BEGIN(); mbar_wait(&acc_empty[b], acc_ph ^ 1); K2T_ACC(t_acc); }
+        tc_fence_after();
+        for (int kt = 0; kt < nkt; ++kt) {
+          const int nsub = min(4, nkb64 - kt * 4);
+          const int slot = sf_i & 1;
+          { K2T_BEGIN(); mbar_wait(&full[s], ph); K2T_ACC(t_full); }
+          tc_fence_after();
+          if (elect_one()) {
+            uint8_t *st = smem + s * STAGE;
+            const uint32_t a_addr = smem_u32(st);
+            const uint32_t b_addr = smem_u32(st + A_BYTES);
+            const uint32_t sfa_addr = smem_u32(st + A_BYTES + B_BYTES);
+            const uint32_t sfb_addr = sfa_addr + SFA_BYTES;
+            const uint32_t sfa_col = tmem + SF_BASE + slot * SF_COLS;
+            const uint32_t sfb_col = sfa_col + 16;
+            // descriptors: +16 B in smem = +1 in the start-address field (no carry: smem < 256 KB)
+            const uint64_t sfa_d = sdesc_cp_32x128b(sfa_addr), sfb_d = sdesc_cp_32x128b(sfb_addr);
+            const uint64_t a_d = sdesc_kmajor_sw128(a_addr), b_d = sdesc_kmajor_sw128(b_addr);
+            if (nsub == 4) {
+            #pragma unroll
+              for (int i = 0; i < 4; ++i) {
+#if SVDQ_EXP < 2
+                tmem_cp_32x128b_warpx4_cg2(sfa_col + 4 * i, sfa_d + 32 * i);
+#endif
+#if SVDQ_EXP < 1
+                tmem_cp_32x128b_warpx4_cg2(sfb_col + 8 * i, sfb_d + 32 * i);
+#endif
+#if SVDQ_EXP < 1
+                tmem_cp_32x128b_warpx4_cg2(sfb_col + 8 * i + 4, sfb_d + 128 + 32 * i);
+#endif
+              }
+            #pragma unroll
+              for (int i = 0; i < 4; ++i)
+                mma_nvfp4_cg2(d_tmem, a_d + 2 * i, b_d + 2 * i, idesc_q, sfa_col + 4 * i, sfb_col + 8 * i + sfb_off,
+                      (kt | i) != 0);
+            } else {
+              for (int i = 0; i < nsub; ++i) {
+#if SVDQ_EXP < 2
+                tmem_cp_32x128b_warpx4_cg2(sfa_col + 4 * i, sfa_d + 32 * i);
+#endif
+#if SVDQ_EXP < 1
+                tmem_cp_32x128b_warpx4_cg2(sfb_col + 8 * i, sfb_d + 32 * i);
+#endif
+#if SVDQ_EXP < 1
+                tmem_cp_32x128b_warpx4_cg2(sfb_col + 8 * i + 4, sfb_d + 128 + 32 * i);
+#endif
+              }
+              for (int i = 0; i < nsub; ++i)
+                mma_nvfp4_cg2(d_tmem, a_d + 2 * i, b_d + 2 * i, idesc_q, sfa_col + 4 * i, sfb_col + 8 * i + sfb_off,
+                      (kt | i) != 0);
+            }
+            tc_commit_cg2_mc(&empty[s], 0x3);
+          }
+          __syncwarp();
+          ++sf_i;
+          if (++s == kStages) { s = 0; ph ^= 1; }
+        }
+        for (int j = 0; j < nslab; ++j) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          if (elect_one()) {
+            uint8_t *st = smem + s * STAGE;
+            const uint32_t a_addr = smem_u32(st);
+            const uint32_t b_addr = smem_u32(st + A_BYTES);
+            const int nk16 = min(4, (p.rank - j * 64) / 16);
+            for (int i = 0; i < nk16; ++i)
+              mma_bf16_cg2(d_tmem, sdesc_kmajor_sw128(a_addr + 32 * i), sdesc_kmajor_sw128(b_addr + 32 * i),
+                           idesc_h, (nkt > 0 || j > 0 || i > 0) ? 1u : 0u);
+            tc_commit_cg2_mc(&empty[s], 0x3);
+          }
+          __syncwarp();
+          if (++s == kStages) { s = 0; ph ^= 1; }
+        }
+        if (elect_one()) tc_commit_cg2_mc(&acc_full[b], 0x3);
+        __syncwarp();
+      }
+#ifdef SVDQ_TRACE
+      if (lane == 0 && pair < 148) {
+        g_k2p_trace[pair][0] = t_acc; g_k2p_trace[pair][1] = t_full; g_k2p_trace[pair][2] = clock64() - t_start;
+      }
+#endif
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const int et = threadIdx.x - 64;
+    const uint32_t acc_empty0 = mapa_u32(&acc_empty[0], 0);
+    int acc_i = 0;
+    int ebuf = 0;
+    for (int t = pair; t < tiles; t += npairs, ++acc_i) {
+      const int b = acc_i & 1;
+      const uint32_t acc_ph = (acc_i >> 1) & 1;
+      const int64_t m0 = static_cast<int64_t>(t % mt_count) * 256 + 128 * crank;
+      const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
+      const int64_t grow = m0 + row;
+      named_bar(1, 128);
+      for (int c = et; c < BN; c += 128)
+        bias_s[c] = (p.bias && n0 + c < p.N) ? load_bias(p.bias, p.bias_dtype, n0 + c) : 0.f;
+      named_bar(1, 128);
+      mbar_wait(&acc_full[b], acc_ph);
+      tc_fence_after();
+      epilogue_tile<BN>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype, &tmY,
+                        static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0),
+                        smem + EPI_OFF + (warp - 2) * 8192, ebuf, lane, [&]() {
+                          tc_fence_before();
+                          __syncwarp();
+                          if (lane == 0) mbar_arrive_cluster(acc_empty0 + b * 8);
+                        });
+    }
+  }
+  if (warp >= 2 && lane == 0) bulk_wait_group<0>();    // outstanding TMA stores done
+  tc_fence_before();
+  cluster_sync();                                        // all MMAs, loads and reads are done
+  if (warp == 1) tmem_dealloc_cg2(tmem, 512);
+}
+
+}  // namespace
+
+cudaError_t launch_k2_nvfp4_2sm(const K2Maps &maps, const CUtensorMap &sfa, const CUtensorMap &sfb,
+                                const K2Params &p, cudaStream_t s) {
+  static_assert(SMEM <= 227 * 1024, "smem budget");
+  cudaError_t e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  if (e != cudaSuccess) return e;
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t tiles = ((p.M + 255) / 256) * ((p.N + BN - 1) / BN);
+  const int64_t pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs), 1, 1);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k2_nvfp4_2sm_kernel, maps.a, maps.b, maps.xl1, maps.l2, sfa, sfb, maps.y, p);
+}
+
+}  // namespace svdq
