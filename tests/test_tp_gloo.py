@@ -1,0 +1,108 @@
+"""Multi-process (world_size 2, gloo on CPU) tests of the tensor-parallel host logic:
+operand sharding along N (including the NVFP4 128x4 scale-factor layout), the
+all-gather, and the column reassembly.  The per-shard GEMM here is the ORACLE (test
+infrastructure) standing in for K2, so the test pins the partitioning logic: the
+reassembled sharded result must equal the unsharded result bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from helpers import make_case, pack_weight
+from oracle import formats as F
+from oracle import svdquant as S
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _unpack_shard(ops, shard, n):
+    """Device-layout shard buffers -> oracle Operands of the shard."""
+    K = ops.K
+    codes = F.unpack_nibbles(shard.w_codes.numpy().reshape(n, K // 2))
+    if ops.fmt == "nvfp4":
+        scales = F.sf_from_layout(shard.w_scales.numpy(), n, K)
+    else:
+        codes = F.nibble_to_int4(codes)
+        scales = shard.w_scales.numpy().view(np.uint16).reshape(n, K // 64)
+    l2s = shard.l2s.numpy().view(np.uint16).reshape(n, ops.rank)
+    bias = shard.bias.numpy().astype(np.float32) if shard.bias is not None else None
+    return S.Operands(ops.fmt, K, n, ops.rank, codes, scales, ops.scale_dtype, ops.gs_w, ops.gs_x,
+                      ops.lam_inv32, ops.L1s_bits, l2s, bias)
+
+
+def _worker(rank, world, port, fmt, N, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2411_05007_b200 as P
+        from paper_2411_05007_b200 import tp
+        M, K, r = 48, 256, 16
+        x, w, lam, ops = make_case(fmt, M, K, N, r, seed=5, cfg=21)
+        codes, scales = pack_weight(ops)
+        full = P.QuantizedLinear(
+            fmt, K, N, r, torch.from_numpy(codes.reshape(-1).copy()), torch.from_numpy(scales.reshape(-1).copy()),
+            torch.from_numpy(ops.lam_inv32.copy()), torch.from_numpy(ops.L1s_bits.view(np.int16).reshape(-1).copy()),
+            torch.from_numpy(ops.L2s_bits.view(np.int16).reshape(-1).copy()),
+            torch.from_numpy(ops.bias.astype(np.float32)), ops.scale_dtype if fmt == "int4" else "bf16",
+            float(ops.gs_w), float(ops.gs_x))
+        shard = tp.shard_layer(full, world, rank)
+        n0, n = tp.shard_bounds(N, world, rank)
+        sops = _unpack_shard(ops, shard, n)
+        qa = S.quantize_activation(x, ops)                 # K1 output is identical on every rank
+        y_local = torch.from_numpy(S.gemm_reference(qa, sops))   # oracle stands in for K2
+        blocks = torch.empty(world * M, n, dtype=torch.float64)
+        dist.all_gather_into_tensor(blocks, y_local.contiguous())
+        y = tp.assemble_columns(blocks, world).numpy()
+        if rank == 0:
+            q.put(("ok", y, S.gemm_reference(qa, ops)))
+    except Exception as e:  # pragma: no cover - surfaced through the queue
+        q.put(("err", repr(e), None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fmt,N", [("nvfp4", 512), ("nvfp4", 320), ("int4", 320)])
+def test_column_parallel_gloo_bitwise(fmt, N):
+    """N = 512: shards are whole 128-row scale-factor atoms; N = 320: shard width 160
+    forces the byte-gather re-layout of the 128x4 scale factors."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world = 2
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fmt, N, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    status, y, ref = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+    assert status == "ok", y
+    np.testing.assert_array_equal(y, ref)
+
+
+def test_shard_bounds_validation():
+    from paper_2411_05007_b200 import tp
+    assert tp.shard_bounds(3072, 8, 3) == (1152, 384)
+    with pytest.raises(ValueError):
+        tp.shard_bounds(100, 3, 0)
+    with pytest.raises(ValueError):
+        tp.shard_bounds(3072, 256, 0)       # 12-wide shards
+
+
+def test_assemble_columns():
+    from paper_2411_05007_b200 import tp
+    a = torch.arange(2 * 3 * 4).reshape(2 * 3, 4)      # world 2, M 3, n 4
+    out = tp.assemble_columns(a, 2)
+    assert out.shape == (3, 8)
+    assert out[1].tolist() == [4, 5, 6, 7, 16, 17, 18, 19]
