@@ -23,6 +23,7 @@
 
 #include "formats.cuh"
 #include "k1_launch.h"
+#include "sm100.cuh"
 
 namespace svdq {
 
@@ -88,6 +89,8 @@ __global__ void __launch_bounds__(256, 1)
       for (int i = 0; i < 4; ++i) acc[mt][nt][i] = 0.f;
 
   // NVFP4 constants (App. B.2): t = fl32(fl32(1/gs) * fl32(1/6))
+  griddep_launch_dependents();
+  griddep_wait();                                    // X may be the previous kernel's output
   const float enc = __fdiv_rn(1.0f, p.gs_x);
   const float t6 = __fmul_rn(enc, __fdiv_rn(1.0f, 6.0f));
 
@@ -278,8 +281,7 @@ static cudaError_t launch_k1_t(const K1Params &p, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
   }
   const unsigned grid = static_cast<unsigned>(p.Mpad / BM);
-  kern<<<grid, 256, smem, stream>>>(p);
-  return cudaGetLastError();
+  return launch_ex(kern, dim3(grid), dim3(256), smem, stream, 1u, p);
 }
 
 template <int kFmt, bool kXBf16, bool kScaleBf16, int MT>

@@ -71,8 +71,8 @@ __host__ __device__ inline K1Layout k1_layout(int rank) {
   L.stage_bytes = ((16384 + rank * 128 + 256) + 1023) / 1024 * 1024;
   L.red_stride = rank + 2;                       // padded row stride (floats, even: float2 reads)
   const size_t red = rank ? static_cast<size_t>(128) * L.red_stride * 4 : 0;
-  int s = static_cast<int>((150 * 1024 - red) / L.stage_bytes);
-  L.stages = s > 8 ? 8 : (s < 2 ? 2 : s);
+  int s = static_cast<int>((205 * 1024 - red) / L.stage_bytes);
+  L.stages = s > 12 ? 12 : (s < 2 ? 2 : s);
   L.red_off = static_cast<size_t>(L.stages) * L.stage_bytes;
   L.bar_off = (L.red_off + red + 15) / 16 * 16;
   L.smem = L.bar_off + 256 + 1024 + 1024;     // + 256-entry qinv table
@@ -91,8 +91,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int S = Ly.stages;
   float *red = reinterpret_cast<float *>(smem + Ly.red_off);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + Ly.bar_off);
-  uint64_t *empty = full + 8;
-  uint64_t *dfull = empty + 8;
+  uint64_t *empty = full + 12;
+  uint64_t *dfull = empty + 12;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dfull + 1);
   float *qinv_lut = reinterpret_cast<float *>(smem + Ly.bar_off + 256);
 
@@ -104,7 +104,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kb_begin = crank * nkb / ks;
   const int nsteps = (crank + 1) * nkb / ks - kb_begin;
   const int64_t row0 = static_cast<int64_t>(blockIdx.y) * 128;
-  const uint32_t tcols = r <= 32 ? 32 : (r <= 64 ? 64 : 128);
+  // four accumulators (one per 16-wide K sub-step) so consecutive MMAs are independent
+  const uint32_t tcols = 4 * r <= 128 ? 128 : (4 * r <= 256 ? 256 : 512);
 
   if (threadIdx.x == 0) TRACE(0);
 #ifdef SVDQ_TRACE
@@ -139,10 +140,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = r ? *tmem_slot : 0;
   if (threadIdx.x == 0) TRACE(1);
+  griddep_launch_dependents();                       // next kernel may start its prologue
 
   if (warp == 0) {
     // ---------------------------------------------------------------- producer
     if (elect_one()) {
+      griddep_wait();                                  // X may be the previous kernel's output
       const uint32_t bytes = 16384 + r * 128 + 256;
       // warm L2 with the first ring's worth of X tiles beyond what the smem ring holds
       for (int i = S; i < nsteps && i < 2 * S; ++i)
@@ -175,8 +178,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t la = xa + 16384;
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            mma_bf16(tmem, sdesc_kmajor_sw128(xa + 32 * j), sdesc_kmajor_sw128(la + 32 * j), idesc,
-                     (i | j) != 0);
+            mma_bf16(tmem + j * r, sdesc_kmajor_sw128(xa + 32 * j), sdesc_kmajor_sw128(la + 32 * j), idesc,
+                     i != 0);
           tc_commit(&empty[s]);
         }
         __syncwarp();
@@ -240,10 +243,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const uint32_t o0 = __shfl_down_sync(0xffffffffu, sfb[0], 2);
         const uint32_t o1 = __shfl_down_sync(0xffffffffu, sfb[1], 2);
-        if (rvalid) {
-          *reinterpret_cast<uint32_t *>(xq_row + kb * 32 + q * 4) = codes[0];
-          *reinterpret_cast<uint32_t *>(xq_row + kb * 32 + 16 + q * 4) = codes[1];
-        }
+        // regroup so lane q writes bytes [8q, 8q+8) of the row's 32-byte block: full-sector
+        // 8-byte stores (q0: c0 of q0,q1; q1: c0 of q2,q3; q2: c1 of q0,q1; q3: c1 of q2,q3)
+        const uint32_t src0 = (lane & ~3u) | ((q & 1) * 2);
+        const uint32_t a0 = __shfl_sync(0xffffffffu, codes[0], src0);
+        const uint32_t a1 = __shfl_sync(0xffffffffu, codes[0], src0 + 1);
+        const uint32_t b0 = __shfl_sync(0xffffffffu, codes[1], src0);
+        const uint32_t b1 = __shfl_sync(0xffffffffu, codes[1], src0 + 1);
+        if (rvalid)
+          *reinterpret_cast<uint2 *>(xq_row + kb * 32 + q * 8) = q < 2 ? make_uint2(a0, a1) : make_uint2(b0, b1);
         if (q == 0)
           *reinterpret_cast<uint32_t *>(sf_row + kb * 512) = sfb[0] | (o0 << 8) | (sfb[1] << 16) | (o1 << 24);
       } else {
@@ -257,18 +265,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint16_t sc = scale16_rn_sat<kScaleBf16>(__fdiv_rn(amax, 7.0f));
         const float sd = scale16_to_f32<kScaleBf16>(sc);
         const float qinv = sd == 0.f ? 0.f : __frcp_rn(sd);
-        if (rvalid) {
+        uint32_t words[2];
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint32_t word = 0;
+        for (int c = 0; c < 2; ++c) {
+          uint32_t word = 0;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              int v = __float2int_rn(__fmul_rn(xh[c][j], qinv));
-              v = max(-7, min(7, v));
-              word |= (static_cast<uint32_t>(v) & 0xFu) << (4 * j);
-            }
-            *reinterpret_cast<uint32_t *>(xq_row + kb * 32 + c * 16 + q * 4) = word;
+          for (int j = 0; j < 8; ++j) {
+            int v = __float2int_rn(__fmul_rn(xh[c][j], qinv));
+            v = max(-7, min(7, v));
+            word |= (static_cast<uint32_t>(v) & 0xFu) << (4 * j);
           }
+          words[c] = word;
+        }
+        const uint32_t src0 = (lane & ~3u) | ((q & 1) * 2);
+        const uint32_t a0 = __shfl_sync(0xffffffffu, words[0], src0);
+        const uint32_t a1 = __shfl_sync(0xffffffffu, words[0], src0 + 1);
+        const uint32_t b0 = __shfl_sync(0xffffffffu, words[1], src0);
+        const uint32_t b1 = __shfl_sync(0xffffffffu, words[1], src0 + 1);
+        if (rvalid) {
+          *reinterpret_cast<uint2 *>(xq_row + kb * 32 + q * 8) = q < 2 ? make_uint2(a0, a1) : make_uint2(b0, b1);
           if (q == 0) s16_row[kb] = sc;
         }
       }
@@ -287,11 +302,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait_spin(dfull, 0);
     tc_fence_after();
     for (int c16 = 0; c16 < r / 16; ++c16) {
-      uint32_t v[16];
-      tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(quad * 32) << 16) + c16 * 16, v);
-      tmem_ld_wait();
+      float acc[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) red[rl * Ly.red_stride + c16 * 16 + j] = __uint_as_float(v[j]);
+      for (int a = 0; a < 4; ++a) {                   // fixed accumulator order: deterministic
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(quad * 32) << 16) + a * r + c16 * 16, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = a == 0 ? __uint_as_float(v[j]) : acc[j] + __uint_as_float(v[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) red[rl * Ly.red_stride + c16 * 16 + j] = acc[j];
     }
   }
   tc_fence_before();
@@ -326,26 +347,50 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc_n(tmem, tcols);
 }
 
+// Largest K split (cluster size) whose whole grid is co-resident in one wave: clusters of
+// 4 or more strand SMs at GPC boundaries (e.g. 144 CTAs in clusters of 4 would need two
+// waves on 148 SMs), so capacity is queried, not assumed.
+template <typename Kern>
+int choose_ksplit(Kern kern, const K1Layout &Ly, int64_t tiles, int64_t nkb) {
+  int best = 1;
+  int64_t best_ctas = tiles;
+  for (int ks = 1; ks <= 8; ++ks) {
+    if (ks > nkb) break;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(ks), static_cast<unsigned>(tiles), 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = Ly.smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(ks);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    const int64_t ctas = tiles * ks;
+    if (ctas <= static_cast<int64_t>(nclusters) * ks && ctas > best_ctas) {
+      best = ks;
+      best_ctas = ctas;
+    }
+  }
+  return best;
+}
+
 template <int kFmt, bool kScaleBf16>
-cudaError_t launch_t(const K1Maps &maps, const K1Params &p, int ks, cudaStream_t s) {
+cudaError_t launch_t(const K1Maps &maps, const K1Params &p, int /*ks_hint*/, cudaStream_t s) {
   auto kern = k1_tc_kernel<kFmt, kScaleBf16>;
   const K1Layout Ly = k1_layout(p.rank);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(Ly.smem));
   if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(ks), static_cast<unsigned>(p.Mpad / 128), 1);
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = Ly.smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = static_cast<unsigned>(ks);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, maps.x, maps.l1s, p, ks);
+  const int ks = choose_ksplit(kern, Ly, p.Mpad / 128, p.K / 64);
+  return launch_ex(kern, dim3(static_cast<unsigned>(ks), static_cast<unsigned>(p.Mpad / 128), 1),
+                   dim3(kThreads, 1, 1), Ly.smem, s, static_cast<unsigned>(ks), maps.x, maps.l1s, p, ks);
 }
 
 }  // namespace

@@ -150,6 +150,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_launch_dependents();
+  griddep_wait();                                   // inputs may come from the previous kernel
 
   if (warp == 0) {
     // ---------------------------------------------------------------- producer
@@ -383,8 +385,7 @@ cudaError_t launch_k2_int4(const K2Maps &maps, const K2Params &p, cudaStream_t s
   }
   const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
   const unsigned grid = static_cast<unsigned>(tiles < num_sms ? tiles : num_sms);
-  k2_int4_kernel<<<grid, kThreads, SMEM, s>>>(maps.a, maps.b, maps.xl1, maps.l2, p);
-  return cudaGetLastError();
+  return launch_ex(k2_int4_kernel, dim3(grid), dim3(kThreads), SMEM, s, 1u, maps.a, maps.b, maps.xl1, maps.l2, p);
 }
 
 }  // namespace svdq

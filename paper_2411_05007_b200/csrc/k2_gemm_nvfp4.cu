@@ -161,10 +161,12 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_launch_dependents();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
+      griddep_wait();                                  // xq / xs / xl1 come from K1
 #ifdef SVDQ_TRACE
       long long t_prod_wait = 0;
       const long long t_start = clock64();
@@ -311,6 +313,7 @@ __global__ void __launch_bounds__(192, 1)
     const int et = threadIdx.x - 64;           // 0..127
     int acc_i = 0;
     int ebuf = 0;
+    griddep_wait();                            // Y / bias may be touched by the previous kernel
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++acc_i) {
       const int b = acc_i & 1;
       const uint32_t acc_ph = (acc_i >> 1) & 1;
@@ -353,8 +356,7 @@ static cudaError_t launch_bn(const K2Maps &maps, const K2Params &p, cudaStream_t
   }
   const int64_t tiles = ((p.M + 127) / 128) * ((p.N + BN - 1) / BN);
   const unsigned grid = static_cast<unsigned>(tiles < num_sms ? tiles : num_sms);
-  kern<<<grid, 192, C::SMEM, s>>>(maps.a, maps.b, maps.xl1, maps.l2, maps.y, p);
-  return cudaGetLastError();
+  return launch_ex(kern, dim3(grid), dim3(192), C::SMEM, s, 1u, maps.a, maps.b, maps.xl1, maps.l2, maps.y, p);
 }
 
 int k2_nvfp4_bn(int64_t M, int64_t N) {

@@ -140,10 +140,12 @@ __global__ void __launch_bounds__(192, 1)
   cluster_sync();                                        // barriers of both CTAs initialised
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_launch_dependents();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (elect_one()) {
+      griddep_wait();                                    // xq / xs / xl1 come from K1
       const uint32_t full0 = mapa_u32(&full[0], 0);      // leader's barriers
       int s = 0;
       uint32_t ph = 0;
@@ -284,6 +286,7 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t acc_empty0 = mapa_u32(&acc_empty[0], 0);
     int acc_i = 0;
     int ebuf = 0;
+    griddep_wait();
     for (int t = pair; t < tiles; t += npairs, ++acc_i) {
       const int b = acc_i & 1;
       const uint32_t acc_ph = (acc_i >> 1) & 1;
@@ -326,19 +329,8 @@ cudaError_t launch_k2_nvfp4_2sm(const K2Maps &maps, const CUtensorMap &sfa, cons
   }
   const int64_t tiles = ((p.M + 255) / 256) * ((p.N + BN - 1) / BN);
   const int64_t pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs), 1, 1);
-  cfg.blockDim = dim3(192, 1, 1);
-  cfg.dynamicSmemBytes = SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k2_nvfp4_2sm_kernel, maps.a, maps.b, maps.xl1, maps.l2, sfa, sfb, maps.y, p);
+  return launch_ex(k2_nvfp4_2sm_kernel, dim3(static_cast<unsigned>(2 * pairs)), dim3(192), SMEM, s, 2u, maps.a,
+                   maps.b, maps.xl1, maps.l2, sfa, sfb, maps.y, p);
 }
 
 }  // namespace svdq

@@ -114,3 +114,12 @@ def test_int4_group_accumulators_bit_exact():
         raise
     ref = S.int4_group_accum(qa, qb)
     np.testing.assert_array_equal(acc.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+@pytest.mark.parametrize("M,K,N,r", [(300, 6208, 400, 48), (257, 6144, 192, 0), (1000, 8192, 3072, 128),
+                                     (129, 6400, 208, 16)])
+def test_k2_long_k_pair_kernel(fmt, M, K, N, r):
+    """K >= 6144 selects the CTA-pair (cta_group::2) NVFP4 kernel: ragged M / N (N not a
+    multiple of the 192 tile, second SF atom absent), K tails (K % 256 = 64), ranks 0..128."""
+    run_k2(fmt, M, K, N, r, seed=M + K, sample=64 if M > 512 else None)

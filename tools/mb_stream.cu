@@ -11,6 +11,7 @@
 #include <cudaTypedefs.h>
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include "../paper_2411_05007_b200/csrc/sm100.cuh"
 
 using namespace svdq;
@@ -40,6 +41,11 @@ __global__ void __launch_bounds__(576, 1) stream_kernel(const __grid_constant__ 
         uint4 a = *reinterpret_cast<const uint4 *>(p);
         uint4 b = *reinterpret_cast<const uint4 *>(p + 32);
         acc += a.x ^ b.y;
+        if (kb + 1 < kb_begin + nkb_here) {   // unroll x4 with all loads first
+          uint4 c0 = *reinterpret_cast<const uint4 *>(p + 64), c1 = *reinterpret_cast<const uint4 *>(p + 96);
+          ++kb;
+          acc += c0.z ^ c1.w;
+        }
       }
     }
     if (acc == 12345) sink[0] = acc;
@@ -142,8 +148,8 @@ __global__ void __launch_bounds__(64, 1) gen_kernel(const __grid_constant__ CUte
   }
 }
 
-int main() {
-  const int64_t M = 4096, K = 3072;
+int main(int argc, char **argv) {
+  const int64_t M = argc > 1 ? atoll(argv[1]) : 4096, K = argc > 2 ? atoll(argv[2]) : 3072;
   uint16_t *X;
   cudaMalloc(&X, M * K * 2);
   cudaMemset(X, 1, M * K * 2);
@@ -177,7 +183,7 @@ int main() {
   }
   cudaFree(sink);
   cudaMalloc(&sink, M * K + 4096);
-  const int NB = 16;                                 // 16 distinct inputs: 400 MB > L2 (cold)
+  const int NB = M * K * 2 > (200ll << 20) ? 3 : 16;        // distinct inputs, total > L2 (cold)
   uint16_t *Xs;
   cudaMalloc(&Xs, (size_t)NB * M * K * 2);
   cudaMemset(Xs, 1, (size_t)NB * M * K * 2);
@@ -190,41 +196,39 @@ int main() {
     enc(&tms[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Xs + (size_t)i * M * K, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
-  // shape variants, all cold (16 distinct inputs)
-  struct V { const char *name; int inner; int rows; int chunks; CUtensorMapSwizzle swz; int stage; };
-  V vs[] = {{"box 64x128 SW128", 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B, 16384},
-            {"box 128x128 none", 128, 128, 1, CU_TENSOR_MAP_SWIZZLE_NONE, 32768},
-            {"box 256x128 none", 256, 128, 1, CU_TENSOR_MAP_SWIZZLE_NONE, 65536},
-            {"box 256x64 none", 256, 64, 1, CU_TENSOR_MAP_SWIZZLE_NONE, 32768}};
-  for (auto &v : vs) {
+  // CTAs per SM / grid variants, all cold (16 distinct inputs), box 64x128 SW128
+  {
     CUtensorMap maps[NB];
     for (int i = 0; i < NB; ++i) {
       memset(&maps[i], 0, sizeof(CUtensorMap));
       cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
       cuuint64_t str[1] = {(cuuint64_t)(K * 2)};
-      cuuint32_t box[2] = {(cuuint32_t)v.inner, (cuuint32_t)v.rows}, es[2] = {1, 1};
-      CUresult r = enc(&maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Xs + (size_t)i * M * K, dims, str, box, es,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, v.swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r) printf("encode failed %d\n", r);
+      cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
+      enc(&maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Xs + (size_t)i * M * K, dims, str, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
-    const int S = 4;
-    const int rowtiles = M / v.rows;
-    const int ks = 4 * 128 / v.rows >= 1 ? (v.rows == 64 ? 2 : 4) : 4;
-    size_t smem = (size_t)S * v.stage + 2048;
-    auto k = gen_kernel;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid(ks, rowtiles);
-    cudaEvent_t a, b;
-    cudaEventCreate(&a); cudaEventCreate(&b);
-    for (int w = 0; w < 3; ++w) k<<<grid, 64, smem>>>(maps[w], K, ks, S, v.inner, v.rows, v.stage, sink);
-    cudaEventRecord(a);
-    for (int w = 0; w < 2 * NB; ++w) k<<<grid, 64, smem>>>(maps[w % NB], K, ks, S, v.inner, v.rows, v.stage, sink);
-    cudaEventRecord(b);
-    cudaEventSynchronize(b);
-    float ms;
-    cudaEventElapsedTime(&ms, a, b);
-    printf("%-20s grid %dx%d: cold %.2f us  %.2f TB/s  %s\n", v.name, ks, rowtiles, 1e3 * ms / (2 * NB),
-           M * K * 2 / (ms / (2 * NB) * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+    struct G { int ks; int S; };
+    G gs[] = {{3, 6}, {4, 6}, {4, 3}, {8, 3}};
+    for (auto &gv : gs) {
+      size_t smem = (size_t)gv.S * 16384 + 2048;
+      auto k = gen_kernel;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 64, smem);
+      dim3 grid(gv.ks, M / 128);
+      cudaEvent_t a, b;
+      cudaEventCreate(&a); cudaEventCreate(&b);
+      for (int w = 0; w < 3; ++w) k<<<grid, 64, smem>>>(maps[w], K, gv.ks, gv.S, 64, 128, 16384, sink);
+      cudaEventRecord(a);
+      for (int w = 0; w < 2 * NB; ++w) k<<<grid, 64, smem>>>(maps[w % NB], K, gv.ks, gv.S, 64, 128, 16384, sink);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      printf("ks %2d stages %d ctas %4d (occ/SM %d): cold %.2f us  %.2f TB/s  %s\n", gv.ks, gv.S, gv.ks * (int)(M / 128), occ,
+             1e3 * ms / (2 * NB), M * K * 2 / (ms / (2 * NB) * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+    }
   }
   // LDG cold
   {

@@ -1,0 +1,28 @@
+"""Time K1 alone on one shape (graph of 10 launches over 3 distinct DRAM-cold inputs).
+    SVDQ_LIB=... python tools/time_k1.py M K [r]"""
+import os, sys
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2411_05007_b200 as P
+M, K = int(sys.argv[1]), int(sys.argv[2])
+r = int(sys.argv[3]) if len(sys.argv) > 3 else 32
+dev = torch.device("cuda")
+layer = P.QuantizedLinear.empty("nvfp4", K, 64, r, device=dev)
+layer.lambda_inv.fill_(1.0); layer.l1s.zero_(); layer._sync_view()
+nb = max(3, int(400e6 // (M * K * 2)) + 1)
+xs = [torch.randn(M, K, device=dev).to(torch.bfloat16) for _ in range(nb)]
+outs = [P.svdq_quantize_act_lowrank_down(layer, x) for x in xs[:1]]
+xq, xsc, xl1 = outs[0]
+s = torch.cuda.Stream()
+torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=s):
+    for i in range(10):
+        P.svdq_quantize_act_lowrank_down(layer, xs[i % nb], xq, xsc, xl1, stream=s)
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+with torch.cuda.stream(s):
+    g.replay()
+    a.record(s); g.replay(); b.record(s)
+torch.cuda.synchronize()
+us = a.elapsed_time(b) / 10 * 1e3
+print(f"K1 M={M} K={K} r={r} lib={os.path.basename(os.environ.get('SVDQ_LIB', 'libsvdq.so'))}: {us:.2f} us  {M*K*2.5625/us/1e3:.2f} TB/s")
