@@ -136,8 +136,9 @@ svdq_status make_sf_map(CUtensorMap *map, const void *base, int64_t rows, int64_
   return SVDQ_OK;
 }
 
-// CTA-pair kernel for long reductions (measured on B200: K = 12288 / 15360 layers run
-// 13-15 % faster as pairs; K = 3072 layers 5 % faster on the 1-CTA kernel).
+// CTA-pair kernel unless the problem is small (measured on B200 with the 8-warp TMA-store
+// epilogue: pairs are 12-13 % faster at K = 12288 / 15360 and equal or 1 % faster at
+// K = 3072, M >= 4096; the 1-CTA kernel is 3 % faster at M = 512, K = 3072).
 // SVDQ_K2_PAIR=0 / 1 forces one kernel (testing / comparison).
 bool use_pair_kernel(int64_t M, int64_t K) {
   static int mode = -1;
@@ -146,7 +147,7 @@ bool use_pair_kernel(int64_t M, int64_t K) {
     mode = e ? atoi(e) : 2;
   }
   if (M <= 128 || mode == 0) return false;
-  return mode == 1 || K >= 6144;
+  return mode == 1 || K >= 6144 || M >= 1024;
 }
 
 }  // namespace
@@ -290,7 +291,8 @@ svdq_status svdq_gemm_w4a4_lowrank_up(const svdq_linear *L, const uint8_t *xq, c
                                     : y_dtype == SVDQ_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                                            : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const int64_t ysz = y_dtype == SVDQ_FP32 ? 4 : 2;
-    if ((st = make_map(&maps.y, Y, ydt, N, M, ldy * ysz, static_cast<uint32_t>(128 / ysz), 32)) != SVDQ_OK)
+    if ((st = make_map(&maps.y, Y, ydt, N, M, ldy * ysz, static_cast<uint32_t>(64 / ysz), 32,
+                       CU_TENSOR_MAP_SWIZZLE_64B)) != SVDQ_OK)
       return st;
     if ((st = make_map(&maps.a, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, M, K / 2, 128, 128)) != SVDQ_OK) return st;
     if ((st = make_map(&maps.b, L->w_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, N, K / 2, 128, b_rows)) != SVDQ_OK) return st;

@@ -70,7 +70,7 @@ struct K2Params {
   int32_t *dbg_acc;       // INT4 debug: per-group int32 accumulators [K/64][M][N]
 };
 struct K2Maps {
-  CUtensorMap a, b, xl1, l2, y;   // y: output store map, box {128 B of columns, 32 rows}, SW128
+  CUtensorMap a, b, xl1, l2, y;   // y: output store map, box {64 B of columns, 32 rows}, SW64
 };
 cudaError_t launch_k2_nvfp4(const K2Maps &maps, const K2Params &p, cudaStream_t s);
 int k2_nvfp4_bn(int64_t M, int64_t N);   // N tile the 1-CTA NVFP4 GEMM will use

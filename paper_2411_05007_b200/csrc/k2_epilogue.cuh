@@ -1,10 +1,7 @@
 // Shared epilogue of the NVFP4 GEMMs (K2): TMEM -> registers -> alpha, bias ->
-// 16-bit (or fp32) -> 128-B-swizzled smem staging -> TMA bulk tensor store.
+// 16-bit (or fp32) -> 64-B-swizzled smem staging -> TMA bulk tensor store.
 //   Y[m,n] = out_rn(fl32(alpha * acc[m,n]) + bias[n])        (App. B.5, reading Q16)
-// One warp owns one TMEM lane quadrant (32 rows).  Each 32-row x 128-byte chunk is
-// staged in a 4 KB buffer (two per warp, so the TMA store of one overlaps the next
-// chunk) whose 16-byte columns are XOR-swizzled by row, matching the store map's
-// SWIZZLE_128B layout; TMA clips rows >= M and columns >= N.
+// Warps own TMEM lane quadrants (32 rows); TMA clips rows >= M and columns >= N.
 #pragma once
 #include <cstdint>
 #include <cuda_bf16.h>
@@ -22,45 +19,43 @@ __device__ __forceinline__ uint32_t pack2(float a, float b, int dt) {
          (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(b))) << 16);
 }
 
-// Drains `ncols` accumulator columns of this warp's 32 TMEM lanes.  `release` is invoked
-// once every tcgen05.ld of the tile has completed (the accumulator buffer may be reused).
-template <int NCOLS, typename Release>
+// Drains this warp's share of the tile: `nwarps_per_quad` warps share a TMEM lane quadrant
+// (32 rows) and take interleaved 64-byte column chunks (32 bf16/fp16 or 16 fp32 columns).
+// Each chunk is staged in a 2 KB buffer (two per warp) with the 64-byte swizzle of the store
+// map (16-byte column j of row r at j ^ ((r >> 1) & 3)), then written by a TMA bulk tensor
+// store.  `release` runs once every tcgen05.ld of the tile has completed.
+template <int NCOLS, int NWQ, typename Release>
 __device__ __forceinline__ void epilogue_tile(uint32_t tmem_acc_lane, const float *bias_s, float alpha, int y_dtype,
-                                              const CUtensorMap *tmY, int32_t row0, int32_t col0, uint8_t *stage,
-                                              int &buf, int lane, Release release) {
-  const int cpc = y_dtype == 2 ? 32 : 64;                 // columns per 128-byte chunk
+                                              const CUtensorMap *tmY, int32_t row0, int32_t col0, int sub,
+                                              uint8_t *stage, int &buf, int lane, Release release) {
+  const int cpc = y_dtype == 2 ? 16 : 32;                 // columns per 64-byte chunk
   const int nchunks = NCOLS / cpc;
-  for (int ch = 0; ch < nchunks; ++ch) {
-    float v[64];
+  const int last = sub + ((nchunks - 1 - sub) / NWQ) * NWQ;
+  for (int ch = sub; ch < nchunks; ch += NWQ) {
+    float v[32];
     if (y_dtype == 2) {
+      uint32_t r[16];
+      tmem_ld_32x32b_x16(tmem_acc_lane + ch * 16, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+    } else {
       uint32_t r[32];
       tmem_ld_32x32b_x32(tmem_acc_lane + ch * 32, r);
       tmem_ld_wait();
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-    } else {
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(tmem_acc_lane + ch * 64, r);
-      uint32_t r2[32];
-      tmem_ld_32x32b_x32(tmem_acc_lane + ch * 64 + 32, r2);
-      tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        v[j] = __uint_as_float(r[j]);
-        v[32 + j] = __uint_as_float(r2[j]);
-      }
     }
-    if (ch == nchunks - 1) release();
-    // staging buffer of this chunk: wait until the TMA store that last used it has read it
-    uint8_t *sb = stage + buf * 4096;
-    if (lane == 0) bulk_wait_group_read<1>();
+    if (ch == last) release();
+    uint8_t *sb = stage + buf * 2048;
+    if (lane == 0) bulk_wait_group_read<1>();            // the store that last used sb has read it
     __syncwarp();
     const float *bs = bias_s + ch * cpc;
-    uint8_t *rowp = sb + lane * 128;
-    const uint32_t sw = static_cast<uint32_t>(lane & 7);
+    uint8_t *rowp = sb + lane * 64;
+    const uint32_t sw = static_cast<uint32_t>((lane >> 1) & 3);
     if (y_dtype == 2) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < 4; ++c) {
         float4 o;
         o.x = __fadd_rn(__fmul_rn(alpha, v[4 * c + 0]), bs[4 * c + 0]);
         o.y = __fadd_rn(__fmul_rn(alpha, v[4 * c + 1]), bs[4 * c + 1]);
@@ -70,7 +65,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tmem_acc_lane, const floa
       }
     } else {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < 4; ++c) {
         float o[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) o[e] = __fadd_rn(__fmul_rn(alpha, v[8 * c + e]), bs[8 * c + e]);

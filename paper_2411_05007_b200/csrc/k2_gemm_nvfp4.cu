@@ -56,7 +56,7 @@ struct NvCfg {
   static constexpr int SFA_BYTES = 4 * 512;              // 128 rows x 16 sf
   static constexpr int SFB_BYTES = 2 * 4 * 512;          // two 128-row atoms x 16 sf
   static constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
-  static constexpr int EPI_BYTES = 4 * 2 * 4096;          // per epilogue warp: two 4 KB staging buffers
+  static constexpr int EPI_BYTES = 8 * 2 * 2048;          // 8 epilogue warps x two 2 KB staging buffers
   static constexpr int kStages = (225 * 1024 - EPI_BYTES - 2048) / STAGE;
   static constexpr int SF_COLS = 16 + 32;                // TMEM columns per SF slot
   static constexpr int SF_BASE = 2 * BN;
@@ -111,7 +111,7 @@ __device__ __forceinline__ void store8(void *Y, int dt, int64_t ldy, int64_t row
 }
 
 template <int BN>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     k2_nvfp4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmL,
                     const __grid_constant__ CUtensorMap tmY, const K2Params p) {
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 4);
+      mbar_init(&acc_empty[b], 8);                   // 8 epilogue warps
     }
     fence_mbar_init();
   }
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(192, 1)
     // ------------------------------------------------------------ epilogue
     const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
     const int row = quad * 32 + lane;
-    const int et = threadIdx.x - 64;           // 0..127
+    const int et = threadIdx.x - 64;           // 0..255
     int acc_i = 0;
     int ebuf = 0;
     griddep_wait();                            // Y / bias may be touched by the previous kernel
@@ -321,15 +321,15 @@ __global__ void __launch_bounds__(192, 1)
       const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
       const int64_t grow = m0 + row;
       // stage this tile's bias (fp32) in smem
-      named_bar(1, 128);                        // previous tile's readers are done
-      for (int c = et; c < BN; c += 128)
+      named_bar(1, 256);                        // previous tile's readers are done
+      for (int c = et; c < BN; c += 256)
         bias_s[c] = (p.bias && n0 + c < p.N) ? load_bias(p.bias, p.bias_dtype, n0 + c) : 0.f;
-      named_bar(1, 128);
+      named_bar(1, 256);
       mbar_wait(&acc_full[b], acc_ph);
       tc_fence_after();
-      epilogue_tile<BN>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype, &tmY,
-                        static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0),
-                        epi_stage + (warp - 2) * 8192, ebuf, lane, [&]() {
+      epilogue_tile<BN, 2>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
+                           &tmY, static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
+                           epi_stage + (warp - 2) * 4096, ebuf, lane, [&]() {
                           tc_fence_before();
                           __syncwarp();
                           if (lane == 0) mbar_arrive(&acc_empty[b]);
@@ -356,7 +356,7 @@ static cudaError_t launch_bn(const K2Maps &maps, const K2Params &p, cudaStream_t
   }
   const int64_t tiles = ((p.M + 127) / 128) * ((p.N + BN - 1) / BN);
   const unsigned grid = static_cast<unsigned>(tiles < num_sms ? tiles : num_sms);
-  return launch_ex(kern, dim3(grid), dim3(192), C::SMEM, s, 1u, maps.a, maps.b, maps.xl1, maps.l2, maps.y, p);
+  return launch_ex(kern, dim3(grid), dim3(320), C::SMEM, s, 1u, maps.a, maps.b, maps.xl1, maps.l2, maps.y, p);
 }
 
 int k2_nvfp4_bn(int64_t M, int64_t N) {

@@ -54,7 +54,7 @@ constexpr int kStages = 5;
 constexpr int SF_COLS = 48;
 constexpr int SF_BASE = 2 * BN;
 constexpr int EPI_OFF = kStages * STAGE;                 // 4 epilogue warps x two 4 KB staging buffers
-constexpr int BAR_OFF = EPI_OFF + 4 * 8192;
+constexpr int BAR_OFF = EPI_OFF + 8 * 4096;
 constexpr int SMEM = BAR_OFF + 256 + BN * 4 + 1024;
 static_assert(STAGE % 1024 == 0, "stage alignment");
 static_assert(SF_BASE + 2 * SF_COLS <= 512, "TMEM budget");
@@ -87,7 +87,7 @@ __device__ __forceinline__ void store8(void *Y, int dt, int64_t ldy, int64_t row
   *reinterpret_cast<uint4 *>(static_cast<uint16_t *>(Y) + row * ldy + col) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     k2_nvfp4_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmL,
                         const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 8);                       // 4 epilogue warps x 2 CTAs
+      mbar_init(&acc_empty[b], 16);                      // 8 epilogue warps x 2 CTAs
     }
     fence_mbar_init();
   }
@@ -293,15 +293,15 @@ __global__ void __launch_bounds__(192, 1)
       const int64_t m0 = static_cast<int64_t>(t % mt_count) * 256 + 128 * crank;
       const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
       const int64_t grow = m0 + row;
-      named_bar(1, 128);
-      for (int c = et; c < BN; c += 128)
+      named_bar(1, 256);
+      for (int c = et; c < BN; c += 256)
         bias_s[c] = (p.bias && n0 + c < p.N) ? load_bias(p.bias, p.bias_dtype, n0 + c) : 0.f;
-      named_bar(1, 128);
+      named_bar(1, 256);
       mbar_wait(&acc_full[b], acc_ph);
       tc_fence_after();
-      epilogue_tile<BN>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype, &tmY,
-                        static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0),
-                        smem + EPI_OFF + (warp - 2) * 8192, ebuf, lane, [&]() {
+      epilogue_tile<BN, 2>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
+                           &tmY, static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
+                           smem + EPI_OFF + (warp - 2) * 4096, ebuf, lane, [&]() {
                           tc_fence_before();
                           __syncwarp();
                           if (lane == 0) mbar_arrive_cluster(acc_empty0 + b * 8);
@@ -329,7 +329,7 @@ cudaError_t launch_k2_nvfp4_2sm(const K2Maps &maps, const CUtensorMap &sfa, cons
   }
   const int64_t tiles = ((p.M + 255) / 256) * ((p.N + BN - 1) / BN);
   const int64_t pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  return launch_ex(k2_nvfp4_2sm_kernel, dim3(static_cast<unsigned>(2 * pairs)), dim3(192), SMEM, s, 2u, maps.a,
+  return launch_ex(k2_nvfp4_2sm_kernel, dim3(static_cast<unsigned>(2 * pairs)), dim3(320), SMEM, s, 2u, maps.a,
                    maps.b, maps.xl1, maps.l2, sfa, sfb, maps.y, p);
 }
 
