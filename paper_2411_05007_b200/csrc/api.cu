@@ -240,6 +240,9 @@ svdq_status svdq_quantize_act_lowrank_down(const svdq_linear *L, const void *X, 
         (st = make_map(&maps.l1s, L->l1s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->K, L->rank, L->K * 2, 64,
                        static_cast<uint32_t>(L->rank))) != SVDQ_OK)
       return st;
+    if ((st = make_map(&maps.lam, L->lambda_inv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 32, L->K / 32, 128, 32, 2)) !=
+        SVDQ_OK)
+      return st;
     e = launch_k1_tc(maps, p, static_cast<cudaStream_t>(stream));
   } else {
     e = launch_k1(p, static_cast<cudaStream_t>(stream));

@@ -48,7 +48,7 @@ struct K1Params {
 };
 cudaError_t launch_k1(const K1Params &p, cudaStream_t s);       // mma.sync path (fp16 X)
 struct K1Maps {
-  CUtensorMap x, l1s;
+  CUtensorMap x, l1s, lam;    // lam: lambda_inv viewed as [K/32][32] fp32, box {32, 2}, 128-B swizzle
 };
 cudaError_t launch_k1_tc(const K1Maps &maps, const K1Params &p, cudaStream_t s);   // bf16 X
 int k1_tc_ksplit(int64_t Mpad, int64_t K);

@@ -19,8 +19,12 @@
 #include <cuda_bf16.h>
 
 #include "formats.cuh"
+#include <cstdlib>
 #include "k1_launch.h"
 #include "sm100.cuh"
+#ifndef SVDQ_K1EXP
+#define SVDQ_K1EXP 0   // ablation bits: 1 no stores, 2 no MMA, 4 no L1s load, 8 no quantizer math
+#endif
 
 #ifdef SVDQ_TRACE
 namespace svdq { __device__ unsigned long long g_k1_trace[256]; __device__ unsigned long long g_k1_cta[1024][3]; }
@@ -56,6 +60,31 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   return v;
 }
 
+// packed fp32 pairs (low word = even element): sm_100a FMUL2
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t pack64(uint32_t lo, uint32_t hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "r"(lo), "r"(hi));
+  return d;
+}
+// two bf16 in one word -> fp32 pair (exact)
+__device__ __forceinline__ uint64_t bf16x2_to_f32x2(uint32_t w) { return pack64(w << 16, w & 0xFFFF0000u); }
+__device__ __forceinline__ float lo32(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); }
+__device__ __forceinline__ float hi32(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
+__device__ __forceinline__ void lds_v2x64(uint32_t addr, uint64_t &a, uint64_t &b) {
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(addr));
+}
+__device__ __forceinline__ uint32_t e2m1x2_pair(uint64_t v) {   // low element -> low nibble
+  uint32_t r;
+  asm("{\n\t.reg .b8 b;\n\tcvt.rn.satfinite.e2m1x2.f32 b, %2, %1;\n\tcvt.u32.u8 %0, b;\n\t}"
+      : "=r"(r) : "f"(lo32(v)), "f"(hi32(v)));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(lo))) |
          (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(hi))) << 16);
@@ -82,6 +111,7 @@ __host__ __device__ inline K1Layout k1_layout(int rank) {
 template <int kFmt, bool kScaleBf16>
 __global__ void __launch_bounds__(kThreads, 1)
     k1_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmL,
+                 const __grid_constant__ CUtensorMap tmLam,
                  const K1Params p, int ks) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -128,6 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmX);
     if (r) tma_prefetch(&tmL);
+    tma_prefetch(&tmLam);
   }
   if (warp == 1 && r) tmem_alloc_n(tmem_slot, tcols);
   if (kFmt == 0 && threadIdx.x >= 64 && threadIdx.x < 64 + 256) {
@@ -146,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------------------------------------------------------- producer
     if (elect_one()) {
       griddep_wait();                                  // X may be the previous kernel's output
-      const uint32_t bytes = 16384 + r * 128 + 256;
+      const uint32_t bytes = 16384 + ((SVDQ_K1EXP & 4) ? 0 : r * 128) + 256;
       // warm L2 with the first ring's worth of X tiles beyond what the smem ring holds
       for (int i = S; i < nsteps && i < 2 * S; ++i)
         tma_prefetch_2d(&tmX, (kb_begin + i) * 64, static_cast<int32_t>(row0));
@@ -160,8 +191,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t *st = smem + s * Ly.stage_bytes;
         mbar_arrive_expect_tx(&full[s], bytes);
         tma_load_2d(st, &tmX, &full[s], kb * 64, static_cast<int32_t>(row0));
-        if (r) tma_load_2d(st + 16384, &tmL, &full[s], kb * 64, 0);
-        bulk_load(st + 16384 + r * 128, p.lam_inv + kb * 64, 256, &full[s]);
+        if (r && !(SVDQ_K1EXP & 4)) tma_load_2d(st + 16384, &tmL, &full[s], kb * 64, 0);
+        // lambda_inv block as [2][32] fp32 with 128-B swizzle: the four 64-B lane groups land in
+        // distinct banks, so the quantizers' broadcast loads are conflict-free
+        tma_load_2d(st + 16384 + r * 128, &tmLam, &full[s], 0, kb * 2);
       }
     }
   } else if (warp == 1) {
@@ -177,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t xa = smem_u32(smem + s * Ly.stage_bytes);
           const uint32_t la = xa + 16384;
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
+          for (int j = 0; j < ((SVDQ_K1EXP & 2) ? 0 : 4); ++j)
             mma_bf16(tmem + j * r, sdesc_kmajor_sw128(xa + 32 * j), sdesc_kmajor_sw128(la + 32 * j), idesc,
                      i != 0);
           tc_commit(&empty[s]);
@@ -196,95 +229,97 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t row = row0 + rl;
     const bool rvalid = row < p.M;
     const float t6 = __fmul_rn(__frcp_rn(p.gs_x), __frcp_rn(6.0f));
-    uint8_t *xq_row = p.xq + row * (K / 2);
-    uint8_t *sf_row = p.xs + sf_offset(row, 0, K);        // + kb * 512 per 64-wide block
-    uint16_t *s16_row = reinterpret_cast<uint16_t *>(p.xs) + row * (K / 64);
+    // per-lane output pointers advance by one 64-wide K block per step
+    uint2 *xq_ptr = reinterpret_cast<uint2 *>(p.xq + row * (K / 2) + static_cast<int64_t>(kb_begin) * 32) + q;
+    uint32_t *sf_ptr = reinterpret_cast<uint32_t *>(p.xs + sf_offset(row, 0, K) + static_cast<int64_t>(kb_begin) * 512);
+    uint16_t *s16_ptr = reinterpret_cast<uint16_t *>(p.xs) + row * (K / 64) + kb_begin;
     const uint32_t swz = static_cast<uint32_t>(rl & 7);
-    for (int i = 0; i < nsteps; ++i) {
-      const int s = i % S;
-      const uint32_t ph = (i / S) & 1;
-      const int kb = kb_begin + i;
+    const uint32_t lut = smem_u32(qinv_lut);
+    const uint32_t stage0 = smem_u32(smem);
+    const bool store_codes = rvalid;
+    const bool store_sf = rvalid && q == 0;
+    // byte offset of lambda chunk t (elements 16q + 4t .. +4) in the swizzled [2][128 B] block
+    uint32_t lam_off[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      lam_off[t] = (q >> 1) * 128 + ((((q & 1) * 4 + t) ^ (q >> 1)) * 16);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < nsteps; ++i, xq_ptr += 4, sf_ptr += 128, ++s16_ptr) {
       mbar_wait(&full[s], ph);                            // suspend (do not hammer the barrier)
       if (qw == 0 && lane == 0) TRACE(66 + i);            // first quantizer sees stage i
-      const uint32_t xa = smem_u32(smem + s * Ly.stage_bytes) + rl * 128;
-      const float *lam = reinterpret_cast<const float *>(smem + s * Ly.stage_bytes + 16384 + r * 128);
-      float xh[2][8];
+      const uint32_t sbase = stage0 + s * Ly.stage_bytes;
+      const uint32_t xa = sbase + rl * 128;
+      const uint32_t la = sbase + 16384 + r * 128;
+      // lane q owns elements [16q, 16q + 16) of the 64-wide block: one whole NVFP4 group
+      uint64_t xh[8];                                     // x_hat as fp32 pairs (fl32(x * lambda_inv))
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const float4 la = *reinterpret_cast<const float4 *>(lam + c * 32 + q * 8);
-        const float4 lb = *reinterpret_cast<const float4 *>(lam + c * 32 + q * 8 + 4);
-        const float lm[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
-        const uint4 v = lds128(xa + ((static_cast<uint32_t>(c * 4 + q) ^ swz) * 16));
-        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          xh[c][2 * j] = __fmul_rn(__uint_as_float(w4[j] << 16), lm[2 * j]);
-          xh[c][2 * j + 1] = __fmul_rn(__uint_as_float(w4[j] & 0xFFFF0000u), lm[2 * j + 1]);
-        }
+        uint64_t l0, l1, l2, l3;
+        lds_v2x64(la + lam_off[2 * c], l0, l1);
+        lds_v2x64(la + lam_off[2 * c + 1], l2, l3);
+        const uint4 v = lds128(xa + ((static_cast<uint32_t>(2 * q + c) ^ swz) * 16));
+        xh[4 * c + 0] = fmul2(bf16x2_to_f32x2(v.x), l0);
+        xh[4 * c + 1] = fmul2(bf16x2_to_f32x2(v.y), l1);
+        xh[4 * c + 2] = fmul2(bf16x2_to_f32x2(v.z), l2);
+        xh[4 * c + 3] = fmul2(bf16x2_to_f32x2(v.w), l3);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);       // tile consumed: values are in registers
+      if (++s == S) { s = 0; ph ^= 1; }
+      if (SVDQ_K1EXP & 8) {
+        if (xh[0] == 12345ull) p.xq[0] = 1;     // keep the loads alive
+        continue;
+      }
       if (qw == 15 && lane == 0) TRACE(130 + i);          // last quantizer released stage i
       if constexpr (kFmt == 0) {
-        uint32_t sfb[2], codes[2];
+        float amax = 0.f;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          float amax = 0.f;
+        for (int j = 0; j < 8; ++j) amax = fmaxf(amax, fmaxf(fabsf(lo32(xh[j])), fabsf(hi32(xh[j]))));
+        const uint32_t sf = e4m3_rn_sat(__fmul_rn(amax, t6));
+        float qinv;
+        asm("ld.shared.f32 %0, [%1];" : "=f"(qinv) : "r"(lut + sf * 4));
+        const uint64_t q2 = pack64(__float_as_uint(qinv), __float_as_uint(qinv));
+        uint32_t w[2];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) amax = fmaxf(amax, fabsf(xh[c][j]));
-          amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
-          const uint32_t sf = e4m3_rn_sat(__fmul_rn(amax, t6));
-          const float qinv = qinv_lut[sf];
-          float v[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = __fmul_rn(xh[c][j], qinv);
-          codes[c] = e2m1x8(v);
-          sfb[c] = sf;
-        }
-        const uint32_t o0 = __shfl_down_sync(0xffffffffu, sfb[0], 2);
-        const uint32_t o1 = __shfl_down_sync(0xffffffffu, sfb[1], 2);
-        // regroup so lane q writes bytes [8q, 8q+8) of the row's 32-byte block: full-sector
-        // 8-byte stores (q0: c0 of q0,q1; q1: c0 of q2,q3; q2: c1 of q0,q1; q3: c1 of q2,q3)
-        const uint32_t src0 = (lane & ~3u) | ((q & 1) * 2);
-        const uint32_t a0 = __shfl_sync(0xffffffffu, codes[0], src0);
-        const uint32_t a1 = __shfl_sync(0xffffffffu, codes[0], src0 + 1);
-        const uint32_t b0 = __shfl_sync(0xffffffffu, codes[1], src0);
-        const uint32_t b1 = __shfl_sync(0xffffffffu, codes[1], src0 + 1);
-        if (rvalid)
-          *reinterpret_cast<uint2 *>(xq_row + kb * 32 + q * 8) = q < 2 ? make_uint2(a0, a1) : make_uint2(b0, b1);
-        if (q == 0)
-          *reinterpret_cast<uint32_t *>(sf_row + kb * 512) = sfb[0] | (o0 << 8) | (sfb[1] << 16) | (o1 << 24);
+        for (int c = 0; c < 2; ++c)
+          w[c] = e2m1x2_pair(fmul2(xh[4 * c], q2)) | (e2m1x2_pair(fmul2(xh[4 * c + 1], q2)) << 8) |
+                 (e2m1x2_pair(fmul2(xh[4 * c + 2], q2)) << 16) | (e2m1x2_pair(fmul2(xh[4 * c + 3], q2)) << 24);
+#if SVDQ_K1EXP & 16          // math kept alive, stores (almost) never
+        if (w[0] == 0x9E3779B9u && w[1] == sf) *xq_ptr = make_uint2(w[0], w[1]);
+#elif SVDQ_K1EXP & 32        // same stores, no math
+        if (store_codes) *xq_ptr = make_uint2(static_cast<uint32_t>(xh[0]), static_cast<uint32_t>(xh[7] >> 32));
+        reinterpret_cast<uint8_t *>(sf_ptr)[q] = static_cast<uint8_t>(xh[3]);
+#else
+        if (store_codes && !(SVDQ_K1EXP & (1 | 64))) *xq_ptr = make_uint2(w[0], w[1]);
+        if (!(SVDQ_K1EXP & (1 | 128))) reinterpret_cast<uint8_t *>(sf_ptr)[q] = static_cast<uint8_t>(sf);
+#endif
       } else {
         float amax = 0.f;
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-          for (int j = 0; j < 8; ++j) amax = fmaxf(amax, fabsf(xh[c][j]));
+        for (int j = 0; j < 8; ++j) amax = fmaxf(amax, fmaxf(fabsf(lo32(xh[j])), fabsf(hi32(xh[j]))));
         amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
         amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
         const uint16_t sc = scale16_rn_sat<kScaleBf16>(__fdiv_rn(amax, 7.0f));
         const float sd = scale16_to_f32<kScaleBf16>(sc);
         const float qinv = sd == 0.f ? 0.f : __frcp_rn(sd);
-        uint32_t words[2];
+        const uint64_t q2 = pack64(__float_as_uint(qinv), __float_as_uint(qinv));
+        uint32_t w[2];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           uint32_t word = 0;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            int v = __float2int_rn(__fmul_rn(xh[c][j], qinv));
-            v = max(-7, min(7, v));
-            word |= (static_cast<uint32_t>(v) & 0xFu) << (4 * j);
+          for (int j = 0; j < 4; ++j) {
+            const uint64_t t = fmul2(xh[4 * c + j], q2);
+            const int v0 = max(-7, min(7, __float2int_rn(lo32(t))));
+            const int v1 = max(-7, min(7, __float2int_rn(hi32(t))));
+            word |= ((static_cast<uint32_t>(v0) & 0xFu) | ((static_cast<uint32_t>(v1) & 0xFu) << 4)) << (8 * j);
           }
-          words[c] = word;
+          w[c] = word;
         }
-        const uint32_t src0 = (lane & ~3u) | ((q & 1) * 2);
-        const uint32_t a0 = __shfl_sync(0xffffffffu, words[0], src0);
-        const uint32_t a1 = __shfl_sync(0xffffffffu, words[0], src0 + 1);
-        const uint32_t b0 = __shfl_sync(0xffffffffu, words[1], src0);
-        const uint32_t b1 = __shfl_sync(0xffffffffu, words[1], src0 + 1);
-        if (rvalid) {
-          *reinterpret_cast<uint2 *>(xq_row + kb * 32 + q * 8) = q < 2 ? make_uint2(a0, a1) : make_uint2(b0, b1);
-          if (q == 0) s16_row[kb] = sc;
+        if (store_codes) {
+          *xq_ptr = make_uint2(w[0], w[1]);
+          if (store_sf) *s16_ptr = sc;
         }
       }
     }
@@ -388,9 +423,10 @@ cudaError_t launch_t(const K1Maps &maps, const K1Params &p, int /*ks_hint*/, cud
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(Ly.smem));
   if (e != cudaSuccess) return e;
-  const int ks = choose_ksplit(kern, Ly, p.Mpad / 128, p.K / 64);
+  int ks = choose_ksplit(kern, Ly, p.Mpad / 128, p.K / 64);
+  if (const char *e = getenv("SVDQ_K1_KS")) ks = atoi(e);     // ablation override (debug)
   return launch_ex(kern, dim3(static_cast<unsigned>(ks), static_cast<unsigned>(p.Mpad / 128), 1),
-                   dim3(kThreads, 1, 1), Ly.smem, s, static_cast<unsigned>(ks), maps.x, maps.l1s, p, ks);
+                   dim3(kThreads, 1, 1), Ly.smem, s, static_cast<unsigned>(ks), maps.x, maps.l1s, maps.lam, p, ks);
 }
 
 }  // namespace
