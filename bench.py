@@ -39,6 +39,16 @@ def flux_block_layers(batch=1):
     return synth.flux_double_block(batch) + synth.flux_single_block(batch)
 
 
+def bench_config(args, world):
+    """The workload description shared by both arms (svdq and --impl reference)."""
+    return {"workload": "flux1-dev block linears: 1 double block (img 4096 tok + txt 512 tok: "
+                        "qkv, proj, mlp_up, mlp_down) + 1 single block (4608 tok: linear1, linear2)",
+            "batch": args.batch, "hidden": 3072, "mlp": 12288, "rank": 32, "format": args.fmt,
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+            "l2": "flushed between steps outside the per-step events (512 MiB write, then a 256 MiB read "
+                  "so the flush's dirty lines are written back before the step starts)"}
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -81,7 +91,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.002)
 
     def __enter__(self):
         if self.nv:
@@ -143,54 +153,83 @@ def run_svdq(args, rank, world, local_rank):
     k1_bytes = sum(L.M * L.K * 2 + L.M * L.K * (0.5625 if args.fmt == "nvfp4" else 0.53125)
                    + L.M * L.r * 2 for L in layers)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    flush_sink = torch.empty((), dtype=torch.int64, device=dev)
     stream = torch.cuda.Stream(device=dev)
 
-    def step(st, k1_events=None, k2_events=None, only=None):
-        for j, (L, layer, b) in enumerate(built):
-            if only == "k1":
+    def l2_flush():
+        flush.zero_()
+        flush_sink.copy_(flush[: 256 << 20].view(torch.int64).sum())
+
+    def step(bl, st, k1_events=None, k2_events=None, only=None):
+        for j, (L, layer, b) in enumerate(bl):
+            if only != "k2":
+                if k1_events is not None:
+                    k1_events[j][0].record(st)
                 P.svdq_quantize_act_lowrank_down(layer, b["x"], b["xq"], b["xs"], b["xl1"], stream=st)
-                continue
-            if only == "k2":
+                if k1_events is not None:
+                    k1_events[j][1].record(st)
+            if only != "k1":
+                if k2_events is not None:
+                    k2_events[j][0].record(st)
                 P.svdq_gemm_w4a4_lowrank_up(layer, b["xq"], b["xs"], b["xl1"], L.M, Y=b["y"], stream=st)
-                continue
-            if k1_events is not None:
-                k1_events[j][0].record(st)
-            P.svdq_quantize_act_lowrank_down(layer, b["x"], b["xq"], b["xs"], b["xl1"], stream=st)
-            if k1_events is not None:
-                k1_events[j][1].record(st)
-                k2_events[j][0].record(st)
-            P.svdq_gemm_w4a4_lowrank_up(layer, b["xq"], b["xs"], b["xl1"], L.M, Y=b["y"], stream=st)
-            if k2_events is not None:
-                k2_events[j][1].record(st)
+                if k2_events is not None:
+                    k2_events[j][1].record(st)
 
-    # eager warm-up (also sets kernel attributes), then capture the step as CUDA graphs:
-    # one plain (timed region) and one with external timing events around every launch.
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            step(stream)
-    torch.cuda.synchronize()
     ext = lambda: torch.cuda.Event(enable_timing=True, external=True)
-    k1_ev = [(ext(), ext()) for _ in built]
-    k2_ev = [(ext(), ext()) for _ in built]
-    g_plain, g_ev = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-    n0 = P.svdq_launch_count()
-    with torch.cuda.graph(g_plain, stream=stream):
-        step(stream)
-    launches_per_step = P.svdq_launch_count() - n0
-    with torch.cuda.graph(g_ev, stream=stream):
-        step(stream, k1_ev, k2_ev)
-    g_k1, g_k2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g_k1, stream=stream):
-        step(stream, only="k1")
-    with torch.cuda.graph(g_k2, stream=stream):
-        step(stream, only="k2")
-    torch.cuda.synchronize()
     ev = lambda: torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            g_plain.replay()
-    torch.cuda.synchronize()
 
+    def capture(bl):
+        """CUDA graphs of one step: plain (timed region), with external timing events around
+        every launch (per-kernel durations), K1-only and K2-only."""
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                step(bl, stream)
+        torch.cuda.synchronize()
+        g = {"k1_ev": [(ext(), ext()) for _ in bl], "k2_ev": [(ext(), ext()) for _ in bl]}
+        for name in ("plain", "ev", "k1", "k2"):
+            g[name] = torch.cuda.CUDAGraph()
+        n0 = P.svdq_launch_count()
+        with torch.cuda.graph(g["plain"], stream=stream):
+            step(bl, stream)
+        g["launches"] = P.svdq_launch_count() - n0
+        with torch.cuda.graph(g["ev"], stream=stream):
+            step(bl, stream, g["k1_ev"], g["k2_ev"])
+        with torch.cuda.graph(g["k1"], stream=stream):
+            step(bl, stream, only="k1")
+        with torch.cuda.graph(g["k2"], stream=stream):
+            step(bl, stream, only="k2")
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                g["plain"].replay()
+        torch.cuda.synchronize()
+        return g
+
+    def time_graph(gr, n):
+        tot = []
+        for _ in range(n):
+            a, b = ev(), ev()
+            with torch.cuda.stream(stream):
+                l2_flush()
+                a.record(stream)
+                gr.replay()
+                b.record(stream)
+            torch.cuda.synchronize()
+            tot.append(a.elapsed_time(b))
+        return float(np.mean(tot))
+
+    def per_kernel(g, n):
+        k1_rows, k2_rows = [], []
+        for _ in range(n):
+            with torch.cuda.stream(stream):
+                l2_flush()
+                g["ev"].replay()
+            torch.cuda.synchronize()
+            k1_rows.append([a.elapsed_time(b) for a, b in g["k1_ev"]])
+            k2_rows.append([a.elapsed_time(b) for a, b in g["k2_ev"]])
+        return np.array(k1_rows).mean(axis=0) / 1e3, np.array(k2_rows).mean(axis=0) / 1e3   # seconds
+
+    g = capture(built)
     step_ev = [(ev(), ev()) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
@@ -198,45 +237,88 @@ def run_svdq(args, rank, world, local_rank):
     with ClockSampler(dev.index) as clk:
         with torch.cuda.stream(stream):
             for s in range(args.steps):
-                flush.zero_()                       # L2 flush (outside the per-step events)
+                l2_flush()                          # L2 flush (outside the per-step events)
                 step_ev[s][0].record(stream)
-                g_plain.replay()
+                g["plain"].replay()
                 step_ev[s][1].record(stream)
         torch.cuda.synchronize()
-    launches = launches_per_step * args.steps
+    launches = g["launches"] * args.steps
     if world > 1:
         dist.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in step_ev]
-    total_ms = float(sum(step_ms))
-    # per-kernel durations: replay the event graph (same inputs, L2 flushed before each)
-    k1_rows, k2_rows = [], []
-    for s in range(args.steps):
-        with torch.cuda.stream(stream):
-            flush.zero_()
-            g_ev.replay()
-        torch.cuda.synchronize()
-        k1_rows.append([a.elapsed_time(b) for a, b in k1_ev])
-        k2_rows.append([a.elapsed_time(b) for a, b in k2_ev])
-    k1_ms = np.array(k1_rows)
-    k2_ms = np.array(k2_rows)
-    # K1-only / K2-only graphs: the same launches back to back, no K1<->K2 alternation
-    only_ms = {}
-    for name, g in (("k1", g_k1), ("k2", g_k2)):
-        tot = 0.0
-        for s in range(args.steps):
-            a, b = ev(), ev()
-            with torch.cuda.stream(stream):
-                flush.zero_()
-                a.record(stream)
-                g.replay()
-                b.record(stream)
-            torch.cuda.synchronize()
-            tot += a.elapsed_time(b)
-        only_ms[name] = tot / args.steps
+    total_ms = float(sum(a.elapsed_time(b) for a, b in step_ev))
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
+    nrep = max(3, min(args.steps, 20))
+    k1_avg_s, k2_avg_s = per_kernel(g, nrep)
+    only_ms = {"k1": time_graph(g["k1"], nrep), "k2": time_graph(g["k2"], nrep)}
+
+    # ---------------- low-rank overhead: the same step at rank 0
+    lowrank = None
+    if rank == 0 and not args.no_extras:
+        layers0 = [synth.Layer(L.name, L.M, L.K, L.N, 0, L.dtype) for L in layers]
+        built0 = build_layers(P, torch, layers0, args.fmt, dev)
+        g0 = capture(built0)
+        step0_ms = time_graph(g0["plain"], nrep)
+        step_r_ms = time_graph(g["plain"], nrep)
+        k1_0, k2_0 = per_kernel(g0, nrep)
+        lowrank = {
+            "value": round((step_r_ms - step0_ms) / (time_graph(g0["k2"], nrep)), 4),
+            "def": "[t_step(r=32) - t_step(r=0)] / t_K2-only(r=0), CUDA-graph replays, L2 flushed "
+                   "(SURVEY 8(d): [t_K1(r)+t_K2(r)-t_K1(0)-t_K2(0)] / t_K2(0))",
+            "step_ms_r32": round(step_r_ms, 4), "step_ms_r0": round(step0_ms, 4),
+            "per_layer": {L.name: round(float((k1_avg_s[j] + k2_avg_s[j] - k1_0[j] - k2_0[j]) / k2_0[j]), 4)
+                          for j, L in enumerate(layers)},
+        }
+        # ---------------- library context: cuBLASLt NVFP4 GEMM alone on the rank-0 operands
+        library = None
+        if args.fmt == "nvfp4" and hasattr(torch, "float4_e2m1fn_x2"):
+            try:
+                mm = []
+                for (L, layer, b) in built0:
+                    fa = b["xq"].reshape(L.M, L.K // 2).view(torch.float4_e2m1fn_x2)
+                    fb = layer.w_codes.reshape(L.N, L.K // 2).view(torch.float4_e2m1fn_x2)
+                    mm.append((fa, fb.t(), b["xs"].view(torch.float8_e4m3fn),
+                               layer.w_scales.view(torch.float8_e4m3fn), b["y"]))
+                lev = [(ext(), ext()) for _ in mm]
+
+                def lib_step(events=None):
+                    for j, (fa, fbt, sa, sb, y) in enumerate(mm):
+                        if events is not None:
+                            events[j][0].record(stream)
+                        torch._scaled_mm(fa, fbt, sa, sb, out_dtype=torch.bfloat16)
+                        if events is not None:
+                            events[j][1].record(stream)
+                with torch.cuda.stream(stream):
+                    for _ in range(3):
+                        lib_step()
+                torch.cuda.synchronize()
+                gl = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gl, stream=stream):
+                    lib_step(lev)
+                rows = []
+                for _ in range(nrep):
+                    with torch.cuda.stream(stream):
+                        l2_flush()
+                        gl.replay()
+                    torch.cuda.synchronize()
+                    rows.append([a.elapsed_time(b) for a, b in lev])
+                lib_s = np.array(rows).mean(axis=0) / 1e3
+                k2f = np.array([2.0 * L.M * L.N * L.K for L in layers])
+                library = {
+                    "kernel": "cuBLASLt block-scaled NVFP4 GEMM (torch._scaled_mm), plain Q(X)Q(W) only: "
+                              "no smoothing, quantization, low-rank branch or bias",
+                    "tflops": round(float(k2f.sum() / lib_s.sum() / 1e12), 1),
+                    "k2_r0_tflops": round(float(k2f.sum() / k2_0.sum() / 1e12), 1),
+                    "per_layer_tflops": {L.name: round(float(k2f[j] / lib_s[j] / 1e12), 1)
+                                         for j, L in enumerate(layers)},
+                }
+            except Exception as e:  # noqa: BLE001  (context only; never part of the product path)
+                library = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
+        lowrank["library_context"] = library
+        del built0, g0
+        torch.cuda.empty_cache()
 
     # ---------------- end to end through the public API with host buffers
     hx = [b["x"].cpu().pin_memory() for (_, _, b) in built]
@@ -260,7 +342,8 @@ def run_svdq(args, rank, world, local_rank):
         dist.barrier()
     e0, e1 = ev(), ev()
     e0.record(stream)
-    for _ in range(args.steps):
+    n_e2e = max(3, min(args.steps, 20))
+    for _ in range(n_e2e):
         e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
@@ -273,47 +356,51 @@ def run_svdq(args, rank, world, local_rank):
     if rank != 0:
         return None
     pk, pk_kind = peaks()
-    fp4_peak = 4.0 * pk.get("bf16_tflops_sustained", pk["bf16_tflops"])     # guide: fp4 = 4 x bf16 nominal
+    fp4_sus = 4.0 * pk.get("bf16_tflops_sustained", pk["bf16_tflops"])     # guide: fp4 = 4 x bf16 nominal
+    fp4_burst = 4.0 * pk["bf16_tflops"]
     k2_flops = np.array([2.0 * L.M * L.N * L.K for L in layers])
-    k2_avg_s = k2_ms.mean(axis=0) / 1e3
     k2_achieved = float(k2_flops.sum() / k2_avg_s.sum() / 1e12)
-    k1_avg_s = k1_ms.mean(axis=0) / 1e3
     k1_gbs = float(k1_bytes / k1_avg_s.sum() / 1e9)
     value = world * flops * args.steps / (total_ms / 1e3) / 1e12
     per_layer = {L.name: {"M": L.M, "K": L.K, "N": L.N,
                           "k1_us": round(float(k1_avg_s[j] * 1e6), 2),
                           "k2_us": round(float(k2_avg_s[j] * 1e6), 2),
-                          "k2_tflops": round(float(k2_flops[j] / k2_avg_s[j] / 1e12), 1)}
+                          "k2_tflops": round(float(k2_flops[j] / k2_avg_s[j] / 1e12), 1),
+                          "k1_gbs": round(float((L.M * L.K * (2.5625 if args.fmt == "nvfp4" else 2.53125)
+                                                 + 2 * L.M * L.r) / k1_avg_s[j] / 1e9), 1)}
                  for j, L in enumerate(layers)}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "k2_traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get("bytes_per_launch")
     clocks = clk.summary()
+    f_sm = (clocks.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)) * 1e6
+    cfg = bench_config(args, world)
+    cfg["block_latency_ms"] = round(total_ms / args.steps, 4)
     return {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "e2m1 x e2m1 -> f32 (NVFP4 g16 e4m3 scales) + bf16 low-rank",
+        "vs_baseline": None, "dtype": "e2m1 x e2m1 -> f32 (NVFP4 g16 e4m3 scales) + bf16 low-rank"
+        if args.fmt == "nvfp4" else "int4 x int4 -> int32 (kind::i8) -> f32 (g64 16-bit scales) + bf16 low-rank",
         "data": "synthetic (seeded; DESIGN.md input recipe), weights prepared on GPU by svdq_quantize_weights",
-        "config": {"workload": "flux1-dev block linears: 1 double block (img 4096 tok + txt 512 tok: "
-                               "qkv, proj, mlp_up, mlp_down) + 1 single block (4608 tok: linear1, linear2)",
-                   "batch": args.batch, "hidden": 3072, "mlp": 12288, "rank": 32, "format": args.fmt,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "l2": "flushed between steps (512 MiB write outside the per-step events)",
-                   "block_latency_ms": round(total_ms / args.steps, 4)},
-        "roofline": {"bound": "tensor", "achieved": round(k2_achieved, 1), "peak": round(fp4_peak, 1),
-                     "unit": "TFLOP/s", "frac": round(k2_achieved / fp4_peak, 4), "traffic": traffic,
+        "config": cfg,
+        "roofline": {"bound": "tensor", "achieved": round(k2_achieved, 1), "peak": round(fp4_sus, 1),
+                     "unit": "TFLOP/s", "frac": round(k2_achieved / fp4_sus, 4), "traffic": traffic,
                      "kernel": "svdq_gemm_w4a4_lowrank_up (K2, NVFP4)",
                      "peak_source": f"4 x {pk_kind} sustained bf16 (MEASURED_PEAKS.json), guide fp4:bf16 = 9:2.25",
+                     "frac_vs_burst": round(k2_achieved / fp4_burst, 4),
+                     "frac_vs_clock_peak": round(k2_achieved * 1e12 / (148 * 32768 * f_sm), 4),
+                     "clock_peak_def": "148 SMs x 32768 dense FP4 FLOP/clk x median SM clock of the timed region",
                      "achieved_def": "sum 2*M*N*K over the step's linears / sum of K2 CUDA-event durations"},
         "k1": {"bound": "hbm", "achieved": round(k1_gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                "frac": round(k1_gbs / pk["hbm_gbs"], 4),
                "achieved_def": "sum (2MK + 0.5625MK + 2Mr) / sum of K1 durations"},
+        "lowrank_overhead": lowrank,
         "per_layer": per_layer,
-        "e2e": {"value": round(world * flops * args.steps / (e2e_ms / 1e3) / 1e12, 3), "unit": UNIT,
+        "e2e": {"value": round(world * flops * n_e2e / (e2e_ms / 1e3) / 1e12, 3), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms_per_step": round(e2e_ms / args.steps, 3),
+                "ms_per_step": round(e2e_ms / n_e2e, 3),
                 "path": "svdq_linear_forward (C ABI) per linear; pinned host X in, Y out"},
         "graph_only_ms": {"k1_all_layers": round(only_ms["k1"], 4), "k2_all_layers": round(only_ms["k2"], 4),
                           "note": "each kernel's launches replayed back to back as one graph (L2 flushed before)"},
@@ -325,32 +412,46 @@ def run_svdq(args, rank, world, local_rank):
 
 
 # ------------------------------------------------------------------ oracle timings
-def oracle_sample_tflops(layers, rows, budget_s=None):
-    """Oracle forward (K1 + K2 semantics) on `rows` tokens of each layer.  Operands come
-    from the oracle's own prepare_operands with a cheap (randomized) decomposition of
-    W_hat -- weight preparation is offline on both arms and untimed."""
-    from oracle import svdquant as S
+def oracle_operands(L, i, fmt):
+    """Valid stored operands of the layer's shape for TIMING the oracle forward: random
+    E2M1 / INT4 codes and scale bytes, bf16 L1s / L2s, lambda from the input recipe.  The
+    oracle's forward cost does not depend on the values; its weight preparation (SVD,
+    residual quantization) is offline on both arms and untimed."""
     from oracle import formats as F
+    from oracle import svdquant as S
+    g = np.random.default_rng(7000 + i)
+    if fmt == "nvfp4":
+        codes = g.integers(0, 16, (L.N, L.K), dtype=np.uint8)
+        scales = g.integers(0x30, 0x40, (L.N, L.K // 16), dtype=np.uint8)
+        sdt, gs_w = "e4m3", np.float32(0.01)
+    else:
+        codes = g.integers(-7, 8, (L.N, L.K), dtype=np.int8)
+        scales = F.bf16_bits(g.uniform(0.005, 0.02, (L.N, L.K // 64)))
+        sdt, gs_w = "bf16", np.float32(1.0)
+    lam_inv = np.float32(1.0) / np.abs(g.standard_normal(L.K)).astype(np.float32).clip(0.1, 10)
+    l1s = F.bf16_bits(g.standard_normal((L.r, L.K)) * 0.02)
+    l2s = F.bf16_bits(g.standard_normal((L.N, L.r)) * 0.02)
+    bias = F.bf16_round(synth.gen_bias(L.N, synth.rng(4, i, 3)))
+    return S.Operands(fmt, L.K, L.N, L.r, codes, scales, sdt, gs_w, np.float32(1.0),
+                      lam_inv.astype(np.float32), l1s, l2s, bias)
+
+
+def oracle_forward_time(layers, rows, fmt, idx=None):
+    """Seconds and algorithmic FLOPs of the oracle forward (K1 + K2 semantics) on `rows`
+    tokens of each layer (the layers' own synthetic activations, first `rows` rows)."""
+    from oracle import formats as F
+    from oracle import svdquant as S
     t_total, flops = 0.0, 0.0
     for i, L in enumerate(layers):
-        w = synth.gen_w(L.K, L.N, synth.rng(4, i, 1))
-        xcal = synth.gen_x(256, L.K, synth.rng(4, i, 2))
-        lam = S.compute_smoothing(xcal, w, 0.5)
-        w_hat = S.smooth_weight(w, lam)
-        g = np.random.default_rng(i).standard_normal((L.N, L.r + 8))
-        q, _ = np.linalg.qr(w_hat @ g)
-        u, s, vt = np.linalg.svd(q.T @ w_hat, full_matrices=False)
-        L1 = (q @ u[:, :L.r]) * s[:L.r]
-        L2 = vt[:L.r]
-        d = S.Decomposition(w_hat, L1, L2, w_hat - L1 @ L2, s)
-        ops = S.prepare_operands(w, lam, L.r, "nvfp4", decomp=d,
-                                 bias=F.bf16_round(synth.gen_bias(L.N, synth.rng(4, i, 3))))
+        if idx is not None and i not in idx:
+            continue
+        ops = oracle_operands(L, i, fmt)
         x = F.bf16_round(synth.gen_x(rows, L.K, synth.rng(4, i, 0)))
         t0 = time.perf_counter()
         S.forward(x, ops)
         t_total += time.perf_counter() - t0
         flops += 2.0 * rows * L.N * L.K
-    return flops / t_total / 1e12, t_total
+    return t_total, flops
 
 
 def blas_threads():
@@ -362,24 +463,29 @@ def blas_threads():
 
 
 def run_reference(args):
+    """The reference arm of this tier: the CPU oracle, as it stands, on the same workload.
+    Step s = the oracle forward of `--ref-rows` tokens of linear (s mod 10) of the step, so
+    every step is a bounded sample and the run ends within a few minutes."""
     layers = flux_block_layers(args.batch)
     rows = args.ref_rows
-    for _ in range(args.warmup):
-        oracle_sample_tflops(layers[:1], 8)
-    vals, ts = [], []
-    for _ in range(args.steps):
-        v, t = oracle_sample_tflops(layers, rows)
-        vals.append(v)
+    for w in range(args.warmup):
+        oracle_forward_time(layers, 8, args.fmt, idx={w % len(layers)})
+    t_all, f_all, ts = 0.0, 0.0, []
+    for s in range(args.steps):
+        t, f = oracle_forward_time(layers, rows, args.fmt, idx={s % len(layers)})
+        t_all += t
+        f_all += f
         ts.append(t)
-    value = float(np.mean(vals))
+    value = f_all / t_all / 1e12
     cores = blas_threads()
-    sample = f"{rows} tokens of each of the step's {len(layers)} linears per step (oracle forward, fp64)"
+    sample = (f"{rows} tokens of one of the step's {len(layers)} linears per step (rotating; oracle "
+              f"forward in fp64 with NumPy/BLAS)")
     return {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * float(np.mean(ts)), 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle)",
         "data": "synthetic (seeded)",
-        "config": {"workload": "flux1-dev block linears (row sample)", "rank": 32, "format": args.fmt},
+        "config": bench_config(args, 1),
         "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -389,7 +495,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="svdq", choices=["svdq", "reference"])
     ap.add_argument("--fmt", default="nvfp4", choices=["nvfp4", "int4"])
@@ -397,6 +503,7 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=32)
     ap.add_argument("--cpu-rows", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the rank-0 overhead / library legs")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "svdq":
         args.warmup = 3
@@ -418,11 +525,11 @@ def main():
     out = run_svdq(args, rank, world, local_rank)
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:
-            v, t = oracle_sample_tflops(flux_block_layers(args.batch)[:2], args.cpu_rows)
-            out["cpu_baseline"] = {"value": round(v, 6), "unit": UNIT, "cores": blas_threads(),
+            t, f = oracle_forward_time(flux_block_layers(args.batch), args.cpu_rows, args.fmt)
+            out["cpu_baseline"] = {"value": round(f / t / 1e12, 6), "unit": UNIT, "cores": blas_threads(),
                                    "kind": "oracle",
-                                   "sample": f"{args.cpu_rows} tokens of the img qkv + proj linears "
-                                             f"(oracle forward, {t:.1f} s)"}
+                                   "sample": f"{args.cpu_rows} tokens of each of the step's 10 linears "
+                                             f"(oracle forward, fp64 NumPy/BLAS; {t:.1f} s of CPU time)"}
         print(json.dumps(out))
     if world > 1:
         import torch.distributed as dist

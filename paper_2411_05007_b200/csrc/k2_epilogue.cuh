@@ -19,68 +19,67 @@ __device__ __forceinline__ uint32_t pack2(float a, float b, int dt) {
          (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(b))) << 16);
 }
 
-// Drains this warp's share of the tile: `nwarps_per_quad` warps share a TMEM lane quadrant
-// (32 rows) and take interleaved 64-byte column chunks (32 bf16/fp16 or 16 fp32 columns).
-// Each chunk is staged in a 2 KB buffer (two per warp) with the 64-byte swizzle of the store
-// map (16-byte column j of row r at j ^ ((r >> 1) & 3)), then written by a TMA bulk tensor
-// store.  `release` runs once every tcgen05.ld of the tile has completed.
+// Drains this warp's share of the tile: `NWQ` warps share a TMEM lane quadrant (32 rows) and
+// take interleaved 32-column blocks.  All of the warp's tcgen05.ld are issued back to back
+// and the accumulator is released (`release`) as soon as they complete, BEFORE any math or
+// store: the MMA warp can then start the tile after next while this warp converts and stores
+// (measured: releasing after the last 64-B chunk's store cost ~15 % of the issuer's time at
+// K = 3072).  Each 64-byte column chunk (32 bf16/fp16 or 16 fp32 columns) is staged in a 2 KB
+// buffer (two per warp) with the 64-byte swizzle of the store map (16-byte column j of row r
+// at j ^ ((r >> 1) & 3)), then written by a TMA bulk tensor store.
 template <int NCOLS, int NWQ, typename Release>
 __device__ __forceinline__ void epilogue_tile(uint32_t tmem_acc_lane, const float *bias_s, float alpha, int y_dtype,
                                               const CUtensorMap *tmY, int32_t row0, int32_t col0, int sub,
                                               uint8_t *stage, int &buf, int lane, Release release) {
-  const int cpc = y_dtype == 2 ? 16 : 32;                 // columns per 64-byte chunk
-  const int nchunks = NCOLS / cpc;
-  const int last = sub + ((nchunks - 1 - sub) / NWQ) * NWQ;
-  for (int ch = sub; ch < nchunks; ch += NWQ) {
-    float v[32];
-    if (y_dtype == 2) {
-      uint32_t r[16];
-      tmem_ld_32x32b_x16(tmem_acc_lane + ch * 16, r);
-      tmem_ld_wait();
+  constexpr int NB = NCOLS / (32 * NWQ);                  // 32-column blocks per warp
+  static_assert(NCOLS % (32 * NWQ) == 0, "column split");
+  uint32_t r[NB][32];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-    } else {
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(tmem_acc_lane + ch * 32, r);
-      tmem_ld_wait();
+  for (int i = 0; i < NB; ++i) tmem_ld_32x32b_x32(tmem_acc_lane + (sub + i * NWQ) * 32, r[i]);
+  tmem_ld_wait();
+  release();
+  const uint32_t sw = static_cast<uint32_t>((lane >> 1) & 3);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-    }
-    if (ch == last) release();
-    uint8_t *sb = stage + buf * 2048;
-    if (lane == 0) bulk_wait_group_read<1>();            // the store that last used sb has read it
-    __syncwarp();
-    const float *bs = bias_s + ch * cpc;
-    uint8_t *rowp = sb + lane * 64;
-    const uint32_t sw = static_cast<uint32_t>((lane >> 1) & 3);
-    if (y_dtype == 2) {
+  for (int i = 0; i < NB; ++i) {
+    const int cb = sub + i * NWQ;
+    const float *bs = bias_s + cb * 32;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float4 o;
-        o.x = __fadd_rn(__fmul_rn(alpha, v[4 * c + 0]), bs[4 * c + 0]);
-        o.y = __fadd_rn(__fmul_rn(alpha, v[4 * c + 1]), bs[4 * c + 1]);
-        o.z = __fadd_rn(__fmul_rn(alpha, v[4 * c + 2]), bs[4 * c + 2]);
-        o.w = __fadd_rn(__fmul_rn(alpha, v[4 * c + 3]), bs[4 * c + 3]);
-        *reinterpret_cast<float4 *>(rowp + ((c ^ sw) * 16)) = o;
+    for (int h = 0; h < 2; ++h) {
+      if (y_dtype != 2 && h == 1) break;                  // 16-bit: one 64-B chunk per block
+      uint8_t *sb = stage + buf * 2048;
+      if (lane == 0) bulk_wait_group_read<1>();          // the store that last used sb has read it
+      __syncwarp();
+      uint8_t *rowp = sb + lane * 64;
+      if (y_dtype == 2) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float4 o;
+          const int j = 16 * h + 4 * c;
+          o.x = __fadd_rn(__fmul_rn(alpha, __uint_as_float(r[i][j + 0])), bs[j + 0]);
+          o.y = __fadd_rn(__fmul_rn(alpha, __uint_as_float(r[i][j + 1])), bs[j + 1]);
+          o.z = __fadd_rn(__fmul_rn(alpha, __uint_as_float(r[i][j + 2])), bs[j + 2]);
+          o.w = __fadd_rn(__fmul_rn(alpha, __uint_as_float(r[i][j + 3])), bs[j + 3]);
+          *reinterpret_cast<float4 *>(rowp + ((c ^ sw) * 16)) = o;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[e] = __fadd_rn(__fmul_rn(alpha, __uint_as_float(r[i][8 * c + e])), bs[8 * c + e]);
+          *reinterpret_cast<uint4 *>(rowp + ((c ^ sw) * 16)) =
+              make_uint4(pack2(o[0], o[1], y_dtype), pack2(o[2], o[3], y_dtype), pack2(o[4], o[5], y_dtype),
+                         pack2(o[6], o[7], y_dtype));
+        }
       }
-    } else {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float o[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = __fadd_rn(__fmul_rn(alpha, v[8 * c + e]), bs[8 * c + e]);
-        *reinterpret_cast<uint4 *>(rowp + ((c ^ sw) * 16)) =
-            make_uint4(pack2(o[0], o[1], y_dtype), pack2(o[2], o[3], y_dtype), pack2(o[4], o[5], y_dtype),
-                       pack2(o[6], o[7], y_dtype));
+      fence_proxy_async();                                 // generic smem writes -> TMA (async proxy)
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmY, sb, col0 + cb * 32 + h * 16, row0);
+        bulk_commit_group();
       }
+      buf ^= 1;
     }
-    fence_proxy_async();                                   // generic smem writes -> TMA (async proxy)
-    __syncwarp();
-    if (lane == 0) {
-      tma_store_2d(tmY, sb, col0 + ch * cpc, row0);
-      bulk_commit_group();
-    }
-    buf ^= 1;
   }
 }
 

@@ -149,13 +149,16 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t full0 = mapa_u32(&full[0], 0);      // leader's barriers
       int s = 0;
       uint32_t ph = 0;
+#ifdef SVDQ_TRACE
+      long long t_pwait = 0;
+#endif
       for (int t = pair; t < tiles; t += npairs) {
         const int64_t m0 = static_cast<int64_t>(t % mt_count) * 256;
         const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
         const int32_t ma = static_cast<int32_t>(m0 + 128 * crank);
         const int32_t nb = static_cast<int32_t>(n0 + BNH * crank);
         for (int kt = 0; kt < nkt; ++kt) {
-          mbar_wait(&empty[s], ph ^ 1);
+          { K2T_BEGIN(); mbar_wait(&empty[s], ph ^ 1); K2T_ACC(t_pwait); }
           uint8_t *st = smem + s * STAGE;
           const uint32_t fb = full0 + s * 8;
           if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE);
@@ -176,6 +179,9 @@ __global__ void __launch_bounds__(320, 1)
           if (++s == kStages) { s = 0; ph ^= 1; }
         }
       }
+#ifdef SVDQ_TRACE
+      if (crank == 0 && pair < 148) g_k2p_trace[pair][6] = t_pwait;
+#endif
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader)
@@ -286,6 +292,10 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t acc_empty0 = mapa_u32(&acc_empty[0], 0);
     int acc_i = 0;
     int ebuf = 0;
+#ifdef SVDQ_TRACE
+    long long t_ewait = 0, t_edrain = 0;
+    const long long t_estart = clock64();
+#endif
     griddep_wait();
     for (int t = pair; t < tiles; t += npairs, ++acc_i) {
       const int b = acc_i & 1;
@@ -297,16 +307,27 @@ __global__ void __launch_bounds__(320, 1)
       for (int c = et; c < BN; c += 256)
         bias_s[c] = (p.bias && n0 + c < p.N) ? load_bias(p.bias, p.bias_dtype, n0 + c) : 0.f;
       named_bar(1, 256);
-      mbar_wait(&acc_full[b], acc_ph);
+      { K2T_BEGIN(); mbar_wait(&acc_full[b], acc_ph); K2T_ACC(t_ewait); }
       tc_fence_after();
+#ifdef SVDQ_TRACE
+      const long long _td = clock64();
+#endif
       epilogue_tile<BN, 2>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
                            &tmY, static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
                            smem + EPI_OFF + (warp - 2) * 4096, ebuf, lane, [&]() {
                           tc_fence_before();
                           __syncwarp();
                           if (lane == 0) mbar_arrive_cluster(acc_empty0 + b * 8);
+#ifdef SVDQ_TRACE
+                          t_edrain += clock64() - _td;
+#endif
                         });
     }
+#ifdef SVDQ_TRACE
+    if (warp == 2 && lane == 0 && crank == 0 && pair < 148) {
+      g_k2p_trace[pair][3] = t_ewait; g_k2p_trace[pair][4] = t_edrain; g_k2p_trace[pair][5] = clock64() - t_estart;
+    }
+#endif
   }
   if (warp >= 2 && lane == 0) bulk_wait_group<0>();    // outstanding TMA stores done
   tc_fence_before();

@@ -25,7 +25,8 @@ pair = os.environ.get("SVDQ_K2_PAIR") == "1"
 (P.abi.lib().svdq_k2p_trace_read if pair else P.abi.lib().svdq_k2_trace_read)(buf)
 if pair:
     t = np.array(buf[:], dtype=np.int64).reshape(148, 8)[:74]
-    for i, n in enumerate(["mma_acc_wait", "mma_full_wait", "mma_total"]):
+    for i, n in enumerate(["mma_acc_wait", "mma_full_wait", "mma_total", "epi_accfull_wait", "epi_drain",
+                           "epi_total", "prod_empty_wait"]):
         print("%-16s median %9.0f  min %9.0f  max %9.0f" % (n, np.median(t[:, i]), t[:, i].min(), t[:, i].max()))
     sys.exit(0)
 t = np.array(buf[:], dtype=np.int64).reshape(148, 8)
