@@ -50,11 +50,18 @@ constexpr int B_BYTES = BNH * 128;            // 12 KB
 constexpr int SFA_BYTES = 2048;
 constexpr int SFB_BYTES = 4096;               // two 128-row atoms x 4 K-blocks
 constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;   // 34 KB
-constexpr int kStages = 5;
+#ifndef SVDQ_K2P_STAGES
+#define SVDQ_K2P_STAGES 5
+#endif
+#ifndef SVDQ_K2P_EPIBUF
+#define SVDQ_K2P_EPIBUF 2
+#endif
+constexpr int kStages = SVDQ_K2P_STAGES;
+constexpr int kEpiBuf = SVDQ_K2P_EPIBUF;      // 2 KB staging buffers per epilogue warp
 constexpr int SF_COLS = 48;
 constexpr int SF_BASE = 2 * BN;
 constexpr int EPI_OFF = kStages * STAGE;                 // 4 epilogue warps x two 4 KB staging buffers
-constexpr int BAR_OFF = EPI_OFF + 8 * 4096;
+constexpr int BAR_OFF = EPI_OFF + 8 * 2048 * kEpiBuf;
 constexpr int SMEM = BAR_OFF + 256 + BN * 4 + 1024;
 static_assert(STAGE % 1024 == 0, "stage alignment");
 static_assert(SF_BASE + 2 * SF_COLS <= 512, "TMEM budget");
@@ -161,6 +168,11 @@ __global__ void __launch_bounds__(320, 1)
           { K2T_BEGIN(); mbar_wait(&empty[s], ph ^ 1); K2T_ACC(t_pwait); }
           uint8_t *st = smem + s * STAGE;
           const uint32_t fb = full0 + s * 8;
+#if SVDQ_EXP & 4                                         // ablation: no operand traffic at all
+          if (crank == 0) mbar_arrive(&full[s]);
+          if (++s == kStages) { s = 0; ph ^= 1; }
+          continue;
+#endif
           if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE);
           tma_load_2d_cg2(st, &tmA, fb, kt * 128, ma);
           tma_load_2d_cg2(st + A_BYTES, &tmB, fb, kt * 128, nb);
@@ -223,13 +235,13 @@ __global__ void __launch_bounds__(320, 1)
             if (nsub == 4) {
             #pragma unroll
               for (int i = 0; i < 4; ++i) {
-#if SVDQ_EXP < 2
+#if (SVDQ_EXP & 3) < 2
                 tmem_cp_32x128b_warpx4_cg2(sfa_col + 4 * i, sfa_d + 32 * i);
 #endif
-#if SVDQ_EXP < 1
+#if (SVDQ_EXP & 3) < 1
                 tmem_cp_32x128b_warpx4_cg2(sfb_col + 8 * i, sfb_d + 32 * i);
 #endif
-#if SVDQ_EXP < 1
+#if (SVDQ_EXP & 3) < 1
                 tmem_cp_32x128b_warpx4_cg2(sfb_col + 8 * i + 4, sfb_d + 128 + 32 * i);
 #endif
               }
@@ -239,13 +251,13 @@ __global__ void __launch_bounds__(320, 1)
                       (kt | i) != 0);
             } else {
               for (int i = 0; i < nsub; ++i) {
-#if SVDQ_EXP < 2
+#if (SVDQ_EXP & 3) < 2
                 tmem_cp_32x128b_warpx4_cg2(sfa_col + 4 * i, sfa_d + 32 * i);
 #endif
-#if SVDQ_EXP < 1
+#if (SVDQ_EXP & 3) < 1
                 tmem_cp_32x128b_warpx4_cg2(sfb_col + 8 * i, sfb_d + 32 * i);
 #endif
-#if SVDQ_EXP < 1
+#if (SVDQ_EXP & 3) < 1
                 tmem_cp_32x128b_warpx4_cg2(sfb_col + 8 * i + 4, sfb_d + 128 + 32 * i);
 #endif
               }
@@ -312,9 +324,24 @@ __global__ void __launch_bounds__(320, 1)
 #ifdef SVDQ_TRACE
       const long long _td = clock64();
 #endif
-      epilogue_tile<BN, 2>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
+#if SVDQ_EXP & 16                                        // ablation: no epilogue work at all
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc_empty0 + b * 8);
+      continue;
+#endif
+#ifdef SVDQ_EPI_DIRECT
+      epilogue_tile_direct<BN, 2>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha,
+                                  p.y_dtype, p.Y, p.ldy, p.M, p.N, m0 + quad * 32, n0, (warp - 2) >> 2, lane, [&]() {
+                                    tc_fence_before();
+                                    __syncwarp();
+                                    if (lane == 0) mbar_arrive_cluster(acc_empty0 + b * 8);
+                                  });
+      continue;
+#endif
+      epilogue_tile<BN, 2, kEpiBuf>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
                            &tmY, static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
-                           smem + EPI_OFF + (warp - 2) * 4096, ebuf, lane, [&]() {
+                           smem + EPI_OFF + (warp - 2) * 2048 * kEpiBuf, ebuf, lane, [&]() {
                           tc_fence_before();
                           __syncwarp();
                           if (lane == 0) mbar_arrive_cluster(acc_empty0 + b * 8);

@@ -10,9 +10,20 @@ dev = torch.device("cuda")
 layer = P.QuantizedLinear.empty("nvfp4", K, 64, r, device=dev)
 layer.lambda_inv.fill_(1.0); layer.l1s.zero_(); layer._sync_view()
 x = torch.from_numpy(synth.gen_x(M, K, synth.rng(9, 0, 0))).to(dev).to(torch.bfloat16)
+cold = os.environ.get("COLD", "0") == "1"
+flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 for _ in range(3):
     P.svdq_quantize_act_lowrank_down(layer, x)
 torch.cuda.synchronize()
+if cold:
+    flush.zero_()
+    flush[: 256 << 20].view(torch.int64).sum()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+P.svdq_quantize_act_lowrank_down(layer, x)
+e1.record()
+torch.cuda.synchronize()
+print("cold" if cold else "warm", "event time %.2f us" % (e0.elapsed_time(e1) * 1e3))
 buf = (ctypes.c_ulonglong * 256)()
 P.abi.lib().svdq_k1_trace_read(buf)
 t = np.array(buf[:], dtype=np.int64)
