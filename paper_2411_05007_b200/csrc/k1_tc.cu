@@ -176,25 +176,36 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------------------------------------------------------- producer
     if (elect_one()) {
-      griddep_wait();                                  // X may be the previous kernel's output
       const uint32_t bytes = 16384 + ((SVDQ_K1EXP & 4) ? 0 : r * 128) + 256;
-      // warm L2 with the first ring's worth of X tiles beyond what the smem ring holds
-      for (int i = S; i < nsteps && i < 2 * S; ++i)
+      // Before the programmatic dependency resolves (the previous kernel may still be running
+      // and may be producing X): warm L2 with the first two rings' worth of X tiles -- an L2
+      // prefetch never returns stale data, L2 being the point of coherence -- and stage the
+      // first ring's L1s / lambda_inv tiles, which no kernel of this stream writes.
+      for (int i = 0; i < nsteps && i < 2 * S; ++i)
         tma_prefetch_2d(&tmX, (kb_begin + i) * 64, static_cast<int32_t>(row0));
-      for (int i = 0; i < nsteps; ++i) {
+      auto load_weights = [&](int i) {
         const int s = i % S;
-        const uint32_t ph = (i / S) & 1;
         const int kb = kb_begin + i;
-        mbar_wait_spin(&empty[s], ph ^ 1);
-        TRACE(2 + i);                                     // producer issues stage i
-        if (i + 2 * S < nsteps) tma_prefetch_2d(&tmX, (kb_begin + i + 2 * S) * 64, static_cast<int32_t>(row0));
         uint8_t *st = smem + s * Ly.stage_bytes;
         mbar_arrive_expect_tx(&full[s], bytes);
-        tma_load_2d(st, &tmX, &full[s], kb * 64, static_cast<int32_t>(row0));
         if (r && !(SVDQ_K1EXP & 4)) tma_load_2d(st + 16384, &tmL, &full[s], kb * 64, 0);
         // lambda_inv block as [2][32] fp32 with 128-B swizzle: the four 64-B lane groups land in
         // distinct banks, so the quantizers' broadcast loads are conflict-free
         tma_load_2d(st + 16384 + r * 128, &tmLam, &full[s], 0, kb * 2);
+      };
+      for (int i = 0; i < nsteps && i < S; ++i) load_weights(i);
+      griddep_wait();                                  // X may be the previous kernel's output
+      for (int i = 0; i < nsteps; ++i) {
+        const int s = i % S;
+        const uint32_t ph = (i / S) & 1;
+        const int kb = kb_begin + i;
+        if (i >= S) {
+          mbar_wait_spin(&empty[s], ph ^ 1);
+          load_weights(i);
+        }
+        TRACE(2 + i);                                     // producer issues stage i
+        if (i + 2 * S < nsteps) tma_prefetch_2d(&tmX, (kb_begin + i + 2 * S) * 64, static_cast<int32_t>(row0));
+        tma_load_2d(smem + s * Ly.stage_bytes, &tmX, &full[s], kb * 64, static_cast<int32_t>(row0));
       }
     }
   } else if (warp == 1) {

@@ -152,22 +152,43 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (elect_one()) {
-      griddep_wait();                                    // xq / xs / xl1 come from K1
       const uint32_t full0 = mapa_u32(&full[0], 0);      // leader's barriers
       int s = 0;
       uint32_t ph = 0;
 #ifdef SVDQ_TRACE
       long long t_pwait = 0;
 #endif
+      // Weight tiles (B, SFB) of the first tile's first ring do not depend on K1: issue them
+      // before the programmatic dependency resolves, so they land while K1 finishes.
+      const int pre = (SVDQ_EXP & 4) || pair >= tiles ? 0 : min(kStages, nkt);
+      {
+        const int64_t n0 = static_cast<int64_t>(pair / mt_count) * BN;
+        for (int kt = 0; kt < pre; ++kt) {
+          uint8_t *st = smem + kt * STAGE;
+          const uint32_t fb = full0 + kt * 8;
+          if (crank == 0) mbar_arrive_expect_tx(&full[kt], 2 * STAGE);
+          tma_load_2d_cg2(st + A_BYTES, &tmB, fb, kt * 128, static_cast<int32_t>(n0 + BNH * crank));
+          tma_load_3d_cg2(st + A_BYTES + B_BYTES + SFA_BYTES, &tmSFB, fb, 0, kt * 4,
+                          static_cast<int32_t>(n0 / 128));
+        }
+      }
+      griddep_wait();                                    // xq / xs / xl1 come from K1
+      bool first = true;
       for (int t = pair; t < tiles; t += npairs) {
         const int64_t m0 = static_cast<int64_t>(t % mt_count) * 256;
         const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
         const int32_t ma = static_cast<int32_t>(m0 + 128 * crank);
         const int32_t nb = static_cast<int32_t>(n0 + BNH * crank);
         for (int kt = 0; kt < nkt; ++kt) {
-          { K2T_BEGIN(); mbar_wait(&empty[s], ph ^ 1); K2T_ACC(t_pwait); }
           uint8_t *st = smem + s * STAGE;
           const uint32_t fb = full0 + s * 8;
+          if (first && kt < pre) {                         // B / SFB already in flight
+            tma_load_2d_cg2(st, &tmA, fb, kt * 128, ma);
+            tma_load_3d_cg2(st + A_BYTES + B_BYTES, &tmSFA, fb, 0, kt * 4, static_cast<int32_t>(m0 / 128 + crank));
+            if (++s == kStages) { s = 0; ph ^= 1; }
+            continue;
+          }
+          { K2T_BEGIN(); mbar_wait(&empty[s], ph ^ 1); K2T_ACC(t_pwait); }
 #if SVDQ_EXP & 4                                         // ablation: no operand traffic at all
           if (crank == 0) mbar_arrive(&full[s]);
           if (++s == kStages) { s = 0; ph ^= 1; }
@@ -181,6 +202,7 @@ __global__ void __launch_bounds__(320, 1)
                           static_cast<int32_t>(n0 / 128));
           if (++s == kStages) { s = 0; ph ^= 1; }
         }
+        first = false;
         for (int j = 0; j < nslab; ++j) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t *st = smem + s * STAGE;

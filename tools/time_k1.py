@@ -1,4 +1,6 @@
-"""Time K1 alone on one shape (graph of 10 launches over 3 distinct DRAM-cold inputs).
+"""Time K1 alone on one shape: a CUDA graph of 10 launches cycling over distinct DRAM-cold
+inputs (back to back), and single launches with an L2 flush (512 MiB write + 256 MiB read)
+before each (the bench's condition).
     SVDQ_LIB=... python tools/time_k1.py M K [r]"""
 import os, sys
 import torch
@@ -19,10 +21,30 @@ g = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g, stream=s):
     for i in range(10):
         P.svdq_quantize_act_lowrank_down(layer, xs[i % nb], xq, xsc, xl1, stream=s)
+g1 = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g1, stream=s):
+    P.svdq_quantize_act_lowrank_down(layer, xs[0], xq, xsc, xl1, stream=s)
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 with torch.cuda.stream(s):
     g.replay()
     a.record(s); g.replay(); b.record(s)
 torch.cuda.synchronize()
 us = a.elapsed_time(b) / 10 * 1e3
-print(f"K1 M={M} K={K} r={r} lib={os.path.basename(os.environ.get('SVDQ_LIB', 'libsvdq.so'))}: {us:.2f} us  {M*K*2.5625/us/1e3:.2f} TB/s")
+flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+sink = torch.empty((), dtype=torch.int64, device=dev)
+tf, tw = [], []
+for i in range(10):
+    with torch.cuda.stream(s):
+        flush.zero_(); sink.copy_(flush[: 256 << 20].view(torch.int64).sum())
+        a.record(s); g1.replay(); b.record(s)
+    torch.cuda.synchronize()
+    tf.append(a.elapsed_time(b) * 1e3)
+    with torch.cuda.stream(s):
+        a.record(s); g1.replay(); b.record(s)
+    torch.cuda.synchronize()
+    tw.append(a.elapsed_time(b) * 1e3)
+tf = sum(tf) / len(tf); tw = sum(tw) / len(tw)
+B = M * K * 2.5625 + 2 * M * r
+print(f"K1 M={M} K={K} r={r} lib={os.path.basename(os.environ.get('SVDQ_LIB', 'libsvdq.so'))}: "
+      f"back-to-back cold {us:.2f} us ({B/us/1e3:.2f} TB/s) | single after flush {tf:.2f} us ({B/tf/1e3:.2f} TB/s) "
+      f"| single L2-warm {tw:.2f} us")
