@@ -6,19 +6,24 @@
 //   facc[m,n] += fl32(fl32(f32(acc_g[m,n]) * sx[m,g]) * sw[n,g])      (App. B.5, Q23)
 //   Y = out_rn(facc + sum_t xl1[m,t] l2s[n,t] + bias[n])
 //
-// Persistent, one CTA per SM over 128 x 128 tiles; 14 warps:
+// Persistent, one CTA per SM over 128 x 128 tiles; 20 warps:
 //   warp 0      TMA producer: packed code tiles [rows x 64 B] (two K groups) into a
 //               4-deep ring; at each tile start the low-rank slabs (xl1 / l2s, SW128).
 //   warp 1      TMEM allocator + MMA issuer: per K group two kind::i8 MMAs (K = 32)
 //               into one of two int32 TMEM buffers; the low-rank slab (kind::f16)
 //               into an fp32 TMEM region.
-//   warps 2..5  unpackers: int4 nibbles -> int8 (sign extended with byte-SIMD ops) in
+//   warps 2..3  unpackers (two rows of A and B per thread): int4 nibbles -> int8 (sign extended with byte-SIMD ops) in
 //               the 128-B swizzled K-major layout the MMA reads.  Within every aligned
 //               16-element block the k order is permuted identically for A and B, which
 //               leaves every group sum unchanged.
-//   warps 6..13 epilogue (two per TMEM lane quadrant, 64 columns each): per group
-//               tcgen05.ld of the int32 sums, promotion, release; per tile the low-rank
-//               term, bias, store.  Debug mode stores acc_g instead.
+//   warps 4..19 epilogue (four per TMEM lane quadrant, 32 columns each): per group one
+//               tcgen05.ld of the int32 sums, immediate release of the buffer, then the
+//               promotion on packed fp32 pairs (add/mul/fma .f32x2: 2.5 issue slots per
+//               element); sx / sw for the next 8 groups are fetched while the current 8 are
+//               promoted (sx in registers, sw broadcast from a per-warp smem buffer).  Per
+//               tile the low-rank term, bias, store.  Debug mode stores acc_g instead.
+// The promotion is ~3x the kind::i8 MMA time per group, so 16 warps keep all four
+// schedulers busy while the tensor core idles.
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -27,28 +32,86 @@
 #include "k1_launch.h"
 #include "sm100.cuh"
 
+#ifndef SVDQ_I4EXP
+#define SVDQ_I4EXP 0   // ablation bits: 1 no scale fetch, 2 no promotion math, 4 no unpack, 8 no MMA
+#endif
+
+#ifdef SVDQ_TRACE
+namespace svdq { __device__ unsigned long long g_i4_trace[148][8]; }
+extern "C" int svdq_i4_trace_read(unsigned long long *host) {
+  return cudaMemcpyFromSymbol(host, svdq::g_i4_trace, sizeof(unsigned long long) * 148 * 8) == cudaSuccess ? 0 : 1;
+}
+#define I4T_BEGIN() long long _t0 = clock64()
+#define I4T_ACC(v) (v) += clock64() - _t0
+#else
+#define I4T_BEGIN() do {} while (0)
+#define I4T_ACC(v) do {} while (0)
+#endif
+
 namespace svdq {
 
 namespace {
 
 constexpr int BM = 128;
 constexpr int BN = kInt4BN;                 // 128
-constexpr int kPStages = 4;                 // packed ring
+constexpr int kPStages = 3;                 // packed ring
 constexpr int kUStages = 2;                 // unpacked (int8) ring
 constexpr int PA = BM * 64, PB = BN * 64;   // packed bytes per stage (128 K elements)
 constexpr int UA = BM * 128, UB = BN * 128; // int8 bytes per stage
 constexpr int SLAB = BM * 128 + BN * 128;   // one 64-wide low-rank slab (bf16)
 constexpr int kMaxSlabs = 2;
+constexpr int kEpiWarps = 16;               // four per TMEM lane quadrant, 32 columns each
+constexpr int EC = 32;                      // epilogue columns per warp
+constexpr int kGB = 8;                      // groups per scale block
+constexpr int SWST = (2 * kGB * EC + EC) * 4;   // per-warp sw + sx staging (one block) + bias, bytes
 constexpr int OFF_U = 0;
 constexpr int OFF_SLAB = OFF_U + kUStages * (UA + UB);
 constexpr int OFF_P = OFF_SLAB + kMaxSlabs * SLAB;
 constexpr int OFF_SW = OFF_P + kPStages * (PA + PB);
-constexpr int OFF_BAR = OFF_SW + 2 * BN * 4 + 2 * BN * 4;
+constexpr int OFF_BAR = OFF_SW + kEpiWarps * SWST;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
-constexpr int kThreads = 448;          // 14 warps
-constexpr int kEpiWarps = 8;           // two per TMEM lane quadrant, 64 columns each
-constexpr int EC = BN / 2;             // epilogue columns per warp
-constexpr uint32_t TM_LR = 2 * BN;          // low-rank fp32 region after two int32 buffers
+constexpr int kUnpackWarps = 2;
+constexpr int kThreads = 32 * (2 + kUnpackWarps + kEpiWarps);   // 20 warps: 5 per scheduler -> 96 regs
+constexpr int kAcc = 4;                     // TMEM accumulator ring: 4 x 128 columns = all 512
+// One ring slot per K group (int32 sums); the tile's low-rank slab (fp32) takes a slot as a
+// pseudo-group ahead of the first K group.  A ring of 4 lets the MMA run up to four groups
+// ahead of the promotion, hiding the commit -> tcgen05.ld -> release round trip (~1900 cycles
+// measured; a 2-deep ring was bound at half of that per group).
+static_assert(SMEM <= 227 * 1024, "smem budget");
+
+__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float4 lds_f32x4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
 
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -66,20 +129,32 @@ __device__ __forceinline__ void sts128(void *p, uint4 v) {
                : "memory");
 }
 // 8 int4 nibbles -> two words of 4 sign-extended int8: (e0,e2,e4,e6), (e1,e3,e5,e7)
+// Per byte, sign-extend a two's-complement nibble n: v = n ^ 8 lies in [0, 15]; v + 0x78 never
+// carries out of its byte, and flipping bit 7 of it gives v - 8 = n as an int8.  3-4 ALU ops
+// per 4 bytes (the SIMD __vsub4 is emulated with ~10).
 __device__ __forceinline__ void unpack8(uint32_t w, uint32_t &lo, uint32_t &hi) {
-  lo = __vsub4((w & 0x0F0F0F0Fu) ^ 0x08080808u, 0x08080808u);
-  hi = __vsub4(((w >> 4) & 0x0F0F0F0Fu) ^ 0x08080808u, 0x08080808u);
+  lo = (((w & 0x0F0F0F0Fu) ^ 0x08080808u) + 0x78787878u) ^ 0x80808080u;
+  hi = ((((w >> 4) & 0x0F0F0F0Fu) ^ 0x08080808u) + 0x78787878u) ^ 0x80808080u;
 }
-// Unpack one 64-byte packed row (128 int4) into a 128-byte int8 row, SW128 layout.
-__device__ __forceinline__ void unpack_row(const uint8_t *src, uint8_t *dst_row, int row) {
+// Unpack 16-byte packed chunks (32 int4 of one row each) into the two 16-byte int8 chunks
+// 2c, 2c + 1 of the row's 128-byte SW128 line.  A warp takes 8 rows x 4 chunks per load: the
+// loads are 512 contiguous bytes and the stores hit each 16-byte bank group 4 times (optimal).
+// All NCH loads are issued before any store so their latencies overlap.
+template <int NCH, int STRIDE>
+__device__ __forceinline__ void unpack_chunks(const uint8_t *src_tile, uint8_t *dst_tile, int q0) {
+  uint4 v[NCH];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {                      // 16 packed bytes -> two 16-byte chunks
-    const uint4 v = lds128(src + c * 16);
+  for (int i = 0; i < NCH; ++i) v[i] = lds128(src_tile + (q0 + i * STRIDE) * 16);   // explicit .shared
+#pragma unroll
+  for (int i = 0; i < NCH; ++i) {
+    const int q = q0 + i * STRIDE;
+    const int row = q >> 2, c = q & 3;
     uint4 o0, o1;
-    unpack8(v.x, o0.x, o0.y);
-    unpack8(v.y, o0.z, o0.w);
-    unpack8(v.z, o1.x, o1.y);
-    unpack8(v.w, o1.z, o1.w);
+    unpack8(v[i].x, o0.x, o0.y);
+    unpack8(v[i].y, o0.z, o0.w);
+    unpack8(v[i].z, o1.x, o1.y);
+    unpack8(v[i].w, o1.z, o1.w);
+    uint8_t *dst_row = dst_tile + row * 128;
     sts128(dst_row + (((2 * c) ^ (row & 7)) * 16), o0);
     sts128(dst_row + (((2 * c + 1) ^ (row & 7)) * 16), o1);
   }
@@ -95,6 +170,7 @@ __device__ __forceinline__ float load_bias(const void *b, int dt, int64_t i) {
   return static_cast<const float *>(b)[i];
 }
 
+template <bool kDbg>
 __global__ void __launch_bounds__(kThreads, 1)
     k2_int4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmL,
@@ -107,19 +183,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *p_empty = p_full + kPStages;        // [kPStages]
   uint64_t *u_full = p_empty + kPStages;        // [kUStages]
   uint64_t *u_empty = u_full + kUStages;        // [kUStages]
-  uint64_t *g_full = u_empty + kUStages;        // [2]
-  uint64_t *g_empty = g_full + 2;               // [2]
-  uint64_t *slab_full = g_empty + 2;
+  uint64_t *g_full = u_empty + kUStages;        // [kAcc]
+  uint64_t *g_empty = g_full + kAcc;            // [kAcc]
+  uint64_t *slab_full = g_empty + kAcc;
   uint64_t *slab_empty = slab_full + 1;
-  uint64_t *lr_full = slab_empty + 1;
-  uint64_t *lr_empty = lr_full + 1;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(lr_empty + 1);
-  float *sw_s = reinterpret_cast<float *>(smem + OFF_SW);       // [2][BN]
-  float *bias_s = sw_s + 2 * BN;                                 // [BN]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(slab_empty + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const bool dbg = p.dbg_acc != nullptr;
+  constexpr bool dbg = kDbg;                           // debug: store the int32 group sums
   const int G = static_cast<int>(p.K / 64);            // K groups
   const int nst = (G + 1) / 2;                          // pipeline steps (2 groups each)
   const int nslab = dbg ? 0 : (p.rank + 63) / 64;
@@ -129,20 +201,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kPStages; ++s) {
       mbar_init(&p_full[s], 1);
-      mbar_init(&p_empty[s], 4);
+      mbar_init(&p_empty[s], kUnpackWarps);
     }
     for (int s = 0; s < kUStages; ++s) {
-      mbar_init(&u_full[s], 4);
+      mbar_init(&u_full[s], kUnpackWarps);
       mbar_init(&u_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kAcc; ++b) {
       mbar_init(&g_full[b], 1);
       mbar_init(&g_empty[b], kEpiWarps);
     }
     mbar_init(slab_full, 1);
     mbar_init(slab_empty, 1);
-    mbar_init(lr_full, 1);
-    mbar_init(lr_empty, kEpiWarps);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -187,11 +257,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idesc_h = idesc_bf16(BM, BN);
     int us = 0;
     uint32_t uph = 0;
-    int gi = 0;        // global group counter -> int32 buffer gi & 1
+    int gi = 0;        // global ring counter -> TMEM slot gi % kAcc
     int it = 0;
+#ifdef SVDQ_TRACE
+    long long t_uf = 0, t_ge = 0;
+    const long long t_st = clock64();
+#endif
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       if (nslab) {
-        mbar_wait(lr_empty, (it & 1) ^ 1);
+        const int b = gi % kAcc;
+        mbar_wait_spin(&g_empty[b], ((gi / kAcc) & 1) ^ 1);
         mbar_wait(slab_full, it & 1);
         tc_fence_after();
         if (elect_one()) {
@@ -200,27 +275,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t la = xa + BM * 128;
             const int nk16 = min(4, (p.rank - j * 64) / 16);
             for (int i = 0; i < nk16; ++i)
-              mma_bf16(tmem + TM_LR, sdesc_kmajor_sw128(xa + 32 * i), sdesc_kmajor_sw128(la + 32 * i),
+              mma_bf16(tmem + b * BN, sdesc_kmajor_sw128(xa + 32 * i), sdesc_kmajor_sw128(la + 32 * i),
                        idesc_h, (j | i) != 0);
           }
           tc_commit(slab_empty);
-          tc_commit(lr_full);
+          tc_commit(&g_full[b]);
         }
         __syncwarp();
+        ++gi;
       }
       for (int k = 0; k < nst; ++k) {
-        mbar_wait(&u_full[us], uph);
+        { I4T_BEGIN(); mbar_wait(&u_full[us], uph); I4T_ACC(t_uf); }
         tc_fence_after();
         const uint32_t ua = smem_u32(smem + OFF_U + us * (UA + UB));
         const uint32_t ub = ua + UA;
         const int ng = min(2, G - 2 * k);
         for (int j = 0; j < ng; ++j, ++gi) {
-          const int b = gi & 1;
-          mbar_wait(&g_empty[b], ((gi >> 1) & 1) ^ 1);
+          const int b = gi % kAcc;
+          { I4T_BEGIN(); mbar_wait_spin(&g_empty[b], ((gi / kAcc) & 1) ^ 1); I4T_ACC(t_ge); }
           tc_fence_after();
           if (elect_one()) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < ((SVDQ_I4EXP & 8) ? 0 : 2); ++h)
               mma_s8(tmem + b * BN, sdesc_kmajor_sw128(ua + 64 * j + 32 * h),
                      sdesc_kmajor_sw128(ub + 64 * j + 32 * h), idesc_i, h);
             tc_commit(&g_full[b]);
@@ -232,19 +308,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++us == kUStages) { us = 0; uph ^= 1; }
       }
     }
-  } else if (warp < 6) {
+#ifdef SVDQ_TRACE
+    if (lane == 0 && blockIdx.x < 148) {
+      g_i4_trace[blockIdx.x][0] = t_uf; g_i4_trace[blockIdx.x][1] = t_ge; g_i4_trace[blockIdx.x][2] = clock64() - t_st;
+    }
+#endif
+  } else if (warp < 2 + kUnpackWarps) {
     // ---------------------------------------------------------------- unpackers
-    const int ut = threadIdx.x - 64;         // 0..127: one A row and one B row
+    const int ut0 = threadIdx.x - 64;        // 16-byte packed chunk q = ut0 + 64 i of A and of B
     int ps = 0, us = 0;
     uint32_t pph = 0, uph = 0;
+#ifdef SVDQ_TRACE
+    long long t_pf = 0, t_ue = 0;
+    const long long t_st = clock64();
+#endif
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       for (int k = 0; k < nst; ++k) {
-        mbar_wait(&p_full[ps], pph);
-        mbar_wait(&u_empty[us], uph ^ 1);
+        { I4T_BEGIN(); mbar_wait(&p_full[ps], pph); I4T_ACC(t_pf); }
+        { I4T_BEGIN(); mbar_wait(&u_empty[us], uph ^ 1); I4T_ACC(t_ue); }
         const uint8_t *src = smem + OFF_P + ps * (PA + PB);
         uint8_t *dst = smem + OFF_U + us * (UA + UB);
-        unpack_row(src + ut * 64, dst + ut * 128, ut);
-        unpack_row(src + PA + ut * 64, dst + UA + ut * 128, ut);
+        if (!(SVDQ_I4EXP & 4)) {
+          constexpr int NCH = BM * 4 / (32 * kUnpackWarps);     // chunks per thread per operand
+          unpack_chunks<NCH, 32 * kUnpackWarps>(src, dst, ut0);
+          unpack_chunks<NCH, 32 * kUnpackWarps>(src + PA, dst + UA, ut0);
+        }
         fence_proxy_async();                  // generic-proxy smem writes -> tensor core
         __syncwarp();
         if (lane == 0) {
@@ -255,86 +343,154 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++us == kUStages) { us = 0; uph ^= 1; }
       }
     }
+#ifdef SVDQ_TRACE
+    if (threadIdx.x == 64 && blockIdx.x < 148) {
+      g_i4_trace[blockIdx.x][3] = t_pf; g_i4_trace[blockIdx.x][4] = t_ue; g_i4_trace[blockIdx.x][5] = clock64() - t_st;
+    }
+#endif
   } else {
     // ---------------------------------------------------------------- epilogue
-    const int quad = warp & 3;
-    const int half = (warp - 6) >> 2;          // column half of the tile
+    const int ew = warp - 2 - kUnpackWarps;     // 0..15
+    const int quad = warp & 3;                  // TMEM lane quadrant this warp may access
+    const int slice = ew >> 2;                  // 32-column slice of the tile
     const int row = quad * 32 + lane;
-    const int et = threadIdx.x - 192;         // 0..255
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const bool sbf = p.scale_bf16 != 0;
     const uint16_t *sx = reinterpret_cast<const uint16_t *>(p.sfa);
     const uint16_t *sw = reinterpret_cast<const uint16_t *>(p.sfb);
+    float *swst = reinterpret_cast<float *>(smem + OFF_SW + ew * SWST);   // [2][kGB][EC]
+    float *bst = swst + 2 * kGB * EC;                                     // [EC]
+    const int nblk = (G + kGB - 1) / kGB;
+    const uint64_t magic2 = f2pack(-12582912.0f, -12582912.0f);
     int gi = 0;
     int it = 0;
+#ifdef SVDQ_TRACE
+    long long t_gf = 0;
+    const long long t_st = clock64();
+#endif
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const int64_t m0 = static_cast<int64_t>(t % mt_count) * BM;
       const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
-      const int64_t c0 = n0 + half * EC;        // first global column of this warp
+      const int64_t c0 = n0 + slice * EC;       // first global column of this warp
       const int64_t grow = m0 + row;
       const bool rvalid = grow < p.M;
-      float facc[EC];
+      const bool cvalid = c0 + lane < p.N;      // this lane's column for the sw / bias fetch
+      uint64_t facc[EC / 2];
 #pragma unroll
-      for (int c = 0; c < EC; ++c) facc[c] = 0.f;
-      if (!dbg) {
-        named_bar(1, 32 * kEpiWarps);
-        if (et < BN) bias_s[et] = (p.bias && n0 + et < p.N) ? load_bias(p.bias, p.bias_dtype, n0 + et) : 0.f;
-      }
-      for (int g = 0; g < G; ++g, ++gi) {
-        const int b = gi & 1;
-        float sxv = 0.f;
-        if (!dbg) {
-          // stage sw[n0 .. n0+BN)[g] (slot g & 1; the barrier also retires slot reuse)
-          if (et < BN) sw_s[(g & 1) * BN + et] = n0 + et < p.N ? load16(sw, (n0 + et) * G + g, sbf) : 0.f;
-          sxv = rvalid ? load16(sx, grow * G + g, sbf) : 0.f;
-          named_bar(1, 32 * kEpiWarps);
+      for (int c = 0; c < EC / 2; ++c) facc[c] = 0ull;
+      // scales of block 0 (raw 16-bit pairs in registers), then each block prefetches the next
+      uint32_t sxn[kGB / 2], swn[kGB / 2];
+      const bool vec = (G % kGB) == 0;          // 16-byte aligned rows of 8 scales
+      auto fetch = [&](int blk) {
+        if (vec && !(SVDQ_I4EXP & 1)) {
+          const uint4 xv = (!dbg && rvalid) ? *reinterpret_cast<const uint4 *>(sx + grow * G + blk * kGB)
+                                            : make_uint4(0, 0, 0, 0);
+          const uint4 wv = (!dbg && cvalid) ? *reinterpret_cast<const uint4 *>(sw + (c0 + lane) * G + blk * kGB)
+                                            : make_uint4(0, 0, 0, 0);
+          sxn[0] = xv.x; sxn[1] = xv.y; sxn[2] = xv.z; sxn[3] = xv.w;
+          swn[0] = wv.x; swn[1] = wv.y; swn[2] = wv.z; swn[3] = wv.w;
+          return;
         }
-        mbar_wait(&g_full[b], (gi >> 1) & 1);
+#pragma unroll
+        for (int j = 0; j < kGB / 2; ++j) {
+          const int g = blk * kGB + 2 * j;
+          if (SVDQ_I4EXP & 1) { sxn[j] = 0x3C003C00u; swn[j] = 0x3C003C00u; continue; }
+          const uint32_t x0 = (!dbg && rvalid && g < G) ? sx[grow * G + g] : 0u;
+          const uint32_t x1 = (!dbg && rvalid && g + 1 < G) ? sx[grow * G + g + 1] : 0u;
+          const uint32_t w0 = (!dbg && cvalid && g < G) ? sw[(c0 + lane) * G + g] : 0u;
+          const uint32_t w1 = (!dbg && cvalid && g + 1 < G) ? sw[(c0 + lane) * G + g + 1] : 0u;
+          sxn[j] = x0 | (x1 << 16);
+          swn[j] = w0 | (w1 << 16);
+        }
+      };
+      auto h2f = [&](uint32_t bits16) {
+        return sbf ? __uint_as_float(bits16 << 16) : __half2float(__ushort_as_half(static_cast<uint16_t>(bits16)));
+      };
+      fetch(0);
+      sts_f32(smem_u32(bst) + lane * 4, (!dbg && p.bias && cvalid) ? load_bias(p.bias, p.bias_dtype, c0 + lane) : 0.f);
+      if (nslab) {                               // low-rank pseudo-group: facc starts at X L1 . L2
+        const int b = gi % kAcc;
+        mbar_wait(&g_full[b], (gi / kAcc) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int cc = 0; cc < EC / 16; ++cc) {
+        for (int hh = 0; hh < 2; ++hh) {
           uint32_t r[16];
-          tmem_ld_32x32b_x16(tmem + b * BN + lane_off + half * EC + cc * 16, r);
+          tmem_ld_32x32b_x16(tmem + b * BN + lane_off + slice * EC + hh * 16, r);
           tmem_ld_wait();
-          if (dbg) {
-            if (rvalid) {
-              int32_t *dst = p.dbg_acc + (static_cast<int64_t>(g) * p.M + grow) * p.N + c0 + cc * 16;
 #pragma unroll
-              for (int j = 0; j < 16; j += 4)
-                if (c0 + cc * 16 + j < p.N)
-                  *reinterpret_cast<int4 *>(dst + j) =
-                      make_int4((int)r[j], (int)r[j + 1], (int)r[j + 2], (int)r[j + 3]);
-            }
-          } else {
-            const float *swg = sw_s + (g & 1) * BN + half * EC + cc * 16;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              // exact int32 -> fp32 (|acc| <= 64*49 < 2^22): magic-number add / subtract
-              const float a = __int_as_float(static_cast<int>(r[j]) + 0x4B400000) - 12582912.0f;
-              facc[cc * 16 + j] = fmaf(__fmul_rn(a, sxv), swg[j], facc[cc * 16 + j]);
-            }
-          }
+          for (int c = 0; c < 8; ++c) facc[hh * 8 + c] = f2pack(__uint_as_float(r[2 * c]), __uint_as_float(r[2 * c + 1]));
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&g_empty[b]);
+        ++gi;
+      }
+      const uint32_t swb = smem_u32(swst);       // [g][column] sw, then [g][lane] sx
+      const uint32_t sxb = swb + kGB * EC * 4;
+      for (int blk = 0; blk < nblk; ++blk) {
+        __syncwarp();                            // previous block's reads are done
+#pragma unroll
+        for (int j = 0; j < kGB / 2; ++j) {
+          sts_f32(swb + ((2 * j) * EC + lane) * 4, h2f(swn[j] & 0xFFFFu));    // broadcast reads below
+          sts_f32(swb + ((2 * j + 1) * EC + lane) * 4, h2f(swn[j] >> 16));
+          sts_f32(sxb + ((2 * j) * EC + lane) * 4, h2f(sxn[j] & 0xFFFFu));
+          sts_f32(sxb + ((2 * j + 1) * EC + lane) * 4, h2f(sxn[j] >> 16));
+        }
+        __syncwarp();
+        if (blk + 1 < nblk) fetch(blk + 1);      // in flight while this block is promoted
+#pragma unroll
+        for (int j = 0; j < kGB; ++j) {
+          const int g = blk * kGB + j;
+          if (g >= G) break;
+          const int b = gi % kAcc;
+          { I4T_BEGIN(); mbar_wait_spin(&g_full[b], (gi / kAcc) & 1); I4T_ACC(t_gf); }
+          tc_fence_after();
+          const float sxv = lds_f32(sxb + (j * EC + lane) * 4);
+          const uint64_t sx2 = f2pack(sxv, sxv);
+          const uint32_t swg = swb + j * EC * 4;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {               // two 16-column halves: 16 live registers
+            uint32_t r[16];
+            tmem_ld_32x32b_x16(tmem + b * BN + lane_off + slice * EC + hh * 16, r);
+            tmem_ld_wait();
+            if (hh == 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&g_empty[b]);   // the int32 buffer is free again
+            }
+            if (SVDQ_I4EXP & 2) {
+              facc[hh * 8] = add2(facc[hh * 8], f2pack(__uint_as_float(r[0]), __uint_as_float(r[15])));
+              continue;
+            }
+            if (dbg) {
+              if (rvalid) {
+                int32_t *dst = p.dbg_acc + (static_cast<int64_t>(g) * p.M + grow) * p.N + c0 + hh * 16;
+#pragma unroll
+                for (int q = 0; q < 16; q += 4)
+                  if (c0 + hh * 16 + q < p.N)
+                    *reinterpret_cast<int4 *>(dst + q) = make_int4((int)r[q], (int)r[q + 1], (int)r[q + 2], (int)r[q + 3]);
+              }
+              continue;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 w4 = lds_f32x4(swg + (hh * 16 + 4 * q) * 4);
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int e = 4 * q + 2 * h;
+                // exact int32 -> fp32 (|acc| <= 64*49 < 2^22): magic-number add, then subtract
+                const uint64_t a2 = add2(f2pack(__int_as_float(static_cast<int>(r[e]) + 0x4B400000),
+                                                __int_as_float(static_cast<int>(r[e + 1]) + 0x4B400000)), magic2);
+                const uint64_t t2 = mul2(a2, sx2);                       // fl32(acc * sx)
+                const int fi = hh * 8 + e / 2;
+                facc[fi] = fma2(t2, h ? f2pack(w4.z, w4.w) : f2pack(w4.x, w4.y), facc[fi]);   // + . * sw
+              }
+            }
+          }
+          ++gi;
+        }
       }
       if (dbg) continue;
-      if (nslab) {
-        mbar_wait(lr_full, it & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int cc = 0; cc < EC / 32; ++cc) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(tmem + TM_LR + lane_off + half * EC + cc * 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) facc[cc * 32 + j] += __uint_as_float(r[j]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(lr_empty);
-      }
       if (rvalid) {
 #pragma unroll
         for (int c8 = 0; c8 < EC / 8; ++c8) {
@@ -342,7 +498,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (col < p.N) {
             float v[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) v[e] = __fadd_rn(facc[c8 * 8 + e], bias_s[half * EC + c8 * 8 + e]);
+            for (int e = 0; e < 8; ++e) {
+              const uint64_t f = facc[c8 * 4 + e / 2];
+              v[e] = __fadd_rn(__uint_as_float(static_cast<uint32_t>((e & 1) ? (f >> 32) : f)),
+                               lds_f32(smem_u32(bst) + (c8 * 8 + e) * 4));
+            }
             if (p.y_dtype == 2) {
               float4 *q = reinterpret_cast<float4 *>(static_cast<float *>(p.Y) + grow * p.ldy + col);
               q[0] = make_float4(v[0], v[1], v[2], v[3]);
@@ -364,7 +524,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      __syncwarp();                              // bst / swst reuse by the next tile
     }
+#ifdef SVDQ_TRACE
+    if (ew == 0 && lane == 0 && blockIdx.x < 148) {
+      g_i4_trace[blockIdx.x][6] = t_gf; g_i4_trace[blockIdx.x][7] = clock64() - t_st;
+    }
+#endif
   }
   tc_fence_before();
   __syncthreads();
@@ -374,7 +540,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace
 
 cudaError_t launch_k2_int4(const K2Maps &maps, const K2Params &p, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(k2_int4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  auto kern = p.dbg_acc ? k2_int4_kernel<true> : k2_int4_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   if (e != cudaSuccess) return e;
   if (p.rank > kMaxSlabs * 64 && !p.dbg_acc) return cudaErrorInvalidValue;
   static int num_sms = 0;
@@ -385,7 +552,7 @@ cudaError_t launch_k2_int4(const K2Maps &maps, const K2Params &p, cudaStream_t s
   }
   const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
   const unsigned grid = static_cast<unsigned>(tiles < num_sms ? tiles : num_sms);
-  return launch_ex(k2_int4_kernel, dim3(grid), dim3(kThreads), SMEM, s, 1u, maps.a, maps.b, maps.xl1, maps.l2, p);
+  return launch_ex(kern, dim3(grid), dim3(kThreads), SMEM, s, 1u, maps.a, maps.b, maps.xl1, maps.l2, p);
 }
 
 }  // namespace svdq

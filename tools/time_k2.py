@@ -7,10 +7,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2411_05007_b200 as P
 M, K, N = (int(a) for a in sys.argv[1:4])
 dev = torch.device("cuda")
-layer = P.QuantizedLinear.empty("nvfp4", K, N, 32, device=dev)
+fmt = os.environ.get("SVDQ_FMT", "nvfp4")
+layer = P.QuantizedLinear.empty(fmt, K, N, 32, device=dev)
 g = torch.Generator(device=dev).manual_seed(0)
 layer.w_codes.random_(0, 256, generator=g)
-layer.w_scales.fill_(0x30)
+layer.w_scales.fill_(0x30 if fmt == "nvfp4" else 0x3c)
 layer.l1s.zero_(); layer.l2s.zero_(); layer.lambda_inv.fill_(1.0)
 layer.gs_w = 1.0
 layer._sync_view()
@@ -34,4 +35,4 @@ with torch.cuda.stream(s):
     b.record(s)
 torch.cuda.synchronize()
 us = a.elapsed_time(b) / 20 * 1e3
-print(f"M={M} K={K} N={N} pair={os.environ.get('SVDQ_K2_PAIR', '1')} lib={os.path.basename(os.environ.get('SVDQ_LIB', 'libsvdq.so'))}: {us:.2f} us  {2*M*N*K/us/1e6:.1f} TFLOP/s")
+print(f"{fmt} M={M} K={K} N={N} pair={os.environ.get('SVDQ_K2_PAIR', '1')} lib={os.path.basename(os.environ.get('SVDQ_LIB', 'libsvdq.so'))}: {us:.2f} us  {2*M*N*K/us/1e6:.1f} TFLOP/s")
