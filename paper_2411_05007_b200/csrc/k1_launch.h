@@ -8,8 +8,8 @@ namespace svdq {
 
 // Launch with programmatic stream serialization (PDL) and an optional cluster size.
 template <typename Kern, typename... Args>
-inline cudaError_t launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, unsigned cluster_x,
-                             Args... args) {
+inline cudaError_t launch_ex_impl(bool force_cluster, Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                  unsigned cluster_x, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -20,7 +20,7 @@ inline cudaError_t launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cuda
   attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[n].val.programmaticStreamSerializationAllowed = 1;
   ++n;
-  if (cluster_x > 1) {
+  if (cluster_x > 1 || force_cluster) {     // kernels using cluster instructions need the attribute
     attr[n].id = cudaLaunchAttributeClusterDimension;
     attr[n].val.clusterDim.x = cluster_x;
     attr[n].val.clusterDim.y = 1;
@@ -30,6 +30,18 @@ inline cudaError_t launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cuda
   cfg.attrs = attr;
   cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <typename Kern, typename... Args>
+inline cudaError_t launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, unsigned cluster_x,
+                             Args... args) {
+  return launch_ex_impl(false, kern, grid, block, smem, s, cluster_x, args...);
+}
+// Always launched as clusters of `cluster_x` CTAs (also when cluster_x == 1).
+template <typename Kern, typename... Args>
+inline cudaError_t launch_ex_cluster(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                     unsigned cluster_x, Args... args) {
+  return launch_ex_impl(true, kern, grid, block, smem, s, cluster_x, args...);
 }
 
 struct K1Params {

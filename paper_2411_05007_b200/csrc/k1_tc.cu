@@ -98,8 +98,8 @@ struct K1Layout {
 __host__ __device__ inline K1Layout k1_layout(int rank) {
   K1Layout L;
   L.stage_bytes = ((16384 + rank * 128 + 256) + 1023) / 1024 * 1024;
-  L.red_stride = rank + 2;                       // padded row stride (floats, even: float2 reads)
-  const size_t red = rank ? static_cast<size_t>(128) * L.red_stride * 4 : 0;
+  L.red_stride = rank;                           // receive buffer [src rank][owned row][rank] fp32
+  const size_t red = rank ? static_cast<size_t>(136) * rank * 4 : 0;   // ks * ceil(128 / ks) <= 135 rows
   int s = static_cast<int>((205 * 1024 - red) / L.stage_bytes);
   L.stages = s > 12 ? 12 : (s < 2 ? 2 : s);
   L.red_off = static_cast<size_t>(L.stages) * L.stage_bytes;
@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + Ly.bar_off);
   uint64_t *empty = full + 12;
   uint64_t *dfull = empty + 12;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dfull + 1);
+  uint64_t *recv_full = dfull + 1;                // partial xl1 slices pushed by the cluster
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(recv_full + 1);
   float *qinv_lut = reinterpret_cast<float *>(smem + Ly.bar_off + 256);
 
   const int warp = threadIdx.x >> 5;
@@ -153,8 +154,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[s], kQuantWarps + (r ? 1 : 0));
     }
     mbar_init(dfull, 1);
+    mbar_init(recv_full, 1);
     fence_mbar_init();
   }
+  // rows of the 128-row tile whose xl1 this CTA reduces and stores: [rows_lo, rows_hi)
+  const int rows_lo = crank * 128 / ks;
+  const int rows_hi = (crank + 1) * 128 / ks;
+  const int own_max = (128 + ks - 1) / ks;       // receive-slot stride (rows) per source CTA
+  if (r && threadIdx.x == 0)                     // every CTA of the cluster (self included) pushes its slice
+    mbar_arrive_expect_tx(recv_full, static_cast<uint32_t>(ks * (rows_hi - rows_lo) * r * 4));
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmX);
     if (r) tma_prefetch(&tmL);
@@ -169,6 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (r) cluster_arrive();                          // barriers initialised: peers may push later
   const uint32_t tmem = r ? *tmem_slot : 0;
   if (threadIdx.x == 0) TRACE(1);
   griddep_launch_dependents();                       // next kernel may start its prologue
@@ -342,55 +351,60 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
   if (r == 0) return;
   // -------------------------------------------------------------------- xl1 reduction
+  // Push, not pull: each TMEM lane (= tile row) sends its partial xl1 row straight into the
+  // receive buffer of the CTA that owns the row (st.async, counted on that CTA's recv_full);
+  // the owner sums the ks slices in fixed source-rank order (deterministic), rounds to bf16
+  // and stores.  No CTA waits for a peer except for the bytes it needs.
+  cluster_wait();                                    // every peer's barrier is initialised
   if (warp >= 2 && warp < 6) {
     const int quad = warp & 3;
     const int rl = quad * 32 + lane;
+    int owner = 0;
+    while (owner + 1 < ks && (owner + 1) * 128 / ks <= rl) ++owner;
+    const int lr = rl - owner * 128 / ks;
+    const uint32_t dst = mapa_u32(red, static_cast<uint32_t>(owner)) +
+                         static_cast<uint32_t>(((crank * own_max) + lr) * r * 4);
+    const uint32_t bar = mapa_u32(recv_full, static_cast<uint32_t>(owner));
     mbar_wait_spin(dfull, 0);
     tc_fence_after();
     for (int c16 = 0; c16 < r / 16; ++c16) {
+      uint32_t v[4][16];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(quad * 32) << 16) + a * r + c16 * 16, v[a]);
+      tmem_ld_wait();
       float acc[16];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {                   // fixed accumulator order: deterministic
-        uint32_t v[16];
-        tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(quad * 32) << 16) + a * r + c16 * 16, v);
-        tmem_ld_wait();
+      for (int j = 0; j < 16; ++j)                   // fixed accumulator order: deterministic
+        acc[j] = ((__uint_as_float(v[0][j]) + __uint_as_float(v[1][j])) + __uint_as_float(v[2][j])) +
+                 __uint_as_float(v[3][j]);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] = a == 0 ? __uint_as_float(v[j]) : acc[j] + __uint_as_float(v[j]);
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) red[rl * Ly.red_stride + c16 * 16 + j] = acc[j];
+      for (int q = 0; q < 4; ++q)
+        st_async_v4(dst + (c16 * 16 + 4 * q) * 4, acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3], bar);
     }
   }
   tc_fence_before();
-  if (threadIdx.x == 64) TRACE(195);                      // TMEM drained
-  cluster_sync();                                    // every partial tile is in smem
+  if (threadIdx.x == 64) TRACE(195);                      // TMEM drained, slices pushed
+  __syncthreads();
+  if (warp == 1) tmem_dealloc_n(tmem, tcols);
+  mbar_wait(recv_full, 0);                               // all ks slices of my rows arrived
   if (threadIdx.x == 64) TRACE(196);
   {
-    const int rows_lo = crank * 128 / ks;
-    const int rows_hi = (crank + 1) * 128 / ks;
     const int pairs = (rows_hi - rows_lo) * (r / 2);
     for (int idx = threadIdx.x; idx < pairs; idx += kThreads) {
-      const int rl = rows_lo + idx / (r / 2);
+      const int lr = idx / (r / 2);
       const int col = 2 * (idx % (r / 2));
-      const float *src = red + rl * Ly.red_stride + col;
-      float2 v[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j)                    // all remote loads in flight at once
-        v[j] = j < ks ? ld_dsmem_f32x2(src, static_cast<uint32_t>(j)) : make_float2(0.f, 0.f);
       float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {                  // fixed rank order: deterministic
-        s0 += v[j].x;
-        s1 += v[j].y;
+      for (int j = 0; j < ks; ++j) {                 // fixed source order: deterministic
+        const float2 v = *reinterpret_cast<const float2 *>(red + (j * own_max + lr) * r + col);
+        s0 += v.x;
+        s1 += v.y;
       }
-      const int64_t row = row0 + rl;
+      const int64_t row = row0 + rows_lo + lr;
       if (row < p.M) *reinterpret_cast<uint32_t *>(p.xl1 + row * r + col) = pack_bf16x2(s0, s1);
     }
   }
   if (threadIdx.x == 64) TRACE(197);
-  cluster_sync();                                    // peers finished reading my smem
-  if (threadIdx.x == 64) TRACE(198);
-  if (warp == 1) tmem_dealloc_n(tmem, tcols);
 }
 
 // Largest K split (cluster size) whose whole grid is co-resident in one wave: clusters of
@@ -436,7 +450,7 @@ cudaError_t launch_t(const K1Maps &maps, const K1Params &p, int /*ks_hint*/, cud
   if (e != cudaSuccess) return e;
   int ks = choose_ksplit(kern, Ly, p.Mpad / 128, p.K / 64);
   if (const char *e = getenv("SVDQ_K1_KS")) ks = atoi(e);     // ablation override (debug)
-  return launch_ex(kern, dim3(static_cast<unsigned>(ks), static_cast<unsigned>(p.Mpad / 128), 1),
+  return launch_ex_cluster(kern, dim3(static_cast<unsigned>(ks), static_cast<unsigned>(p.Mpad / 128), 1),
                    dim3(kThreads, 1, 1), Ly.smem, s, static_cast<unsigned>(ks), maps.x, maps.l1s, maps.lam, p, ks);
 }
 

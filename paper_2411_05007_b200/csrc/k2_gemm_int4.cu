@@ -479,6 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int h = 0; h < 2; ++h) {
                 const int e = 4 * q + 2 * h;
                 // exact int32 -> fp32 (|acc| <= 64*49 < 2^22): magic-number add, then subtract
+                // (measured: I2FP.F32.S32 is ~4 % slower than this magic-number conversion)
                 const uint64_t a2 = add2(f2pack(__int_as_float(static_cast<int>(r[e]) + 0x4B400000),
                                                 __int_as_float(static_cast<int>(r[e + 1]) + 0x4B400000)), magic2);
                 const uint64_t t2 = mul2(a2, sx2);                       // fl32(acc * sx)

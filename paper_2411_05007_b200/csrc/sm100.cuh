@@ -228,6 +228,23 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Split cluster barrier: arrive early, wait only where remote shared memory is first touched.
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 16-byte asynchronous store into (possibly remote) shared memory of this cluster; the bytes
+// are counted on the mbarrier at `bar_cluster_addr` (in the destination CTA).
+__device__ __forceinline__ void st_async_v4(uint32_t dst_cluster_addr, float a, float b, float c, float d,
+                                            uint32_t bar_cluster_addr) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+          dst_cluster_addr),
+      "f"(a), "f"(b), "f"(c), "f"(d), "r"(bar_cluster_addr)
+      : "memory");
+}
 // Load a float from the shared memory of CTA `rank` of this cluster (same offset as `p`).
 __device__ __forceinline__ float ld_dsmem_f32(const float *p, uint32_t rank) {
   uint32_t remote;
