@@ -121,6 +121,18 @@ svdq_status svdq_gemm_w4a4_lowrank_up(const svdq_linear *L, const uint8_t *xq, c
                                       const uint16_t *xl1, int64_t M, void *Y, int32_t y_dtype,
                                       int64_t ldy, void *stream);
 
+/* Grouped K2: n (1..4) independent NVFP4 problems in ONE persistent launch (e.g. the image-
+ * and text-stream linears of a FLUX double block, which share no data).  Problem i is exactly
+ * svdq_gemm_w4a4_lowrank_up(layers[i], xq[i], xs[i], xl1[i], M[i], Y[i], y_dtype, ldy[i]) and
+ * produces bit-identical Y; all problems run on the CTA-pair kernel, whose CTA pairs walk the
+ * concatenated tile lists (one tail instead of n).  Arrays are [host], n entries each;
+ * pointers inside follow svdq_gemm_w4a4_lowrank_up.  SVDQ_ERR_UNSUPPORTED for INT4 layers;
+ * SVDQ_ERR_INVALID_ARGUMENT for n outside 1..4 or NULL arrays.                      */
+svdq_status svdq_gemm_w4a4_lowrank_up_grouped(int32_t n, const svdq_linear *const *layers,
+                                              const uint8_t *const *xq, const uint8_t *const *xs,
+                                              const uint16_t *const *xl1, const int64_t *M, void *const *Y,
+                                              int32_t y_dtype, const int64_t *ldy, void *stream);
+
 /* Convenience: K1 then K2 on one stream.  ws: [dev] >= xq+xs+xl1 bytes (16-B aligned parts). */
 svdq_status svdq_linear_forward(const svdq_linear *L, const void *X, int32_t x_dtype, int64_t M,
                                 int64_t ldx, void *Y, int32_t y_dtype, int64_t ldy, void *ws,

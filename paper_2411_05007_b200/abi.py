@@ -36,7 +36,8 @@ DTYPE_OF_TORCH = {torch.bfloat16: "bf16", torch.float16: "fp16", torch.float32: 
 # Every symbol include/svdq.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "svdq_act_buffer_sizes", "svdq_weight_buffer_sizes", "svdq_quantize_act_lowrank_down",
-    "svdq_gemm_w4a4_lowrank_up", "svdq_linear_forward", "svdq_quantize_residual",
+    "svdq_gemm_w4a4_lowrank_up", "svdq_gemm_w4a4_lowrank_up_grouped", "svdq_linear_forward",
+    "svdq_quantize_residual",
     "svdq_quantize_weights_workspace", "svdq_quantize_weights", "svdq_lora_fuse",
     "svdq_debug_int4_group_accum", "svdq_debug_codec", "svdq_status_string", "svdq_last_error",
     "svdq_launch_count", "svdq_version",
@@ -70,6 +71,8 @@ _sig = {
     "svdq_weight_buffer_sizes": [_I32, _I64, _I64, _I32, _SZ, _SZ, _SZ, _SZ],
     "svdq_quantize_act_lowrank_down": [_LP, _P, _I32, _I64, _I64, _P, _P, _P, _P],
     "svdq_gemm_w4a4_lowrank_up": [_LP, _P, _P, _P, _I64, _P, _I32, _I64, _P],
+    "svdq_gemm_w4a4_lowrank_up_grouped": [_I32, C.POINTER(_LP), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
+                                          C.POINTER(_I64), C.POINTER(_P), _I32, C.POINTER(_I64), _P],
     "svdq_linear_forward": [_LP, _P, _I32, _I64, _I64, _P, _I32, _I64, _P, C.c_size_t, _P],
     "svdq_quantize_residual": [_P, _I64, _I64, _I32, _I32, _P, _P, C.POINTER(C.c_float), _P],
     "svdq_quantize_weights_workspace": [_I64, _I64, _I32, _SZ],
@@ -210,6 +213,22 @@ def svdq_gemm_w4a4_lowrank_up(layer: QuantizedLinear, xq, xs, xl1, M: int, Y=Non
     _check(_lib.svdq_gemm_w4a4_lowrank_up(
         layer.ref, _ptr(xq), _ptr(xs), _ptr(xl1), M, _ptr(Y), DTYPE[DTYPE_OF_TORCH[Y.dtype]],
         Y.stride(0), _stream(stream)), "svdq_gemm_w4a4_lowrank_up")
+    return Y
+
+
+def svdq_gemm_w4a4_lowrank_up_grouped(layers, xq, xs, xl1, M, Y, stream=None):
+    """Grouped K2: one launch over n (1..4) independent NVFP4 problems; lists of equal length.
+    Problem i produces exactly svdq_gemm_w4a4_lowrank_up(layers[i], xq[i], xs[i], xl1[i], M[i], Y[i])."""
+    n = len(layers)
+    ydt = {DTYPE_OF_TORCH[y.dtype] for y in Y}
+    if len(ydt) != 1:
+        raise ValueError("grouped K2: all Y must share one dtype")
+    arr = lambda T, vals: (T * n)(*vals)
+    _check(_lib.svdq_gemm_w4a4_lowrank_up_grouped(
+        n, arr(_LP, [C.pointer(l.view) for l in layers]), arr(_P, [x.data_ptr() for x in xq]),
+        arr(_P, [x.data_ptr() for x in xs]), arr(_P, [x.data_ptr() if x is not None else None for x in xl1]),
+        arr(_I64, list(M)), arr(_P, [y.data_ptr() for y in Y]), DTYPE[ydt.pop()],
+        arr(_I64, [y.stride(0) for y in Y]), _stream(stream)), "svdq_gemm_w4a4_lowrank_up_grouped")
     return Y
 
 

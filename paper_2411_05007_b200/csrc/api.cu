@@ -252,9 +252,19 @@ svdq_status svdq_quantize_act_lowrank_down(const svdq_linear *L, const void *X, 
   return SVDQ_OK;
 }
 
-svdq_status svdq_gemm_w4a4_lowrank_up(const svdq_linear *L, const uint8_t *xq, const uint8_t *xs,
-                                      const uint16_t *xl1, int64_t M, void *Y, int32_t y_dtype,
-                                      int64_t ldy, void *stream) {
+}  // extern "C"
+
+namespace {
+// Validation, launch parameters and tensor maps of one K2 problem.  `force_pair` selects the
+// CTA-pair NVFP4 kernel regardless of shape (grouped launches run every problem on it).
+struct K2Prep {
+  K2Params p;
+  K2Maps maps;
+  CUtensorMap sfa_map, sfb_map;
+  bool pair;
+};
+svdq_status prepare_k2(const svdq_linear *L, const uint8_t *xq, const uint8_t *xs, const uint16_t *xl1, int64_t M,
+                       void *Y, int32_t y_dtype, int64_t ldy, bool force_pair, K2Prep *out) {
   svdq_status st = check_linear(L, true);
   if (st != SVDQ_OK) return st;
   if (!xq || !xs || !Y || (L->rank > 0 && !xl1)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null buffer");
@@ -266,7 +276,8 @@ svdq_status svdq_gemm_w4a4_lowrank_up(const svdq_linear *L, const uint8_t *xq, c
     return fail(SVDQ_ERR_ALIGNMENT, "Y / ldy / inputs must be 16-byte aligned");
   if ((st = check_device()) != SVDQ_OK) return st;
   const int64_t K = L->K, N = L->N;
-  K2Params p{};
+  K2Params &p = out->p;
+  p = K2Params{};
   p.M = M;
   p.N = N;
   p.K = K;
@@ -283,12 +294,13 @@ svdq_status svdq_gemm_w4a4_lowrank_up(const svdq_linear *L, const uint8_t *xq, c
   p.ldy = ldy;
   p.scale_bf16 = L->scale_dtype == SVDQ_BF16;
   p.alpha = L->fmt == SVDQ_FMT_NVFP4 ? L->gs_x * L->gs_w : 1.0f;
-  K2Maps maps;
+  K2Maps &maps = out->maps;
   std::memset(&maps, 0, sizeof(maps));
-  const bool pair = L->fmt == SVDQ_FMT_NVFP4 && use_pair_kernel(M, K);
+  const bool pair = L->fmt == SVDQ_FMT_NVFP4 && (force_pair || use_pair_kernel(M, K));
+  out->pair = pair;
   const int BN = L->fmt == SVDQ_FMT_NVFP4 ? (pair ? kNvfp4PairBN : k2_nvfp4_bn(M, N)) : kInt4BN;
   const uint32_t b_rows = pair ? kNvfp4PairBN / 2 : static_cast<uint32_t>(BN);   // B rows staged per CTA
-  CUtensorMap sfa_map, sfb_map;
+  CUtensorMap &sfa_map = out->sfa_map, &sfb_map = out->sfb_map;
   if (L->fmt == SVDQ_FMT_NVFP4) {
     const CUtensorMapDataType ydt = y_dtype == SVDQ_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                     : y_dtype == SVDQ_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
@@ -314,12 +326,54 @@ svdq_status svdq_gemm_w4a4_lowrank_up(const svdq_linear *L, const uint8_t *xq, c
     if ((st = make_map(&maps.xl1, xl1, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->rank, M, L->rank * 2, 64, 128)) != SVDQ_OK) return st;
     if ((st = make_map(&maps.l2, L->l2s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->rank, N, L->rank * 2, 64, b_rows)) != SVDQ_OK) return st;
   }
+  return SVDQ_OK;
+}
+}  // namespace
+
+extern "C" {
+
+svdq_status svdq_gemm_w4a4_lowrank_up(const svdq_linear *L, const uint8_t *xq, const uint8_t *xs,
+                                      const uint16_t *xl1, int64_t M, void *Y, int32_t y_dtype,
+                                      int64_t ldy, void *stream) {
+  K2Prep k;
+  svdq_status st = prepare_k2(L, xq, xs, xl1, M, Y, y_dtype, ldy, false, &k);
+  if (st != SVDQ_OK) return st;
   cudaError_t e = L->fmt == SVDQ_FMT_NVFP4
-                      ? (pair ? launch_k2_nvfp4_2sm(maps, sfa_map, sfb_map, p, static_cast<cudaStream_t>(stream))
-                              : launch_k2_nvfp4(maps, p, static_cast<cudaStream_t>(stream)))
-                      : launch_k2_int4(maps, p, static_cast<cudaStream_t>(stream));
+                      ? (k.pair ? launch_k2_nvfp4_2sm(k.maps, k.sfa_map, k.sfb_map, k.p, static_cast<cudaStream_t>(stream))
+                                : launch_k2_nvfp4(k.maps, k.p, static_cast<cudaStream_t>(stream)))
+                      : launch_k2_int4(k.maps, k.p, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported) return fail(SVDQ_ERR_UNSUPPORTED, "INT4 GEMM not built");
   if (e != cudaSuccess) return cuda_fail(e, "K2 launch");
+  ++g_launches;
+  return SVDQ_OK;
+}
+
+svdq_status svdq_gemm_w4a4_lowrank_up_grouped(int32_t n, const svdq_linear *const *layers,
+                                              const uint8_t *const *xq, const uint8_t *const *xs,
+                                              const uint16_t *const *xl1, const int64_t *M, void *const *Y,
+                                              int32_t y_dtype, const int64_t *ldy, void *stream) {
+  if (n < 1 || n > kMaxGroup) return fail(SVDQ_ERR_INVALID_ARGUMENT, "group size must be 1..%d", kMaxGroup);
+  if (!layers || !xq || !xs || !xl1 || !M || !Y || !ldy) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null array");
+  K2PairArgs g;
+  std::memset(&g, 0, sizeof(g));
+  g.n = n;
+  for (int i = 0; i < n; ++i) {
+    if (!layers[i]) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null layer %d", i);
+    if (layers[i]->fmt != SVDQ_FMT_NVFP4) return fail(SVDQ_ERR_UNSUPPORTED, "grouped K2 is NVFP4 only");
+    K2Prep k;
+    svdq_status st = prepare_k2(layers[i], xq[i], xs[i], xl1[i], M[i], Y[i], y_dtype, ldy[i], true, &k);
+    if (st != SVDQ_OK) return st;
+    g.pr[i].a = k.maps.a;
+    g.pr[i].b = k.maps.b;
+    g.pr[i].xl1 = k.maps.xl1;
+    g.pr[i].l2 = k.maps.l2;
+    g.pr[i].sfa = k.sfa_map;
+    g.pr[i].sfb = k.sfb_map;
+    g.pr[i].y = k.maps.y;
+    g.pr[i].p = k.p;
+  }
+  cudaError_t e = launch_k2_nvfp4_2sm_group(g, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "grouped K2 launch");
   ++g_launches;
   return SVDQ_OK;
 }

@@ -90,6 +90,19 @@ int k2_nvfp4_bn(int64_t M, int64_t N);   // N tile the 1-CTA NVFP4 GEMM will use
 // 3-D uint64 views [tiles128][K/64][64] of the 128x4 scale-factor layout.
 cudaError_t launch_k2_nvfp4_2sm(const K2Maps &maps, const CUtensorMap &sfa, const CUtensorMap &sfb,
                                 const K2Params &p, cudaStream_t s);
+// Grouped form: up to kMaxGroup independent problems in one persistent launch; CTA pairs
+// walk the concatenation of the problems' tile lists.
+constexpr int kMaxGroup = 4;
+struct K2PairProblem {
+  CUtensorMap a, b, xl1, l2, sfa, sfb, y;
+  K2Params p;
+};
+struct K2PairArgs {
+  K2PairProblem pr[kMaxGroup];
+  int n;
+  int tile_begin[kMaxGroup + 1];
+};
+cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &args, cudaStream_t s);
 constexpr int kNvfp4PairBN = 192;
 constexpr int kInt4BN = 128;             // N tile of the INT4 GEMM
 cudaError_t launch_k2_int4(const K2Maps &maps, const K2Params &p, cudaStream_t s);

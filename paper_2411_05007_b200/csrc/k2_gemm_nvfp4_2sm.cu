@@ -94,11 +94,21 @@ __device__ __forceinline__ void store8(void *Y, int dt, int64_t ldy, int64_t row
   *reinterpret_cast<uint4 *>(static_cast<uint16_t *>(Y) + row * ldy + col) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// Tile t of the concatenated tile lists -> (problem, m0, n0).
+struct TileRef {
+  int i;
+  int64_t m0, n0;
+};
+__device__ __forceinline__ TileRef locate(const K2PairArgs &g, int t) {
+  int i = 0;
+  while (i + 1 < g.n && t >= g.tile_begin[i + 1]) ++i;
+  const int lt = t - g.tile_begin[i];
+  const int mt = static_cast<int>((g.pr[i].p.M + 255) / 256);
+  return TileRef{i, static_cast<int64_t>(lt % mt) * 256, static_cast<int64_t>(lt / mt) * BN};
+}
+
 __global__ void __launch_bounds__(320, 1)
-    k2_nvfp4_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmL,
-                        const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
-                        const __grid_constant__ CUtensorMap tmY, const K2Params p) {
+    k2_nvfp4_2sm_kernel(const __grid_constant__ K2PairArgs g) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~static_cast<uintptr_t>(1023));
@@ -114,12 +124,9 @@ __global__ void __launch_bounds__(320, 1)
   const uint32_t crank = cluster_ctarank();             // 0 leader, 1 peer
   const int pair = static_cast<int>(blockIdx.x >> 1);
   const int npairs = static_cast<int>(gridDim.x >> 1);
-  const int nkb64 = static_cast<int>(p.K / 64);
-  const int nkt = (nkb64 + 3) / 4;
-  const int nslab = (p.rank + 63) / 64;
-  const int mt_count = static_cast<int>((p.M + 255) / 256);
-  const int nt_count = static_cast<int>((p.N + BN - 1) / BN);
-  const int tiles = mt_count * nt_count;
+  const int tiles = g.tile_begin[g.n];
+  auto nkt_of = [&](int i) { return static_cast<int>((g.pr[i].p.K / 64 + 3) / 4); };
+  auto nslab_of = [&](int i) { return (g.pr[i].p.rank + 63) / 64; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -133,13 +140,15 @@ __global__ void __launch_bounds__(320, 1)
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
-    tma_prefetch(&tmSFA);
-    tma_prefetch(&tmSFB);
-    if (nslab) {
-      tma_prefetch(&tmX);
-      tma_prefetch(&tmL);
+    for (int i = 0; i < g.n; ++i) {
+      tma_prefetch(&g.pr[i].a);
+      tma_prefetch(&g.pr[i].b);
+      tma_prefetch(&g.pr[i].sfa);
+      tma_prefetch(&g.pr[i].sfb);
+      if (nslab_of(i)) {
+        tma_prefetch(&g.pr[i].xl1);
+        tma_prefetch(&g.pr[i].l2);
+      }
     }
   }
   if (warp == 1) tmem_alloc_cg2(tmem_slot, 512);
@@ -160,31 +169,36 @@ __global__ void __launch_bounds__(320, 1)
 #endif
       // Weight tiles (B, SFB) of the first tile's first ring do not depend on K1: issue them
       // before the programmatic dependency resolves, so they land while K1 finishes.
-      const int pre = (SVDQ_EXP & 4) || pair >= tiles ? 0 : min(kStages, nkt);
-      {
-        const int64_t n0 = static_cast<int64_t>(pair / mt_count) * BN;
+      const int pre = (SVDQ_EXP & 4) || pair >= tiles ? 0 : min(kStages, nkt_of(locate(g, pair).i));
+      if (pre) {
+        const TileRef tr = locate(g, pair);
+        const K2PairProblem &pr = g.pr[tr.i];
         for (int kt = 0; kt < pre; ++kt) {
           uint8_t *st = smem + kt * STAGE;
           const uint32_t fb = full0 + kt * 8;
           if (crank == 0) mbar_arrive_expect_tx(&full[kt], 2 * STAGE);
-          tma_load_2d_cg2(st + A_BYTES, &tmB, fb, kt * 128, static_cast<int32_t>(n0 + BNH * crank));
-          tma_load_3d_cg2(st + A_BYTES + B_BYTES + SFA_BYTES, &tmSFB, fb, 0, kt * 4,
-                          static_cast<int32_t>(n0 / 128));
+          tma_load_2d_cg2(st + A_BYTES, &pr.b, fb, kt * 128, static_cast<int32_t>(tr.n0 + BNH * crank));
+          tma_load_3d_cg2(st + A_BYTES + B_BYTES + SFA_BYTES, &pr.sfb, fb, 0, kt * 4,
+                          static_cast<int32_t>(tr.n0 / 128));
         }
       }
       griddep_wait();                                    // xq / xs / xl1 come from K1
       bool first = true;
       for (int t = pair; t < tiles; t += npairs) {
-        const int64_t m0 = static_cast<int64_t>(t % mt_count) * 256;
-        const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
+        const TileRef tr = locate(g, t);
+        const K2PairProblem &pr = g.pr[tr.i];
+        const int nkt = nkt_of(tr.i);
+        const int nslab = nslab_of(tr.i);
+        const int64_t m0 = tr.m0;
+        const int64_t n0 = tr.n0;
         const int32_t ma = static_cast<int32_t>(m0 + 128 * crank);
         const int32_t nb = static_cast<int32_t>(n0 + BNH * crank);
         for (int kt = 0; kt < nkt; ++kt) {
           uint8_t *st = smem + s * STAGE;
           const uint32_t fb = full0 + s * 8;
           if (first && kt < pre) {                         // B / SFB already in flight
-            tma_load_2d_cg2(st, &tmA, fb, kt * 128, ma);
-            tma_load_3d_cg2(st + A_BYTES + B_BYTES, &tmSFA, fb, 0, kt * 4, static_cast<int32_t>(m0 / 128 + crank));
+            tma_load_2d_cg2(st, &pr.a, fb, kt * 128, ma);
+            tma_load_3d_cg2(st + A_BYTES + B_BYTES, &pr.sfa, fb, 0, kt * 4, static_cast<int32_t>(m0 / 128 + crank));
             if (++s == kStages) { s = 0; ph ^= 1; }
             continue;
           }
@@ -195,10 +209,10 @@ __global__ void __launch_bounds__(320, 1)
           continue;
 #endif
           if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE);
-          tma_load_2d_cg2(st, &tmA, fb, kt * 128, ma);
-          tma_load_2d_cg2(st + A_BYTES, &tmB, fb, kt * 128, nb);
-          tma_load_3d_cg2(st + A_BYTES + B_BYTES, &tmSFA, fb, 0, kt * 4, static_cast<int32_t>(m0 / 128 + crank));
-          tma_load_3d_cg2(st + A_BYTES + B_BYTES + SFA_BYTES, &tmSFB, fb, 0, kt * 4,
+          tma_load_2d_cg2(st, &pr.a, fb, kt * 128, ma);
+          tma_load_2d_cg2(st + A_BYTES, &pr.b, fb, kt * 128, nb);
+          tma_load_3d_cg2(st + A_BYTES + B_BYTES, &pr.sfa, fb, 0, kt * 4, static_cast<int32_t>(m0 / 128 + crank));
+          tma_load_3d_cg2(st + A_BYTES + B_BYTES + SFA_BYTES, &pr.sfb, fb, 0, kt * 4,
                           static_cast<int32_t>(n0 / 128));
           if (++s == kStages) { s = 0; ph ^= 1; }
         }
@@ -208,8 +222,8 @@ __global__ void __launch_bounds__(320, 1)
           uint8_t *st = smem + s * STAGE;
           const uint32_t fb = full0 + s * 8;
           if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
-          tma_load_2d_cg2(st, &tmX, fb, j * 64, ma);
-          tma_load_2d_cg2(st + A_BYTES, &tmL, fb, j * 64, nb);
+          tma_load_2d_cg2(st, &pr.xl1, fb, j * 64, ma);
+          tma_load_2d_cg2(st + A_BYTES, &pr.l2, fb, j * 64, nb);
           if (++s == kStages) { s = 0; ph ^= 1; }
         }
       }
@@ -231,9 +245,14 @@ __global__ void __launch_bounds__(320, 1)
       const long long t_start = clock64();
 #endif
       for (int t = pair; t < tiles; t += npairs, ++acc_i) {
-        const int b = acc_i & 1;
-        const uint32_t acc_ph = (acc_i >> 1) & 1;
-        const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
+        const int b = (SVDQ_EXP & 64) ? 0 : acc_i & 1;            // 64: single accumulator (ablation)
+        const uint32_t acc_ph = (SVDQ_EXP & 64) ? acc_i & 1 : (acc_i >> 1) & 1;
+        const TileRef tr = locate(g, t);
+        const int64_t n0 = tr.n0;
+        const int nkb64 = static_cast<int>(g.pr[tr.i].p.K / 64);
+        const int nkt = nkt_of(tr.i);
+        const int nslab = nslab_of(tr.i);
+        const int rank = g.pr[tr.i].p.rank;
         const uint32_t sfb_off = static_cast<uint32_t>((n0 % 128) / 32);
         const uint32_t d_tmem = tmem + b * BN;
         { K2T_BEGIN(); mbar_wait(&acc_empty[b], acc_ph ^ 1); K2T_ACC(t_acc); }
@@ -300,7 +319,7 @@ __global__ void __launch_bounds__(320, 1)
             uint8_t *st = smem + s * STAGE;
             const uint32_t a_addr = smem_u32(st);
             const uint32_t b_addr = smem_u32(st + A_BYTES);
-            const int nk16 = min(4, (p.rank - j * 64) / 16);
+            const int nk16 = min(4, (rank - j * 64) / 16);
             for (int i = 0; i < nk16; ++i)
               mma_bf16_cg2(d_tmem, sdesc_kmajor_sw128(a_addr + 32 * i), sdesc_kmajor_sw128(b_addr + 32 * i),
                            idesc_h, (nkt > 0 || j > 0 || i > 0) ? 1u : 0u);
@@ -332,11 +351,13 @@ __global__ void __launch_bounds__(320, 1)
 #endif
     griddep_wait();
     for (int t = pair; t < tiles; t += npairs, ++acc_i) {
-      const int b = acc_i & 1;
-      const uint32_t acc_ph = (acc_i >> 1) & 1;
-      const int64_t m0 = static_cast<int64_t>(t % mt_count) * 256 + 128 * crank;
-      const int64_t n0 = static_cast<int64_t>(t / mt_count) * BN;
-      const int64_t grow = m0 + row;
+      const int b = (SVDQ_EXP & 64) ? 0 : acc_i & 1;
+      const uint32_t acc_ph = (SVDQ_EXP & 64) ? acc_i & 1 : (acc_i >> 1) & 1;
+      const TileRef tr = locate(g, t);
+      const K2Params &p = g.pr[tr.i].p;
+      const CUtensorMap *tmY = &g.pr[tr.i].y;
+      const int64_t m0 = tr.m0 + 128 * crank;
+      const int64_t n0 = tr.n0;
       named_bar(1, 256);
       for (int c = et; c < BN; c += 256)
         bias_s[c] = (p.bias && n0 + c < p.N) ? load_bias(p.bias, p.bias_dtype, n0 + c) : 0.f;
@@ -362,7 +383,7 @@ __global__ void __launch_bounds__(320, 1)
       continue;
 #endif
       epilogue_tile<BN, 2, kEpiBuf>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
-                           &tmY, static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
+                           tmY, static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
                            smem + EPI_OFF + (warp - 2) * 2048 * kEpiBuf, ebuf, lane, [&]() {
                           tc_fence_before();
                           __syncwarp();
@@ -386,8 +407,7 @@ __global__ void __launch_bounds__(320, 1)
 
 }  // namespace
 
-cudaError_t launch_k2_nvfp4_2sm(const K2Maps &maps, const CUtensorMap &sfa, const CUtensorMap &sfb,
-                                const K2Params &p, cudaStream_t s) {
+cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
   static_assert(SMEM <= 227 * 1024, "smem budget");
   cudaError_t e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   if (e != cudaSuccess) return e;
@@ -397,10 +417,28 @@ cudaError_t launch_k2_nvfp4_2sm(const K2Maps &maps, const CUtensorMap &sfa, cons
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int64_t tiles = ((p.M + 255) / 256) * ((p.N + BN - 1) / BN);
+  g.tile_begin[0] = 0;
+  for (int i = 0; i < g.n; ++i)
+    g.tile_begin[i + 1] = g.tile_begin[i] + static_cast<int>(((g.pr[i].p.M + 255) / 256) * ((g.pr[i].p.N + BN - 1) / BN));
+  const int64_t tiles = g.tile_begin[g.n];
   const int64_t pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  return launch_ex(k2_nvfp4_2sm_kernel, dim3(static_cast<unsigned>(2 * pairs)), dim3(320), SMEM, s, 2u, maps.a,
-                   maps.b, maps.xl1, maps.l2, sfa, sfb, maps.y, p);
+  return launch_ex(k2_nvfp4_2sm_kernel, dim3(static_cast<unsigned>(2 * pairs)), dim3(320), SMEM, s, 2u, g);
+}
+
+cudaError_t launch_k2_nvfp4_2sm(const K2Maps &maps, const CUtensorMap &sfa, const CUtensorMap &sfb,
+                                const K2Params &p, cudaStream_t s) {
+  K2PairArgs g;                              // host staging, copied into the launch parameters
+  static_assert(sizeof(K2PairArgs) < 30 * 1024, "kernel parameter space");
+  g.n = 1;
+  g.pr[0].a = maps.a;
+  g.pr[0].b = maps.b;
+  g.pr[0].xl1 = maps.xl1;
+  g.pr[0].l2 = maps.l2;
+  g.pr[0].sfa = sfa;
+  g.pr[0].sfb = sfb;
+  g.pr[0].y = maps.y;
+  g.pr[0].p = p;
+  return launch_k2_nvfp4_2sm_group(g, s);
 }
 
 }  // namespace svdq

@@ -123,3 +123,36 @@ def test_k2_long_k_pair_kernel(fmt, M, K, N, r):
     """K >= 6144 selects the CTA-pair (cta_group::2) NVFP4 kernel: ragged M / N (N not a
     multiple of the 192 tile, second SF atom absent), K tails (K % 256 = 64), ranks 0..128."""
     run_k2(fmt, M, K, N, r, seed=M + K, sample=64 if M > 512 else None)
+
+
+@pytest.mark.parametrize("shapes", [
+    [(4096 // 8, 3072, 9216 // 8, 32), (512 // 8, 3072, 9216 // 8, 32)],          # img / txt stream pair
+    [(300, 1152, 400, 48), (129, 640, 208, 16), (1, 256, 64, 0), (513, 6208, 192, 32)],
+])
+def test_k2_grouped_equals_single(shapes):
+    """svdq_gemm_w4a4_lowrank_up_grouped: problem i of one grouped launch is bit-identical to
+    its own single launch (same tiles, same per-element K order), and within 1e-3 of the oracle."""
+    need_cuda()
+    import torch
+    import paper_2411_05007_b200 as P
+    dev = torch.device("cuda")
+    layers, xq, xs, xl1, Ms, refs, Ys = [], [], [], [], [], [], []
+    for i, (M, K, N, r) in enumerate(shapes):
+        x, w, lam, ops = make_case("nvfp4", M, K, N, r, seed=70 + i)
+        layer = layer_from_ops(P, ops, dev)
+        qa = S.quantize_activation(x, ops)
+        q, sc = pack_act("nvfp4", qa, K)
+        layers.append(layer)
+        xq.append(to_dev(q.reshape(-1), dev))
+        xs.append(to_dev(sc.reshape(-1), dev))
+        xl1.append(to_dev(qa.xl1_bits.view(np.int16).reshape(-1), dev) if r else None)
+        Ms.append(M)
+        refs.append(S.round_output(S.gemm_reference(qa, ops), "bf16"))
+        Ys.append(torch.full((M, N), float("nan"), dtype=torch.bfloat16, device=dev))
+    P.svdq_gemm_w4a4_lowrank_up_grouped(layers, xq, xs, xl1, Ms, Ys)
+    torch.cuda.synchronize()
+    for i in range(len(shapes)):
+        single = P.svdq_gemm_w4a4_lowrank_up(layers[i], xq[i], xs[i], xl1[i], Ms[i])
+        torch.cuda.synchronize()
+        assert torch.equal(Ys[i], single), f"problem {i} differs from its single launch"
+        assert rel_fro(Ys[i].float().cpu().numpy(), refs[i]) <= 1e-3
