@@ -199,6 +199,26 @@ def run_svdq(args, rank, world, local_rank):
                 P.svdq_quantize_act_lowrank_down(layer, b["x"], b["xq"], b["xs"], b["xl1"], stream=st)
                 P.svdq_gemm_w4a4_lowrank_up(layer, b["xq"], b["xs"], b["xl1"], L.M, Y=b["y"], stream=st)
 
+    def step_grouped(bl, st):
+        """The double block's image- and text-stream linears of the same kind (qkv, proj, MLP up,
+        MLP down) as ONE grouped K1 and ONE grouped K2 launch each (independent problems; a
+        FLUX double block's two streams share no linear); the single block's linears alone."""
+        by = {L.name: (L, layer, b) for (L, layer, b) in bl}
+        for kind in ("qkv", "proj", "mlp_up", "mlp_down"):
+            grp = [by[f"double_{s_}_{kind}"] for s_ in ("img", "txt") if f"double_{s_}_{kind}" in by]
+            if not grp:
+                continue
+            P.svdq_quantize_act_lowrank_down_grouped([g_[1] for g_ in grp], [g_[2]["x"] for g_ in grp],
+                                                     [g_[2]["xq"] for g_ in grp], [g_[2]["xs"] for g_ in grp],
+                                                     [g_[2]["xl1"] for g_ in grp], stream=st)
+            P.svdq_gemm_w4a4_lowrank_up_grouped([g_[1] for g_ in grp], [g_[2]["xq"] for g_ in grp],
+                                                [g_[2]["xs"] for g_ in grp], [g_[2]["xl1"] for g_ in grp],
+                                                [g_[0].M for g_ in grp], [g_[2]["y"] for g_ in grp], stream=st)
+        for (L, layer, b) in bl:
+            if L.name.startswith("single"):
+                P.svdq_quantize_act_lowrank_down(layer, b["x"], b["xq"], b["xs"], b["xl1"], stream=st)
+                P.svdq_gemm_w4a4_lowrank_up(layer, b["xq"], b["xs"], b["xl1"], L.M, Y=b["y"], stream=st)
+
     def capture(bl):
         """CUDA graphs of one step: plain (timed region), with external timing events around
         every launch (per-kernel durations), K1-only and K2-only."""
@@ -216,6 +236,16 @@ def run_svdq(args, rank, world, local_rank):
         g["dag"] = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g["dag"], stream=stream):
             step_dag(bl, stream)
+        g["grouped"] = None
+        if args.fmt == "nvfp4":
+            with torch.cuda.stream(stream):
+                step_grouped(bl, stream)
+            torch.cuda.synchronize()
+            n1 = P.svdq_launch_count()
+            g["grouped"] = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g["grouped"], stream=stream):
+                step_grouped(bl, stream)
+            g["launches_grouped"] = P.svdq_launch_count() - n1
         with torch.cuda.graph(g["ev"], stream=stream):
             step(bl, stream, g["k1_ev"], g["k2_ev"])
         with torch.cuda.graph(g["k1"], stream=stream):
@@ -263,10 +293,10 @@ def run_svdq(args, rank, world, local_rank):
             for s in range(args.steps):
                 l2_flush()                          # L2 flush (outside the per-step events)
                 step_ev[s][0].record(stream)
-                g["dag"].replay()
+                (g["grouped"] or g["dag"]).replay()
                 step_ev[s][1].record(stream)
         torch.cuda.synchronize()
-    launches = g["launches"] * args.steps
+    launches = (g["launches_grouped"] if g["grouped"] is not None else g["launches"]) * args.steps
     if world > 1:
         dist.barrier()
     total_ms = float(sum(a.elapsed_time(b) for a, b in step_ev))
@@ -277,7 +307,8 @@ def run_svdq(args, rank, world, local_rank):
     nrep = max(3, min(args.steps, 20))
     k1_avg_s, k2_avg_s = per_kernel(g, nrep)
     only_ms = {"k1": time_graph(g["k1"], nrep), "k2": time_graph(g["k2"], nrep),
-               "serial": time_graph(g["plain"], nrep), "dag": time_graph(g["dag"], nrep)}
+               "serial": time_graph(g["plain"], nrep), "dag": time_graph(g["dag"], nrep),
+               "grouped": time_graph(g["grouped"], nrep) if g["grouped"] is not None else None}
 
     # ---------------- low-rank overhead: the same step at rank 0
     lowrank = None
@@ -429,11 +460,13 @@ def run_svdq(args, rank, world, local_rank):
                 "path": "svdq_linear_forward (C ABI) per linear; pinned host X in, Y out"},
         "graph_only_ms": {"k1_all_layers": round(only_ms["k1"], 4), "k2_all_layers": round(only_ms["k2"], 4),
                           "step_serial": round(only_ms["serial"], 4), "step_img_txt_concurrent": round(only_ms["dag"], 4),
+                          "step_img_txt_grouped": round(only_ms["grouped"], 4) if only_ms["grouped"] else None,
                           "note": "each kernel's launches replayed back to back as one graph (L2 flushed before)"},
         "gpu_launches": int(launches),
-        "timing": "step captured once as a CUDA graph (20 launches; the double block's image and text "
-                  "streams on two graph branches, the single block after the join), replayed per step; "
-                  "per-kernel times from a second, serial graph with external timing events around each launch",
+        "timing": "step captured once as a CUDA graph and replayed per step: the double block's image- and "
+                  "text-stream linears of each kind run as one grouped K1 + one grouped K2 launch (12 launches "
+                  "per step; INT4: two graph branches, 20 launches); per-kernel times from a second, serial "
+                  "graph of single launches with external timing events around each launch",
         "clocks": clocks,
     }
 

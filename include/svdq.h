@@ -110,6 +110,16 @@ svdq_status svdq_quantize_act_lowrank_down(const svdq_linear *L, const void *X, 
                                            int64_t M, int64_t ldx, uint8_t *xq, uint8_t *xs,
                                            uint16_t *xl1, void *stream);
 
+/* Grouped K1: n (1..4) independent problems (bf16 X; layers sharing format, rank and INT4
+ * scale dtype) in ONE launch whose row tiles are the concatenation of the problems' row tiles.
+ * Problem i is exactly svdq_quantize_act_lowrank_down(layers[i], X[i], BF16, M[i], ldx[i],
+ * xq[i], xs[i], xl1[i]) (bit-identical outputs).  Arrays are [host], n entries each.
+ * SVDQ_ERR_UNSUPPORTED for fp16 X or mixed format / rank.                             */
+svdq_status svdq_quantize_act_lowrank_down_grouped(int32_t n, const svdq_linear *const *layers,
+                                                   const void *const *X, int32_t x_dtype, const int64_t *M,
+                                                   const int64_t *ldx, uint8_t *const *xq, uint8_t *const *xs,
+                                                   uint16_t *const *xl1, void *stream);
+
 /* K2: 4-bit GEMM with the low-rank up-projection folded into the same accumulator.
  *   NVFP4: acc[m,n] = sum_g f(sfa[m,g]) f(sfb[n,g]) sum_{k in g} e2m1(qa) e2m1(qb)
  *                     + sum_t xl1[m,t] l2s[n,t]          (tcgen05 kind::mxf4nvf4 + kind::f16)

@@ -36,6 +36,7 @@ DTYPE_OF_TORCH = {torch.bfloat16: "bf16", torch.float16: "fp16", torch.float32: 
 # Every symbol include/svdq.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "svdq_act_buffer_sizes", "svdq_weight_buffer_sizes", "svdq_quantize_act_lowrank_down",
+    "svdq_quantize_act_lowrank_down_grouped",
     "svdq_gemm_w4a4_lowrank_up", "svdq_gemm_w4a4_lowrank_up_grouped", "svdq_linear_forward",
     "svdq_quantize_residual",
     "svdq_quantize_weights_workspace", "svdq_quantize_weights", "svdq_lora_fuse",
@@ -71,6 +72,8 @@ _sig = {
     "svdq_weight_buffer_sizes": [_I32, _I64, _I64, _I32, _SZ, _SZ, _SZ, _SZ],
     "svdq_quantize_act_lowrank_down": [_LP, _P, _I32, _I64, _I64, _P, _P, _P, _P],
     "svdq_gemm_w4a4_lowrank_up": [_LP, _P, _P, _P, _I64, _P, _I32, _I64, _P],
+    "svdq_quantize_act_lowrank_down_grouped": [_I32, C.POINTER(_LP), C.POINTER(_P), _I32, C.POINTER(_I64),
+                                               C.POINTER(_I64), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), _P],
     "svdq_gemm_w4a4_lowrank_up_grouped": [_I32, C.POINTER(_LP), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
                                           C.POINTER(_I64), C.POINTER(_P), _I32, C.POINTER(_I64), _P],
     "svdq_linear_forward": [_LP, _P, _I32, _I64, _I64, _P, _I32, _I64, _P, C.c_size_t, _P],
@@ -214,6 +217,20 @@ def svdq_gemm_w4a4_lowrank_up(layer: QuantizedLinear, xq, xs, xl1, M: int, Y=Non
         layer.ref, _ptr(xq), _ptr(xs), _ptr(xl1), M, _ptr(Y), DTYPE[DTYPE_OF_TORCH[Y.dtype]],
         Y.stride(0), _stream(stream)), "svdq_gemm_w4a4_lowrank_up")
     return Y
+
+
+def svdq_quantize_act_lowrank_down_grouped(layers, X, xq, xs, xl1, stream=None):
+    """Grouped K1: one launch over n (1..4) problems with bf16 X; lists of equal length.
+    Problem i produces exactly svdq_quantize_act_lowrank_down(layers[i], X[i], xq[i], xs[i], xl1[i])."""
+    n = len(layers)
+    arr = lambda T, vals: (T * n)(*vals)
+    _check(_lib.svdq_quantize_act_lowrank_down_grouped(
+        n, arr(_LP, [C.pointer(l.view) for l in layers]), arr(_P, [x.data_ptr() for x in X]),
+        DTYPE[DTYPE_OF_TORCH[X[0].dtype]], arr(_I64, [x.shape[0] for x in X]), arr(_I64, [x.stride(0) for x in X]),
+        arr(_P, [q.data_ptr() for q in xq]), arr(_P, [q.data_ptr() for q in xs]),
+        arr(_P, [q.data_ptr() if q is not None else None for q in xl1]), _stream(stream)),
+        "svdq_quantize_act_lowrank_down_grouped")
+    return xq, xs, xl1
 
 
 def svdq_gemm_w4a4_lowrank_up_grouped(layers, xq, xs, xl1, M, Y, stream=None):

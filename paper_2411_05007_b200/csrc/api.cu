@@ -200,9 +200,12 @@ svdq_status svdq_weight_buffer_sizes(int32_t fmt, int64_t K, int64_t N, int32_t 
   return SVDQ_OK;
 }
 
-svdq_status svdq_quantize_act_lowrank_down(const svdq_linear *L, const void *X, int32_t x_dtype,
-                                           int64_t M, int64_t ldx, uint8_t *xq, uint8_t *xs,
-                                           uint16_t *xl1, void *stream) {
+}  // extern "C"
+
+namespace {
+// Validation, launch parameters and (bf16 X) tensor maps of one K1 problem.
+svdq_status prepare_k1(const svdq_linear *L, const void *X, int32_t x_dtype, int64_t M, int64_t ldx, uint8_t *xq,
+                       uint8_t *xs, uint16_t *xl1, K1Params *out, K1Maps *maps) {
   svdq_status st = check_linear(L, false);
   if (st != SVDQ_OK) return st;
   if (!X || !xq || !xs || (L->rank > 0 && !xl1)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null buffer");
@@ -213,7 +216,8 @@ svdq_status svdq_quantize_act_lowrank_down(const svdq_linear *L, const void *X, 
   if (ldx % 8 || !aligned16(X) || !aligned16(xq) || !aligned16(xs) || (xl1 && !aligned16(xl1)))
     return fail(SVDQ_ERR_ALIGNMENT, "X / ldx / outputs must be 16-byte aligned");
   if ((st = check_device()) != SVDQ_OK) return st;
-  K1Params p{};
+  K1Params &p = *out;
+  p = K1Params{};
   p.fmt = L->fmt == SVDQ_FMT_NVFP4 ? 0 : 1;
   p.x_bf16 = x_dtype == SVDQ_BF16;
   p.scale_bf16 = L->scale_dtype == SVDQ_BF16;
@@ -229,25 +233,63 @@ svdq_status svdq_quantize_act_lowrank_down(const svdq_linear *L, const void *X, 
   p.xq = xq;
   p.xs = xs;
   p.xl1 = xl1;
-  cudaError_t e;
+  std::memset(maps, 0, sizeof(*maps));
   if (p.x_bf16) {
     // TMA + tcgen05 path: X tiles [128 x 64] and L1s tiles [rank x 64], 128-B swizzle
-    K1Maps maps;
-    std::memset(&maps, 0, sizeof(maps));
-    if ((st = make_map(&maps.x, X, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->K, M, ldx * 2, 64, 128)) != SVDQ_OK)
+    if ((st = make_map(&maps->x, X, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->K, M, ldx * 2, 64, 128)) != SVDQ_OK)
       return st;
     if (L->rank > 0 &&
-        (st = make_map(&maps.l1s, L->l1s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->K, L->rank, L->K * 2, 64,
+        (st = make_map(&maps->l1s, L->l1s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->K, L->rank, L->K * 2, 64,
                        static_cast<uint32_t>(L->rank))) != SVDQ_OK)
       return st;
-    if ((st = make_map(&maps.lam, L->lambda_inv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 32, L->K / 32, 128, 32, 2)) !=
+    if ((st = make_map(&maps->lam, L->lambda_inv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 32, L->K / 32, 128, 32, 2)) !=
         SVDQ_OK)
       return st;
-    e = launch_k1_tc(maps, p, static_cast<cudaStream_t>(stream));
-  } else {
-    e = launch_k1(p, static_cast<cudaStream_t>(stream));
   }
+  return SVDQ_OK;
+}
+}  // namespace
+
+extern "C" {
+
+svdq_status svdq_quantize_act_lowrank_down(const svdq_linear *L, const void *X, int32_t x_dtype,
+                                           int64_t M, int64_t ldx, uint8_t *xq, uint8_t *xs,
+                                           uint16_t *xl1, void *stream) {
+  K1Params p;
+  K1Maps maps;
+  svdq_status st = prepare_k1(L, X, x_dtype, M, ldx, xq, xs, xl1, &p, &maps);
+  if (st != SVDQ_OK) return st;
+  cudaError_t e = p.x_bf16 ? launch_k1_tc(maps, p, static_cast<cudaStream_t>(stream))
+                           : launch_k1(p, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "K1 launch");
+  ++g_launches;
+  return SVDQ_OK;
+}
+
+svdq_status svdq_quantize_act_lowrank_down_grouped(int32_t n, const svdq_linear *const *layers,
+                                                   const void *const *X, int32_t x_dtype, const int64_t *M,
+                                                   const int64_t *ldx, uint8_t *const *xq, uint8_t *const *xs,
+                                                   uint16_t *const *xl1, void *stream) {
+  if (n < 1 || n > kMaxGroup1) return fail(SVDQ_ERR_INVALID_ARGUMENT, "group size must be 1..%d", kMaxGroup1);
+  if (!layers || !X || !M || !ldx || !xq || !xs || !xl1) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null array");
+  if (x_dtype != SVDQ_BF16) return fail(SVDQ_ERR_UNSUPPORTED, "grouped K1 needs bf16 activations");
+  K1Args g;
+  std::memset(&g, 0, sizeof(g));
+  g.n = n;
+  for (int i = 0; i < n; ++i) {
+    if (!layers[i]) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null layer %d", i);
+    if (layers[i]->fmt != layers[0]->fmt || layers[i]->rank != layers[0]->rank ||
+        (layers[i]->fmt == SVDQ_FMT_INT4 && layers[i]->scale_dtype != layers[0]->scale_dtype))
+      return fail(SVDQ_ERR_UNSUPPORTED, "grouped K1: layers must share format, rank and scale dtype");
+    K1Maps maps;
+    svdq_status st = prepare_k1(layers[i], X[i], x_dtype, M[i], ldx[i], xq[i], xs[i], xl1[i], &g.pr[i].p, &maps);
+    if (st != SVDQ_OK) return st;
+    g.pr[i].x = maps.x;
+    g.pr[i].l1s = maps.l1s;
+    g.pr[i].lam = maps.lam;
+  }
+  cudaError_t e = launch_k1_tc_group(g, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "grouped K1 launch");
   ++g_launches;
   return SVDQ_OK;
 }

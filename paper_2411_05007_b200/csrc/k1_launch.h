@@ -63,6 +63,19 @@ struct K1Maps {
   CUtensorMap x, l1s, lam;    // lam: lambda_inv viewed as [K/32][32] fp32, box {32, 2}, 128-B swizzle
 };
 cudaError_t launch_k1_tc(const K1Maps &maps, const K1Params &p, cudaStream_t s);   // bf16 X
+// Grouped K1: up to kMaxGroup1 problems (same fmt, scale dtype and rank) in one launch; the
+// grid's row-tile axis runs over the concatenated row tiles.
+constexpr int kMaxGroup1 = 4;
+struct K1Problem {
+  CUtensorMap x, l1s, lam;
+  K1Params p;
+};
+struct K1Args {
+  K1Problem pr[kMaxGroup1];
+  int n;
+  int tile_begin[kMaxGroup1 + 1];
+};
+cudaError_t launch_k1_tc_group(K1Args &g, cudaStream_t s);
 int k1_tc_ksplit(int64_t Mpad, int64_t K);
 
 struct K2Params {

@@ -110,12 +110,14 @@ __host__ __device__ inline K1Layout k1_layout(int rank) {
 
 template <int kFmt, bool kScaleBf16>
 __global__ void __launch_bounds__(kThreads, 1)
-    k1_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmL,
-                 const __grid_constant__ CUtensorMap tmLam,
-                 const K1Params p, int ks) {
+    k1_tc_kernel(const __grid_constant__ K1Args g, int ks) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~static_cast<uintptr_t>(1023));
+  int pi = 0;                                      // problem of this row tile
+  while (pi + 1 < g.n && static_cast<int>(blockIdx.y) >= g.tile_begin[pi + 1]) ++pi;
+  const K1Params &p = g.pr[pi].p;
+  const CUtensorMap &tmX = g.pr[pi].x, &tmL = g.pr[pi].l1s, &tmLam = g.pr[pi].lam;
   const int r = p.rank;
   const K1Layout Ly = k1_layout(r);
   const int S = Ly.stages;
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int crank = static_cast<int>(blockIdx.x);          // rank in the K-split cluster
   const int kb_begin = crank * nkb / ks;
   const int nsteps = (crank + 1) * nkb / ks - kb_begin;
-  const int64_t row0 = static_cast<int64_t>(blockIdx.y) * 128;
+  const int64_t row0 = static_cast<int64_t>(static_cast<int>(blockIdx.y) - g.tile_begin[pi]) * 128;
   // four accumulators (one per 16-wide K sub-step) so consecutive MMAs are independent
   const uint32_t tcols = 4 * r <= 128 ? 128 : (4 * r <= 256 ? 256 : 512);
 
@@ -442,16 +444,23 @@ int choose_ksplit(Kern kern, const K1Layout &Ly, int64_t tiles, int64_t nkb) {
 }
 
 template <int kFmt, bool kScaleBf16>
-cudaError_t launch_t(const K1Maps &maps, const K1Params &p, int /*ks_hint*/, cudaStream_t s) {
+cudaError_t launch_t(K1Args &g, cudaStream_t s) {
   auto kern = k1_tc_kernel<kFmt, kScaleBf16>;
-  const K1Layout Ly = k1_layout(p.rank);
+  const K1Layout Ly = k1_layout(g.pr[0].p.rank);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(Ly.smem));
   if (e != cudaSuccess) return e;
-  int ks = choose_ksplit(kern, Ly, p.Mpad / 128, p.K / 64);
+  g.tile_begin[0] = 0;
+  int64_t min_nkb = g.pr[0].p.K / 64;
+  for (int i = 0; i < g.n; ++i) {
+    g.tile_begin[i + 1] = g.tile_begin[i] + static_cast<int>(g.pr[i].p.Mpad / 128);
+    min_nkb = g.pr[i].p.K / 64 < min_nkb ? g.pr[i].p.K / 64 : min_nkb;
+  }
+  const int tiles = g.tile_begin[g.n];
+  int ks = choose_ksplit(kern, Ly, tiles, min_nkb);
   if (const char *e = getenv("SVDQ_K1_KS")) ks = atoi(e);     // ablation override (debug)
-  return launch_ex_cluster(kern, dim3(static_cast<unsigned>(ks), static_cast<unsigned>(p.Mpad / 128), 1),
-                   dim3(kThreads, 1, 1), Ly.smem, s, static_cast<unsigned>(ks), maps.x, maps.l1s, maps.lam, p, ks);
+  return launch_ex_cluster(kern, dim3(static_cast<unsigned>(ks), static_cast<unsigned>(tiles), 1),
+                           dim3(kThreads, 1, 1), Ly.smem, s, static_cast<unsigned>(ks), g, ks);
 }
 
 }  // namespace
@@ -464,10 +473,20 @@ int k1_tc_ksplit(int64_t Mpad, int64_t K) {
   return ks;
 }
 
+cudaError_t launch_k1_tc_group(K1Args &g, cudaStream_t s) {
+  const K1Params &p = g.pr[0].p;
+  if (p.fmt == 0) return launch_t<0, true>(g, s);
+  return p.scale_bf16 ? launch_t<1, true>(g, s) : launch_t<1, false>(g, s);
+}
+
 cudaError_t launch_k1_tc(const K1Maps &maps, const K1Params &p, cudaStream_t s) {
-  const int ks = k1_tc_ksplit(p.Mpad, p.K);
-  if (p.fmt == 0) return launch_t<0, true>(maps, p, ks, s);
-  return p.scale_bf16 ? launch_t<1, true>(maps, p, ks, s) : launch_t<1, false>(maps, p, ks, s);
+  K1Args g;                                  // host staging, copied into the launch parameters
+  g.n = 1;
+  g.pr[0].x = maps.x;
+  g.pr[0].l1s = maps.l1s;
+  g.pr[0].lam = maps.lam;
+  g.pr[0].p = p;
+  return launch_k1_tc_group(g, s);
 }
 
 }  // namespace svdq

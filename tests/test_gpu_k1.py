@@ -78,3 +78,34 @@ def test_k1_nvfp4_static_gs():
 def test_k1_flux_qkv_full(fmt):
     """BASELINE config C4 activation shape (M=4608, K=3072, r=32), bit-exact at full size."""
     run_k1(fmt, 4608, 3072, 64, 32, seed=4)
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+def test_k1_grouped_equals_single(fmt):
+    """svdq_quantize_act_lowrank_down_grouped: every problem's codes, scales and xl1 are
+    bit-identical to its own single launch, and match the oracle bit-exactly (codes/scales)."""
+    need_cuda()
+    import torch
+    import paper_2411_05007_b200 as P
+    dev = torch.device("cuda")
+    shapes = [(300, 1152, 32), (64, 1152, 32), (129, 3072, 32)]
+    layers, X, outs, refs = [], [], [], []
+    for i, (M, K, r) in enumerate(shapes):
+        x, w, lam, ops = make_case(fmt, M, K, 128, r, seed=90 + i)
+        layers.append(layer_from_ops(P, ops, dev))
+        X.append(torch.from_numpy(x).to(dev).to(torch.bfloat16))
+        bq, bs, bl = P.svdq_act_buffer_sizes(fmt, M, K, r)
+        outs.append((torch.zeros(bq, dtype=torch.uint8, device=dev), torch.zeros(bs, dtype=torch.uint8, device=dev),
+                     torch.zeros(bl // 2, dtype=torch.int16, device=dev)))
+        refs.append((ops, x))
+    P.svdq_quantize_act_lowrank_down_grouped(layers, X, [o[0] for o in outs], [o[1] for o in outs],
+                                             [o[2] for o in outs])
+    torch.cuda.synchronize()
+    for i, (M, K, r) in enumerate(shapes):
+        sq, ss, sl = P.svdq_quantize_act_lowrank_down(layers[i], X[i])
+        torch.cuda.synchronize()
+        assert torch.equal(outs[i][0], sq) and torch.equal(outs[i][1], ss) and torch.equal(outs[i][2], sl)
+        ops, x = refs[i]
+        qa = S.quantize_activation(x, ops)
+        ref_q = F.pack_nibbles(qa.codes if fmt == "nvfp4" else F.int4_to_nibble(qa.codes))
+        np.testing.assert_array_equal(sq.cpu().numpy().reshape(M, K // 2), ref_q)
