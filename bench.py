@@ -112,7 +112,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ svdq arm
-def build_layers(P, torch, layers, fmt, dev):
+def build_layers(P, torch, layers, fmt, dev, quality=None):
     """Synthetic FLUX-shaped layers (DESIGN.md input recipe), weights prepared on the GPU
     by svdq_quantize_weights (fp64 Gram + eigensolver SVD, residual quantization)."""
     out = []
@@ -126,6 +126,12 @@ def build_layers(P, torch, layers, fmt, dev):
         layer = P.svdq_quantize_weights(torch.from_numpy(w).to(dev), torch.from_numpy(lam).to(dev), L.r,
                                         fmt, "bf16", 1.0, bias=bias)
         x = torch.from_numpy(synth.gen_x(L.M, L.K, synth.rng(4, i, 0))).to(dev).to(torch.bfloat16)
+        if quality is not None:
+            # unscored sanity metric: ||XW + b - Y|| / ||XW + b|| on 64 rows, fp64 reference
+            rows = torch.arange(0, L.M, max(1, L.M // 64), device=dev)[:64]
+            y_s = P.svdq_linear_forward(layer, x[rows].contiguous()).double()
+            ref = x[rows].double() @ torch.from_numpy(w).to(dev).double() + bias.double()
+            quality[L.name] = round(float((y_s - ref).norm() / ref.norm()), 5)
         bq, bs, bl = P.svdq_act_buffer_sizes(fmt, L.M, L.K, L.r)
         bufs = dict(
             x=x,
@@ -148,7 +154,8 @@ def run_svdq(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     layers = flux_block_layers(args.batch)
-    built = build_layers(P, torch, layers, args.fmt, dev)
+    quality = {}
+    built = build_layers(P, torch, layers, args.fmt, dev, quality)
     flops = sum(2.0 * L.M * L.N * L.K for L in layers)
     k1_bytes = sum(L.M * L.K * 2 + L.M * L.K * (0.5625 if args.fmt == "nvfp4" else 0.53125)
                    + L.M * L.r * 2 for L in layers)
@@ -414,6 +421,34 @@ def run_svdq(args, rank, world, local_rank):
             except Exception as e:  # noqa: BLE001  (context only; never part of the product path)
                 library = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
         lowrank["library_context"] = library
+        # ---------------- unfused pipeline (the paper's Fig. 5(a)): K1(r=0) + K2(r=0) + the
+        # low-rank branch as two separate cuBLAS bf16 GEMMs and an add, vs the fused step
+        try:
+            lr = []
+            for (L, l32, b32), (_, l0, b0) in zip(built, built0):
+                l1 = l32.l1s.view(torch.bfloat16).reshape(L.r, L.K)
+                l2 = l32.l2s.view(torch.bfloat16).reshape(L.N, L.r)
+                lr.append((L, l0, b0, l1, l2, torch.empty(L.M, L.r, dtype=torch.bfloat16, device=dev)))
+
+            def unfused_step():
+                for (L, l0, b0, l1, l2, xl1u) in lr:
+                    P.svdq_quantize_act_lowrank_down(l0, b0["x"], b0["xq"], b0["xs"], b0["xl1"], stream=stream)
+                    P.svdq_gemm_w4a4_lowrank_up(l0, b0["xq"], b0["xs"], b0["xl1"], L.M, Y=b0["y"], stream=stream)
+                    torch.matmul(b0["x"], l1.t(), out=xl1u)                # X L1s^T   (re-reads X)
+                    b0["y"].addmm_(xl1u, l2.t(), alpha=l0.gs_x * l0.gs_w)   # + xl1 L2s^T (re-reads / writes Y)
+            with torch.cuda.stream(stream):
+                unfused_step()
+            torch.cuda.synchronize()
+            gu = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gu, stream=stream):
+                unfused_step()
+            t_unf = time_graph(gu, nrep)
+            lowrank["unfused_fig5a"] = {
+                "step_ms_unfused": round(t_unf, 4), "step_ms_fused": round(step_r_ms, 4),
+                "fused_speedup": round(t_unf / step_r_ms, 3),
+                "def": "K1(r=0) + K2(r=0) + cuBLAS bf16 X.L1s^T + cuBLAS addmm xl1.L2s^T into Y, per linear, serial graph"}
+        except Exception as e:  # noqa: BLE001  (context only)
+            lowrank["unfused_fig5a"] = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
         del built0, g0
         torch.cuda.empty_cache()
 
@@ -504,6 +539,8 @@ def run_svdq(args, rank, world, local_rank):
                "frac": round(k1_gbs / pk["hbm_gbs"], 4),
                "achieved_def": "sum (2MK + 0.5625MK + 2Mr) / sum of K1 durations"},
         "lowrank_overhead": lowrank,
+        "quality_rel_err_vs_fp64_XW": {"note": "unscored sanity metric: ||XW + b - Y|| / ||XW + b||, 64 rows per "
+                                               "linear, synthetic outlier activations (SURVEY 8(d))", **quality},
         "per_launch": per_launch,
         "per_layer": per_layer,
         "e2e": {"value": round(world * flops * n_e2e / (e2e_ms / 1e3) / 1e12, 3), "unit": UNIT,
