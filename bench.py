@@ -446,6 +446,10 @@ def run_svdq(args, rank, world, local_rank):
             lowrank["unfused_fig5a"] = {
                 "step_ms_unfused": round(t_unf, 4), "step_ms_fused": round(step_r_ms, 4),
                 "fused_speedup": round(t_unf / step_r_ms, 3),
+                "lowrank_overhead_unfused": round((t_unf - step0_ms) / step0_ms, 4),
+                "lowrank_overhead_fused": round((step_r_ms - step0_ms) / step0_ms, 4),
+                "paper": "57 % for the naive rank-32 branch (Fig. 5(a) caption, P:165); ~50 % of the 4-bit "
+                         "branch latency (P:173)",
                 "def": "K1(r=0) + K2(r=0) + cuBLAS bf16 X.L1s^T + cuBLAS addmm xl1.L2s^T into Y, per linear, serial graph"}
         except Exception as e:  # noqa: BLE001  (context only)
             lowrank["unfused_fig5a"] = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
