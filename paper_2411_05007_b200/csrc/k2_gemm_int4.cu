@@ -32,6 +32,12 @@
 #include "k1_launch.h"
 #include "sm100.cuh"
 
+// Waits of the INT4 kernel: it is issue-bound (promotion on CUDA cores), so waiting warps must
+// not spin (ncu: try_wait loops were a third of all issued instructions).
+#ifndef SVDQ_I4_SLEEP_NS
+#define SVDQ_I4_SLEEP_NS 64
+#endif
+#define SVDQ_I4_WAIT(bar, par) mbar_wait_sleep((bar), (par), SVDQ_I4_SLEEP_NS)
 #ifndef SVDQ_I4EXP
 #define SVDQ_I4EXP 0   // ablation bits: 1 no scale fetch, 2 no promotion math, 4 no unpack, 8 no MMA
 #endif
@@ -266,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       if (nslab) {
         const int b = gi % kAcc;
-        mbar_wait_spin(&g_empty[b], ((gi / kAcc) & 1) ^ 1);
+        SVDQ_I4_WAIT(&g_empty[b], ((gi / kAcc) & 1) ^ 1);
         mbar_wait(slab_full, it & 1);
         tc_fence_after();
         if (elect_one()) {
@@ -292,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ng = min(2, G - 2 * k);
         for (int j = 0; j < ng; ++j, ++gi) {
           const int b = gi % kAcc;
-          { I4T_BEGIN(); mbar_wait_spin(&g_empty[b], ((gi / kAcc) & 1) ^ 1); I4T_ACC(t_ge); }
+          { I4T_BEGIN(); SVDQ_I4_WAIT(&g_empty[b], ((gi / kAcc) & 1) ^ 1); I4T_ACC(t_ge); }
           tc_fence_after();
           if (elect_one()) {
 #pragma unroll
@@ -443,11 +449,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int g = blk * kGB + j;
           if (g >= G) break;
           const int b = gi % kAcc;
-          { I4T_BEGIN(); mbar_wait_spin(&g_full[b], (gi / kAcc) & 1); I4T_ACC(t_gf); }
+          { I4T_BEGIN(); SVDQ_I4_WAIT(&g_full[b], (gi / kAcc) & 1); I4T_ACC(t_gf); }
           tc_fence_after();
           const float sxv = lds_f32(sxb + (j * EC + lane) * 4);
           const uint64_t sx2 = f2pack(sxv, sxv);
           const uint32_t swg = swb + j * EC * 4;
+#pragma unroll
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {               // two 16-column halves: 16 live registers
             uint32_t r[16];

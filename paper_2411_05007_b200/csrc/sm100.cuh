@@ -60,6 +60,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+// Back-off variant for kernels bound by instruction issue: a failed probe parks the warp for
+// ~`ns` nanoseconds instead of re-issuing the probe loop.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(ns);
+  }
+}
+
 // Spin variant (no suspend-time hint) for short latency-critical waits.
 __device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
   asm volatile(
