@@ -78,3 +78,26 @@ def test_no_cpu_fallback_in_product_path():
         if f.endswith(".py"):
             src = open(os.path.join(pkg, f)).read()
             assert not re.search(r"^\s*(from|import)\s+oracle", src, flags=re.M), f
+
+
+def test_grouped_argument_validation_before_device():
+    """Grouped entry points reject bad group sizes / NULL arrays on the host, before any launch."""
+    lib = P.abi.lib()
+    st = lib.svdq_gemm_w4a4_lowrank_up_grouped(0, None, None, None, None, None, None, 0, None, None)
+    assert st == 1
+    st = lib.svdq_gemm_w4a4_lowrank_up_grouped(5, None, None, None, None, None, None, 0, None, None)
+    assert st == 1
+    st = lib.svdq_gemm_w4a4_lowrank_up_grouped(2, None, None, None, None, None, None, 0, None, None)
+    assert st == 1
+    st = lib.svdq_quantize_act_lowrank_down_grouped(0, None, None, 0, None, None, None, None, None, None)
+    assert st == 1
+    st = lib.svdq_quantize_act_lowrank_down_grouped(9, None, None, 0, None, None, None, None, None, None)
+    assert st == 1
+    # fp16 activations are not supported by the grouped K1 (bf16 TMA path only)
+    L = P.abi.svdq_linear()
+    L.fmt, L.K, L.N, L.rank = 0, 128, 64, 16
+    arr = (ctypes.POINTER(P.abi.svdq_linear) * 1)(ctypes.pointer(L))
+    one = (ctypes.c_void_p * 1)(None)
+    i64 = (ctypes.c_int64 * 1)(8)
+    st = lib.svdq_quantize_act_lowrank_down_grouped(1, arr, one, 1, i64, i64, one, one, one, None)
+    assert st == 5
