@@ -124,6 +124,35 @@ def dequantize_int4(codes, s_bits, scale_dtype: str) -> np.ndarray:
 
 
 # --------------------------------------------------------------------------
+# INT8 (8-bit setting of App. D): "per-token dynamic activation quantization and
+# per-channel weight quantization" -- Eq. (1) with q_max = 2^(8-1) - 1 = 127, one scale per
+# row of the operand (a token of X_hat, or an output channel of R^T), fp32 scales (reading W1)
+# --------------------------------------------------------------------------
+INT8_QMAX = 127
+
+
+def quantize_int8_rows(v) -> tuple[np.ndarray, np.ndarray]:
+    """Eq. (1) per row of the last axis:
+        amax = max |v_i|;  s = fl32(amax / 127)   (fp32 scale, stored)
+        qinv = s == 0 ? 0 : fl32(1 / s)
+        q_i  = clamp(rne(fl32(v_i * qinv)), -127, 127)
+    Returns (codes int64 [.., K], scales fp32 [..])."""
+    v = np.asarray(v, dtype=F32)
+    _check_finite(v)
+    amax = np.max(np.abs(v), axis=-1).astype(F32) if v.shape[-1] else np.zeros(v.shape[:-1], F32)
+    s = (amax / F32(INT8_QMAX)).astype(F32)
+    with np.errstate(divide="ignore"):
+        qinv = np.where(s == 0, F32(0), F32(1.0) / s).astype(F32)
+    x = (v * qinv[..., None]).astype(F32)
+    q = np.clip(np.rint(x), -INT8_QMAX, INT8_QMAX).astype(np.int64)
+    return q, s
+
+
+def dequantize_int8_rows(codes, s) -> np.ndarray:
+    return np.asarray(codes).astype(np.float64) * np.asarray(s, np.float64)[..., None]
+
+
+# --------------------------------------------------------------------------
 # Smoothing of the activation, P:122 with reading Q14
 # --------------------------------------------------------------------------
 def smooth_activation(x, lam_inv32) -> np.ndarray:

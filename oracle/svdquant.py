@@ -143,6 +143,9 @@ def quantize_residual(R32, fmt: str, scale_dtype: str = "bf16", gs_w=None):
     if fmt == "int4":
         codes, s = Q.quantize_int4(Rt, scale_dtype)
         return codes, s, F32(1.0)
+    if fmt == "w8a8":                                     # per-channel INT8
+        codes, s = Q.quantize_int8_rows(Rt)
+        return codes, s, F32(1.0)
     raise ValueError(fmt)
 
 
@@ -162,7 +165,7 @@ def prepare_operands(w, lam32, r: int, fmt: str, gs_x=1.0, scale_dtype="bf16",
     L2s_bits = F.bf16_bits(d.L2.T / float(alpha))                                    # [N, r]
     b = None if bias is None else np.asarray(bias, dtype=F32)
     return Operands(fmt, K, N, r, codes, scales,
-                    "e4m3" if fmt == "nvfp4" else scale_dtype,
+                    {"nvfp4": "e4m3", "w8a8": "fp32"}.get(fmt, scale_dtype),
                     F32(gs_w), gs_x, lam_inv32, np.ascontiguousarray(L1s_bits),
                     np.ascontiguousarray(L2s_bits), b)
 
@@ -188,6 +191,8 @@ def quantize_activation(x, ops: Operands, act_scale_dtype: Optional[str] = None)
     xh = Q.smooth_activation(x, ops.lam_inv32)
     if ops.fmt == "nvfp4":
         codes, scales = Q.quantize_nvfp4(xh, ops.gs_x)
+    elif ops.fmt == "w8a8":                               # per-token dynamic INT8
+        codes, scales = Q.quantize_int8_rows(xh)
     else:
         codes, scales = Q.quantize_int4(xh, act_scale_dtype or ops.scale_dtype)
     xl1 = x.astype(np.float64) @ ops.L1s.astype(np.float64).T
@@ -222,6 +227,11 @@ def main_product(act_codes, act_scales, ops: Operands, act_scale_dtype=None) -> 
         A = Q.dequantize_nvfp4(act_codes, act_scales, 1.0)
         B = Q.dequantize_nvfp4(ops.w_codes, ops.w_scales, 1.0)
         return A @ B.T
+    if ops.fmt == "w8a8":
+        # acc = sum_k qa qb exactly (int64; fp64 products/sums of |q| <= 127 are exact below 2^53),
+        # then acc * sx[m] * sw[n]
+        acc = np.asarray(act_codes, np.float64) @ np.asarray(ops.w_codes, np.float64).T
+        return acc * np.asarray(act_scales, np.float64)[:, None] * np.asarray(ops.w_scales, np.float64)[None, :]
     sdt = act_scale_dtype or ops.scale_dtype
     acc = int4_group_accum(act_codes, ops.w_codes)
     sx = F.from_bits16(act_scales, sdt).astype(np.float64)        # [M, G]
