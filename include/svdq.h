@@ -60,7 +60,13 @@ typedef enum {
   SVDQ_ERR_WORKSPACE = 8         /* workspace too small                          */
 } svdq_status;
 
-typedef enum { SVDQ_FMT_NVFP4 = 0, SVDQ_FMT_INT4 = 1 } svdq_format;
+/* SVDQ_FMT_W8A8: the paper's 8-bit setting (App. D): per-token dynamic INT8
+ * activations and per-channel INT8 weights, q_max = 127, fp32 scales (one per token / output
+ * channel), Eq. (1); any rank (the paper uses 16).  Codes are int8 bytes [rows][K];
+ * activation scales fp32 [M]; weight scales fp32 [N].  K1 reads each token row twice (the
+ * per-token scale needs the whole row); K2 accumulates the whole K exactly in int32 on
+ * tcgen05 kind::i8 and scales once per tile. */
+typedef enum { SVDQ_FMT_NVFP4 = 0, SVDQ_FMT_INT4 = 1, SVDQ_FMT_W8A8 = 2 } svdq_format;
 typedef enum { SVDQ_BF16 = 0, SVDQ_FP16 = 1, SVDQ_FP32 = 2 } svdq_dtype;
 
 /* Quantized linear layer: non-owning view of caller-owned device buffers. */
@@ -85,8 +91,8 @@ typedef struct svdq_linear {
  * Y = out_rn(fl32(alpha * acc) + bias).                                        */
 
 /* ---------------------------------------------------------------- sizes */
-/* Bytes of K1's outputs for M tokens: xq [M][K/2]; xs (NVFP4: 128x4 layout over
- * ceil(M/128)*128 rows; INT4: [M][K/64] 16-bit); xl1 [M][rank] bf16.             */
+/* Bytes of K1's outputs for M tokens: xq [M][K/2] (W8A8: [M][K]); xs (NVFP4: 128x4 layout
+ * over ceil(M/128)*128 rows; INT4: [M][K/64] 16-bit; W8A8: [M] fp32); xl1 [M][rank] bf16. */
 svdq_status svdq_act_buffer_sizes(int32_t fmt, int64_t M, int64_t K, int32_t rank,
                                   size_t *xq_bytes, size_t *xs_bytes, size_t *xl1_bytes);
 /* Bytes of a layer's weight operands. */

@@ -28,7 +28,7 @@ SVDQ_OK = 0
 STATUS_NAMES = {0: "SVDQ_OK", 1: "SVDQ_ERR_INVALID_ARGUMENT", 2: "SVDQ_ERR_SHAPE", 3: "SVDQ_ERR_RANK",
                 4: "SVDQ_ERR_ALIGNMENT", 5: "SVDQ_ERR_UNSUPPORTED", 6: "SVDQ_ERR_NONFINITE",
                 7: "SVDQ_ERR_CUDA", 8: "SVDQ_ERR_WORKSPACE"}
-FMT = {"nvfp4": 0, "int4": 1}
+FMT = {"nvfp4": 0, "int4": 1, "w8a8": 2}
 DTYPE = {"bf16": 0, "fp16": 1, "fp32": 2}
 TORCH_DTYPE = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}
 DTYPE_OF_TORCH = {torch.bfloat16: "bf16", torch.float16: "fp16", torch.float32: "fp32"}

@@ -62,7 +62,7 @@ int64_t sf_bytes(int64_t rows, int64_t K) { return ((rows + 127) / 128) * 128 * 
 
 svdq_status check_linear(const svdq_linear *L, bool need_weights) {
   if (!L) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null svdq_linear");
-  if (L->fmt != SVDQ_FMT_NVFP4 && L->fmt != SVDQ_FMT_INT4)
+  if (L->fmt != SVDQ_FMT_NVFP4 && L->fmt != SVDQ_FMT_INT4 && L->fmt != SVDQ_FMT_W8A8)
     return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad format %d", L->fmt);
   if (L->K <= 0 || L->K % 64) return fail(SVDQ_ERR_SHAPE, "K=%lld must be a positive multiple of 64", (long long)L->K);
   if (L->N <= 0 || L->N % 16) return fail(SVDQ_ERR_SHAPE, "N=%lld must be a positive multiple of 16", (long long)L->N);
@@ -176,10 +176,17 @@ int32_t svdq_version(void) { return 1; }
 svdq_status svdq_act_buffer_sizes(int32_t fmt, int64_t M, int64_t K, int32_t rank, size_t *xq,
                                   size_t *xs, size_t *xl1) {
   if (!xq || !xs || !xl1) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null output");
-  if (fmt != SVDQ_FMT_NVFP4 && fmt != SVDQ_FMT_INT4) return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad format");
+  if (fmt != SVDQ_FMT_NVFP4 && fmt != SVDQ_FMT_INT4 && fmt != SVDQ_FMT_W8A8)
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad format");
   if (M < 1) return fail(SVDQ_ERR_SHAPE, "M must be >= 1");
   if (K <= 0 || K % 64) return fail(SVDQ_ERR_SHAPE, "K must be a positive multiple of 64");
   if (rank < 0 || rank > 128 || rank % 16) return fail(SVDQ_ERR_RANK, "bad rank");
+  if (fmt == SVDQ_FMT_W8A8) {
+    *xq = static_cast<size_t>(M * K);                                     // int8 codes [M][K]
+    *xs = static_cast<size_t>(M * 4);                                     // fp32 per-token scales [M]
+    *xl1 = static_cast<size_t>(M) * rank * 2;
+    return SVDQ_OK;
+  }
   *xq = static_cast<size_t>(M * K / 2);
   *xs = fmt == SVDQ_FMT_NVFP4 ? static_cast<size_t>(sf_bytes(M, K)) : static_cast<size_t>(M * (K / 64) * 2);
   *xl1 = static_cast<size_t>(M) * rank * 2;
@@ -189,12 +196,15 @@ svdq_status svdq_act_buffer_sizes(int32_t fmt, int64_t M, int64_t K, int32_t ran
 svdq_status svdq_weight_buffer_sizes(int32_t fmt, int64_t K, int64_t N, int32_t rank, size_t *codes,
                                      size_t *scales, size_t *l1s, size_t *l2s) {
   if (!codes || !scales || !l1s || !l2s) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null output");
-  if (fmt != SVDQ_FMT_NVFP4 && fmt != SVDQ_FMT_INT4) return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad format");
+  if (fmt != SVDQ_FMT_NVFP4 && fmt != SVDQ_FMT_INT4 && fmt != SVDQ_FMT_W8A8)
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad format");
   if (K <= 0 || K % 64) return fail(SVDQ_ERR_SHAPE, "K must be a positive multiple of 64");
   if (N <= 0 || N % 16) return fail(SVDQ_ERR_SHAPE, "N must be a positive multiple of 16");
   if (rank < 0 || rank > 128 || rank % 16) return fail(SVDQ_ERR_RANK, "bad rank");
-  *codes = static_cast<size_t>(N * K / 2);
-  *scales = fmt == SVDQ_FMT_NVFP4 ? static_cast<size_t>(sf_bytes(N, K)) : static_cast<size_t>(N * (K / 64) * 2);
+  *codes = static_cast<size_t>(fmt == SVDQ_FMT_W8A8 ? N * K : N * K / 2);
+  *scales = fmt == SVDQ_FMT_NVFP4 ? static_cast<size_t>(sf_bytes(N, K))
+            : fmt == SVDQ_FMT_W8A8 ? static_cast<size_t>(N * 4)
+                                   : static_cast<size_t>(N * (K / 64) * 2);
   *l1s = static_cast<size_t>(rank) * K * 2;
   *l2s = static_cast<size_t>(N) * rank * 2;
   return SVDQ_OK;
@@ -218,7 +228,7 @@ svdq_status prepare_k1(const svdq_linear *L, const void *X, int32_t x_dtype, int
   if ((st = check_device()) != SVDQ_OK) return st;
   K1Params &p = *out;
   p = K1Params{};
-  p.fmt = L->fmt == SVDQ_FMT_NVFP4 ? 0 : 1;
+  p.fmt = L->fmt == SVDQ_FMT_NVFP4 ? 0 : (L->fmt == SVDQ_FMT_W8A8 ? 2 : 1);
   p.x_bf16 = x_dtype == SVDQ_BF16;
   p.scale_bf16 = L->scale_dtype == SVDQ_BF16;
   p.X = X;
@@ -259,10 +269,18 @@ svdq_status svdq_quantize_act_lowrank_down(const svdq_linear *L, const void *X, 
   K1Maps maps;
   svdq_status st = prepare_k1(L, X, x_dtype, M, ldx, xq, xs, xl1, &p, &maps);
   if (st != SVDQ_OK) return st;
-  cudaError_t e = p.x_bf16 ? launch_k1_tc(maps, p, static_cast<cudaStream_t>(stream))
-                           : launch_k1(p, static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "K1 launch");
-  ++g_launches;
+  cudaError_t e = cudaSuccess;
+  if (p.fmt != 2 || p.rank > 0) {      // W8A8: these kernels run the down-projection only
+    e = p.x_bf16 ? launch_k1_tc(maps, p, static_cast<cudaStream_t>(stream))
+                 : launch_k1(p, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "K1 launch");
+    ++g_launches;
+  }
+  if (p.fmt == 2) {                    // per-token INT8 codes + fp32 scales
+    e = launch_k1_int8_rows(p, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "K1 (int8 rows) launch");
+    ++g_launches;
+  }
   return SVDQ_OK;
 }
 
@@ -273,6 +291,8 @@ svdq_status svdq_quantize_act_lowrank_down_grouped(int32_t n, const svdq_linear 
   if (n < 1 || n > kMaxGroup1) return fail(SVDQ_ERR_INVALID_ARGUMENT, "group size must be 1..%d", kMaxGroup1);
   if (!layers || !X || !M || !ldx || !xq || !xs || !xl1) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null array");
   if (x_dtype != SVDQ_BF16) return fail(SVDQ_ERR_UNSUPPORTED, "grouped K1 needs bf16 activations");
+  for (int i = 0; i < n; ++i)
+    if (layers[i] && layers[i]->fmt == SVDQ_FMT_W8A8) return fail(SVDQ_ERR_UNSUPPORTED, "grouped K1: no W8A8");
   K1Args g;
   std::memset(&g, 0, sizeof(g));
   g.n = n;
@@ -336,6 +356,7 @@ svdq_status prepare_k2(const svdq_linear *L, const uint8_t *xq, const uint8_t *x
   p.ldy = ldy;
   p.scale_bf16 = L->scale_dtype == SVDQ_BF16;
   p.alpha = L->fmt == SVDQ_FMT_NVFP4 ? L->gs_x * L->gs_w : 1.0f;
+  p.w8 = L->fmt == SVDQ_FMT_W8A8;
   K2Maps &maps = out->maps;
   std::memset(&maps, 0, sizeof(maps));
   const bool pair = L->fmt == SVDQ_FMT_NVFP4 && (force_pair || use_pair_kernel(M, K));
@@ -357,6 +378,10 @@ svdq_status prepare_k2(const svdq_linear *L, const uint8_t *xq, const uint8_t *x
       if ((st = make_sf_map(&sfa_map, xs, M, K, 1)) != SVDQ_OK) return st;
       if ((st = make_sf_map(&sfb_map, L->w_scales, N, K, 2)) != SVDQ_OK) return st;
     }
+  } else if (L->fmt == SVDQ_FMT_W8A8) {
+    // int8 tiles [rows x 128 B], 128-B swizzle: straight into the kind::i8 operand ring
+    if ((st = make_map(&maps.a, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, M, K, 128, 128)) != SVDQ_OK) return st;
+    if ((st = make_map(&maps.b, L->w_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, BN)) != SVDQ_OK) return st;
   } else {
     // packed int4 tiles [rows x 64 B] (two K groups), dense (no swizzle): unpacked in smem
     if ((st = make_map(&maps.a, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, M, K / 2, 64, 128,
@@ -440,7 +465,8 @@ svdq_status svdq_linear_forward(const svdq_linear *L, const void *X, int32_t x_d
 svdq_status svdq_quantize_residual(const float *R, int64_t K, int64_t N, int32_t fmt, int32_t scale_dtype,
                                    uint8_t *codes, uint8_t *scales, float *gs_w, void *stream) {
   if (!R || !codes || !scales || !gs_w) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null pointer");
-  if (fmt != SVDQ_FMT_NVFP4 && fmt != SVDQ_FMT_INT4) return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad format");
+  if (fmt != SVDQ_FMT_NVFP4 && fmt != SVDQ_FMT_INT4 && fmt != SVDQ_FMT_W8A8)
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad format");
   if (K <= 0 || K % 64) return fail(SVDQ_ERR_SHAPE, "K must be a positive multiple of 64");
   if (N <= 0 || N % 16) return fail(SVDQ_ERR_SHAPE, "N must be a positive multiple of 16");
   if (fmt == SVDQ_FMT_INT4 && scale_dtype != SVDQ_BF16 && scale_dtype != SVDQ_FP16)
@@ -471,7 +497,8 @@ svdq_status svdq_quantize_residual(const float *R, int64_t K, int64_t N, int32_t
   } else {
     *gs_w = 1.0f;
   }
-  SVDQ_CUDA(launch_quantize_residual(R, K, N, fmt == SVDQ_FMT_NVFP4 ? 0 : 1, scale_dtype == SVDQ_BF16,
+  SVDQ_CUDA(launch_quantize_residual(R, K, N, fmt == SVDQ_FMT_NVFP4 ? 0 : (fmt == SVDQ_FMT_W8A8 ? 2 : 1),
+                                     scale_dtype == SVDQ_BF16,
                                      gs, codes, scales, s),
             "quantize residual");
   ++g_launches;
@@ -541,7 +568,7 @@ svdq_status svdq_quantize_weights(const void *W, int32_t w_dtype, const float *l
   if (!W || !lambda || !dst || !ws) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null pointer");
   if (w_dtype != SVDQ_BF16 && w_dtype != SVDQ_FP16 && w_dtype != SVDQ_FP32)
     return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad W dtype");
-  if (fmt != SVDQ_FMT_NVFP4 && fmt != SVDQ_FMT_INT4) return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad format");
+  if (fmt != SVDQ_FMT_NVFP4 && fmt != SVDQ_FMT_INT4 && fmt != SVDQ_FMT_W8A8) return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad format");
   if (K <= 0 || K % 64 || N <= 0 || N % 16) return fail(SVDQ_ERR_SHAPE, "bad K/N");
   if (rank < 0 || rank > 128 || rank % 16 || rank > (K < N ? K : N)) return fail(SVDQ_ERR_RANK, "bad rank");
   if ((L1_opt == nullptr) != (L2_opt == nullptr)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "L1_opt and L2_opt go together");

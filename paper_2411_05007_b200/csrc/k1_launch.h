@@ -45,7 +45,7 @@ inline cudaError_t launch_ex_cluster(Kern kern, dim3 grid, dim3 block, size_t sm
 }
 
 struct K1Params {
-  int fmt;            // 0 NVFP4, 1 INT4
+  int fmt;            // 0 NVFP4, 1 INT4, 2 W8A8 (K1 kernels: down-projection only)
   bool x_bf16;        // X dtype bf16 (else fp16)
   bool scale_bf16;    // INT4 scale dtype bf16 (else fp16)
   const void *X;
@@ -59,6 +59,7 @@ struct K1Params {
   uint16_t *xl1;
 };
 cudaError_t launch_k1(const K1Params &p, cudaStream_t s);       // mma.sync path (fp16 X)
+cudaError_t launch_k1_int8_rows(const K1Params &p, cudaStream_t s);   // W8A8 per-token INT8 codes
 struct K1Maps {
   CUtensorMap x, l1s, lam;    // lam: lambda_inv viewed as [K/32][32] fp32, box {32, 2}, 128-B swizzle
 };
@@ -93,6 +94,7 @@ struct K2Params {
   float alpha;
   int scale_bf16;         // INT4 scales
   int32_t *dbg_acc;       // INT4 debug: per-group int32 accumulators [K/64][M][N]
+  int w8;                 // W8A8 (kind::i8 over the whole K; sfa / sfb are fp32 [M] / [N])
 };
 struct K2Maps {
   CUtensorMap a, b, xl1, l2, y;   // y: output store map, box {64 B of columns, 32 rows}, SW64

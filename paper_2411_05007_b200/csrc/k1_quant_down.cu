@@ -63,7 +63,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
          (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(hi))) << 16);
 }
 
-// kFmt: 0 = NVFP4, 1 = INT4.  kXBf16: X dtype bf16 (else fp16).
+// kFmt: 0 = NVFP4, 1 = INT4, 2 = down-projection only.  kXBf16: X dtype bf16 (else fp16).
 // kScaleBf16: INT4 scale dtype.  MT: 16-row tiles per CTA.  NT: rank / 8.
 template <int kFmt, bool kXBf16, bool kScaleBf16, int MT, int NT>
 __global__ void __launch_bounds__(256, 1)
@@ -157,7 +157,9 @@ __global__ void __launch_bounds__(256, 1)
         }
     }
 
-    // ---------------- smoothing + quantization
+    // ---------------- smoothing + quantization (kFmt 2: down-projection only, W8A8 codes
+    // come from k1_int8_rows)
+    if constexpr (kFmt == 2) continue;
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -308,6 +310,7 @@ static cudaError_t dispatch_mt(const K1Params &p, cudaStream_t s) {
 }
 
 cudaError_t launch_k1(const K1Params &p, cudaStream_t s) {
+  if (p.fmt == 2) return p.x_bf16 ? dispatch_mt<2, true, true>(p, s) : dispatch_mt<2, false, true>(p, s);
   if (p.fmt == 0) {
     return p.x_bf16 ? dispatch_mt<0, true, true>(p, s) : dispatch_mt<0, false, true>(p, s);
   }

@@ -269,6 +269,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t ph = 0;
     for (int i = 0; i < nsteps; ++i, xq_ptr += 4, sf_ptr += 128, ++s16_ptr) {
       mbar_wait(&full[s], ph);                            // suspend (do not hammer the barrier)
+      if constexpr (kFmt == 2) {                         // W8A8: the MMA warp alone uses the tile
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == S) { s = 0; ph ^= 1; }
+        continue;
+      }
       if (qw == 0 && lane == 0) TRACE(66 + i);            // first quantizer sees stage i
       const uint32_t sbase = stage0 + s * Ly.stage_bytes;
       const uint32_t xa = sbase + rl * 128;
@@ -475,6 +481,7 @@ int k1_tc_ksplit(int64_t Mpad, int64_t K) {
 
 cudaError_t launch_k1_tc_group(K1Args &g, cudaStream_t s) {
   const K1Params &p = g.pr[0].p;
+  if (p.fmt == 2) return launch_t<2, true>(g, s);      // W8A8: down-projection only
   if (p.fmt == 0) return launch_t<0, true>(g, s);
   return p.scale_bf16 ? launch_t<1, true>(g, s) : launch_t<1, false>(g, s);
 }

@@ -84,6 +84,10 @@ constexpr int kAcc = 4;                     // TMEM accumulator ring: 4 x 128 co
 // ahead of the promotion, hiding the commit -> tcgen05.ld -> release round trip (~1900 cycles
 // measured; a 2-deep ring was bound at half of that per group).
 static_assert(SMEM <= 227 * 1024, "smem budget");
+// W8A8 operand ring: the two int8 slots plus the packed-int4 region (unused in the 8-bit setting)
+constexpr int kW8Stages = 3;
+static_assert(kPStages >= kW8Stages && kPStages * (PA + PB) >= UA + UB, "W8A8 third stage fits the packed region");
+__host__ __device__ constexpr int w8_stage(int s) { return s < kUStages ? OFF_U + s * (UA + UB) : OFF_P; }
 
 __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
@@ -176,7 +180,10 @@ __device__ __forceinline__ float load_bias(const void *b, int dt, int64_t i) {
   return static_cast<const float *>(b)[i];
 }
 
-template <bool kDbg>
+// kW8: the 8-bit setting (SVDQ_FMT_W8A8): int8 codes arrive by TMA straight into the
+// int8 ring (no unpack), the whole K accumulates in one exact int32 TMEM slot per tile, and the
+// epilogue applies the per-token / per-channel scales once: fl32(fl32(f32(acc) * sx[m]) * sw[n]).
+template <bool kDbg, bool kW8 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k2_int4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmL,
@@ -198,8 +205,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   constexpr bool dbg = kDbg;                           // debug: store the int32 group sums
-  const int G = static_cast<int>(p.K / 64);            // K groups
-  const int nst = (G + 1) / 2;                          // pipeline steps (2 groups each)
+  const int G = kW8 ? 1 : static_cast<int>(p.K / 64);  // K groups (W8A8: one, the whole K)
+  const int nst = static_cast<int>((p.K / 64 + 1) / 2);   // pipeline steps (128 K elements each)
   const int nslab = dbg ? 0 : (p.rank + 63) / 64;
   const int mt_count = static_cast<int>((p.M + BM - 1) / BM);
   const int tiles = mt_count * static_cast<int>((p.N + BN - 1) / BN);
@@ -207,10 +214,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kPStages; ++s) {
       mbar_init(&p_full[s], 1);
-      mbar_init(&p_empty[s], kUnpackWarps);
+      mbar_init(&p_empty[s], kW8 ? 1 : kUnpackWarps);   // W8A8: the int8 ring's barriers
     }
     for (int s = 0; s < kUStages; ++s) {
-      mbar_init(&u_full[s], kUnpackWarps);
+      mbar_init(&u_full[s], kW8 ? 1 : kUnpackWarps);   // W8A8: the producer's TMA fills it
       mbar_init(&u_empty[s], 1);
     }
     for (int b = 0; b < kAcc; ++b) {
@@ -248,6 +255,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         for (int k = 0; k < nst; ++k) {
+          if constexpr (kW8) {                        // int8 tiles [128 rows x 128 B], SW128
+            mbar_wait(&p_empty[ps], pph ^ 1);           // 3-deep ring: the two int8 slots + the
+            uint8_t *st = smem + w8_stage(ps);          // (unused) packed region
+            mbar_arrive_expect_tx(&p_full[ps], UA + UB);
+            tma_load_2d(st, &tmA, &p_full[ps], k * 128, static_cast<int32_t>(m0));
+            tma_load_2d(st + UA, &tmB, &p_full[ps], k * 128, static_cast<int32_t>(n0));
+            if (++ps == kW8Stages) { ps = 0; pph ^= 1; }
+            continue;
+          }
           mbar_wait(&p_empty[ps], pph ^ 1);
           uint8_t *st = smem + OFF_P + ps * (PA + PB);
           mbar_arrive_expect_tx(&p_full[ps], PA + PB);
@@ -290,6 +306,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         ++gi;
       }
+      if constexpr (kW8) {
+        // one exact int32 accumulation over the whole K into a single ring slot
+        const int b = gi % kAcc;
+        SVDQ_I4_WAIT(&g_empty[b], ((gi / kAcc) & 1) ^ 1);
+        tc_fence_after();
+        for (int k = 0; k < nst; ++k) {
+          mbar_wait(&p_full[us], uph);
+          tc_fence_after();
+          const uint32_t ua = smem_u32(smem + w8_stage(us));
+          const uint32_t ub = ua + UA;
+          if (elect_one()) {
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+              mma_s8(tmem + b * BN, sdesc_kmajor_sw128(ua + 32 * h), sdesc_kmajor_sw128(ub + 32 * h), idesc_i,
+                     (k | h) != 0);
+            tc_commit(&p_empty[us]);
+          }
+          __syncwarp();
+          if (++us == kW8Stages) { us = 0; uph ^= 1; }
+        }
+        if (elect_one()) tc_commit(&g_full[b]);
+        __syncwarp();
+        ++gi;
+        continue;
+      }
       for (int k = 0; k < nst; ++k) {
         { I4T_BEGIN(); mbar_wait(&u_full[us], uph); I4T_ACC(t_uf); }
         tc_fence_after();
@@ -320,6 +361,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 #endif
   } else if (warp < 2 + kUnpackWarps) {
+    if constexpr (kW8) {
+      // no unpacking in the 8-bit setting
+    } else {
     // ---------------------------------------------------------------- unpackers
     const int ut0 = threadIdx.x - 64;        // 16-byte packed chunk q = ut0 + 64 i of A and of B
     int ps = 0, us = 0;
@@ -354,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       g_i4_trace[blockIdx.x][3] = t_pf; g_i4_trace[blockIdx.x][4] = t_ue; g_i4_trace[blockIdx.x][5] = clock64() - t_st;
     }
 #endif
+    }
   } else {
     // ---------------------------------------------------------------- epilogue
     const int ew = warp - 2 - kUnpackWarps;     // 0..15
@@ -412,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto h2f = [&](uint32_t bits16) {
         return sbf ? __uint_as_float(bits16 << 16) : __half2float(__ushort_as_half(static_cast<uint16_t>(bits16)));
       };
-      fetch(0);
+      if constexpr (!kW8) fetch(0);
       sts_f32(smem_u32(bst) + lane * 4, (!dbg && p.bias && cvalid) ? load_bias(p.bias, p.bias_dtype, c0 + lane) : 0.f);
       if (nslab) {                               // low-rank pseudo-group: facc starts at X L1 . L2
         const int b = gi % kAcc;
@@ -433,7 +478,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const uint32_t swb = smem_u32(swst);       // [g][column] sw, then [g][lane] sx
       const uint32_t sxb = swb + kGB * EC * 4;
-      for (int blk = 0; blk < nblk; ++blk) {
+      if constexpr (kW8) {
+        // one int32 accumulator per tile: facc += fl32(f32(acc) * sx[m]) * sw[n]
+        const float sxv = rvalid ? reinterpret_cast<const float *>(p.sfa)[grow] : 0.f;
+        __syncwarp();
+        sts_f32(swb + lane * 4, cvalid ? reinterpret_cast<const float *>(p.sfb)[c0 + lane] : 0.f);
+        __syncwarp();
+        const int b = gi % kAcc;
+        SVDQ_I4_WAIT(&g_full[b], (gi / kAcc) & 1);
+        tc_fence_after();
+        const uint64_t sx2 = f2pack(sxv, sxv);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(tmem + b * BN + lane_off + slice * EC + hh * 16, r);
+          tmem_ld_wait();
+          if (hh == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&g_empty[b]);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 w4 = lds_f32x4(swb + (hh * 16 + 4 * q) * 4);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int e = 4 * q + 2 * h;
+              // |acc| may exceed 2^24 over a whole K: correctly rounded int -> fp32 conversion
+              const uint64_t a2 = f2pack(__int2float_rn(static_cast<int>(r[e])),
+                                         __int2float_rn(static_cast<int>(r[e + 1])));
+              const uint64_t t2 = mul2(a2, sx2);
+              const int fi = hh * 8 + e / 2;
+              facc[fi] = fma2(t2, h ? f2pack(w4.z, w4.w) : f2pack(w4.x, w4.y), facc[fi]);
+            }
+          }
+        }
+        ++gi;
+      }
+      for (int blk = 0; blk < (kW8 ? 0 : nblk); ++blk) {
         __syncwarp();                            // previous block's reads are done
 #pragma unroll
         for (int j = 0; j < kGB / 2; ++j) {
@@ -548,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace
 
 cudaError_t launch_k2_int4(const K2Maps &maps, const K2Params &p, cudaStream_t s) {
-  auto kern = p.dbg_acc ? k2_int4_kernel<true> : k2_int4_kernel<false>;
+  auto kern = p.dbg_acc ? k2_int4_kernel<true> : (p.w8 ? k2_int4_kernel<false, true> : k2_int4_kernel<false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   if (e != cudaSuccess) return e;
   if (p.rank > kMaxSlabs * 64 && !p.dbg_acc) return cudaErrorInvalidValue;

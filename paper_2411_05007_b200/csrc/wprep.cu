@@ -108,6 +108,34 @@ __global__ void quant_res_int4_kernel(const float *__restrict__ R, int64_t K, in
   }
 }
 
+// One thread per output channel n: the per-channel INT8 recipe of the 8-bit setting:
+// amax over K, s = fl32(amax / 127), qinv = s == 0 ? 0 : fl32(1 / s),
+// q = clamp(rne(fl32(r * qinv)), -127, 127).  R is [K][N]: threads n read coalesced rows of R.
+__global__ void quant_res_int8_kernel(const float *__restrict__ R, int64_t K, int64_t N, int8_t *__restrict__ codes,
+                                      float *__restrict__ scales) {
+  const int64_t n = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  float amax = 0.f;
+  for (int64_t k = 0; k < K; ++k) amax = fmaxf(amax, fabsf(R[k * N + n]));
+  const float sc = __fdiv_rn(amax, 127.0f);
+  const float qinv = sc == 0.f ? 0.f : __fdiv_rn(1.0f, sc);
+  scales[n] = sc;
+  for (int64_t k = 0; k < K; k += 16) {
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int v = max(-127, min(127, __float2int_rn(__fmul_rn(R[(k + 4 * j + b) * N + n], qinv))));
+        word |= (static_cast<uint32_t>(v) & 0xFFu) << (8 * b);
+      }
+      w[j] = word;
+    }
+    *reinterpret_cast<uint4 *>(codes + n * K + k) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
 __global__ void codec_kernel(const float *__restrict__ in, uint8_t *__restrict__ out, int64_t n,
                              int kind) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -210,6 +238,9 @@ cudaError_t launch_quantize_residual(const float *R, int64_t K, int64_t N, int f
   if (fmt == 0) {
     const int64_t work = ((N + 127) / 128) * 128 * (K / 16);
     quant_res_nvfp4_kernel<<<blocks_for(work, 256), 256, 0, s>>>(R, K, N, gs_w, codes, scales);
+  } else if (fmt == 2) {
+    quant_res_int8_kernel<<<blocks_for(N, 128), 128, 0, s>>>(R, K, N, reinterpret_cast<int8_t *>(codes),
+                                                            reinterpret_cast<float *>(scales));
   } else {
     const int64_t work = N * (K / 64);
     if (scale_bf16)

@@ -20,6 +20,9 @@ def need_cuda():
 def pack_weight(ops):
     if ops.fmt == "nvfp4":
         return F.pack_nibbles(ops.w_codes), F.sf_to_layout(ops.w_scales, ops.K)
+    if ops.fmt == "w8a8":                       # int8 bytes [N][K], fp32 scales [N]
+        return (np.ascontiguousarray(ops.w_codes.astype(np.int8)).view(np.uint8),
+                np.ascontiguousarray(ops.w_scales.astype(np.float32)).view(np.uint8).reshape(-1))
     return (F.pack_nibbles(F.int4_to_nibble(ops.w_codes)),
             np.ascontiguousarray(ops.w_scales).view(np.uint8).reshape(-1))
 
@@ -28,6 +31,9 @@ def pack_act(fmt, qa, K):
     """(xq bytes [M, K/2], xs bytes flat) of an oracle QuantAct."""
     if fmt == "nvfp4":
         return F.pack_nibbles(qa.codes), F.sf_to_layout(qa.scales, K)
+    if fmt == "w8a8":
+        return (np.ascontiguousarray(qa.codes.astype(np.int8)).view(np.uint8),
+                np.ascontiguousarray(qa.scales.astype(np.float32)).view(np.uint8).reshape(-1))
     return (F.pack_nibbles(F.int4_to_nibble(qa.codes)),
             np.ascontiguousarray(qa.scales).view(np.uint8).reshape(-1))
 

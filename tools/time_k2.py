@@ -11,7 +11,10 @@ fmt = os.environ.get("SVDQ_FMT", "nvfp4")
 layer = P.QuantizedLinear.empty(fmt, K, N, 32, device=dev)
 g = torch.Generator(device=dev).manual_seed(0)
 layer.w_codes.random_(0, 256, generator=g)
-layer.w_scales.fill_(0x30 if fmt == "nvfp4" else 0x3c)
+if fmt == "w8a8":
+    layer.w_scales.view(torch.float32).fill_(0.01)
+else:
+    layer.w_scales.fill_(0x30 if fmt == "nvfp4" else 0x3c)
 layer.l1s.zero_(); layer.l2s.zero_(); layer.lambda_inv.fill_(1.0)
 layer.gs_w = 1.0
 layer._sync_view()
