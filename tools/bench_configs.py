@@ -34,6 +34,8 @@ def random_layer(fmt, K, N, r, dt, gen):
     if fmt == "nvfp4":
         L.w_scales.random_(0x30, 0x40, generator=gen)
         L.gs_w = 0.01
+    elif fmt == "w8a8":
+        L.w_scales.view(torch.float32).copy_(torch.rand(N, device=dev, generator=gen) * 0.01 + 0.005)
     else:
         s = (torch.rand(L.w_scales.numel() // 2, device=dev, generator=gen) * 0.01 + 0.005).to(TD[dt])
         L.w_scales.copy_(s.view(torch.uint8))
@@ -131,18 +133,18 @@ def main():
            "configs": {}}
     cfgs = {"C2_pixart_sigma": synth.C2, "C3_sdxl_lora": synth.C3, "C4_flux": synth.C4}
     for cname, layers in cfgs.items():
-        for fmt in ("nvfp4", "int4"):
-            items = make_items(layers, fmt, gen)
+        for fmt in ("nvfp4", "int4", "w8a8"):
+            items = make_items(layers, fmt, gen, rank_override=16 if fmt == "w8a8" else None)
             t, _ = time_layers(items, a.reps, stream, flush)
             items0 = make_items(layers, fmt, gen, rank_override=0)
             t0, _ = time_layers(items0, a.reps, stream, flush)
             rows = {}
             for j, Ly in enumerate(layers):
-                M, K, N, r = Ly.M, Ly.K, Ly.N, Ly.r + Ly.lora
+                M, K, N, r = Ly.M, Ly.K, Ly.N, (16 if fmt == "w8a8" else Ly.r + Ly.lora)
                 k1, k2 = t[j]
                 k1z, k2z = t0[j]
                 fl = 2.0 * M * N * K
-                cb = 0.5625 if fmt == "nvfp4" else 0.53125
+                cb = {"nvfp4": 0.5625, "int4": 0.53125, "w8a8": 1.0}[fmt]
                 k2_bytes = cb * (M + N) * K + 2 * (M + N) * r + 2 * N + 2 * M * N
                 k1_bytes = 2 * M * K + cb * M * K + 2 * M * r
                 rows[Ly.name] = {
