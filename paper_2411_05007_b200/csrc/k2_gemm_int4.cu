@@ -412,7 +412,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     float *swst = reinterpret_cast<float *>(smem + OFF_SW + ew * SWST);   // [2][kGB][EC]
     float *bst = swst + 2 * kGB * EC;                                     // [EC]
     const int nblk = (G + kGB - 1) / kGB;
-    const uint64_t magic2 = f2pack(-12582912.0f, -12582912.0f);
     int gi = 0;
     int it = 0;
 #ifdef SVDQ_TRACE
@@ -535,6 +534,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const float sxv = lds_f32(sxb + (j * EC + lane) * 4);
           const uint64_t sx2 = f2pack(sxv, sxv);
+          const float bsx = __fmul_rn(sxv, -12582912.0f);
+          const uint64_t bsx2 = f2pack(bsx, bsx);
           const uint32_t swg = swb + j * EC * 4;
 #pragma unroll
 #pragma unroll
@@ -567,11 +568,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int e = 4 * q + 2 * h;
-                // exact int32 -> fp32 (|acc| <= 64*49 < 2^22): magic-number add, then subtract
-                // (measured: I2FP.F32.S32 is ~4 % slower than this magic-number conversion)
-                const uint64_t a2 = add2(f2pack(__int_as_float(static_cast<int>(r[e]) + 0x4B400000),
-                                                __int_as_float(static_cast<int>(r[e + 1]) + 0x4B400000)), magic2);
-                const uint64_t t2 = mul2(a2, sx2);                       // fl32(acc * sx)
+                // fl32(acc * sx) in one FMA: the magic-number float m = 1.5 * 2^23 + acc is exact
+                // (|acc| <= 64*49 < 2^22), bsx = fl32(-1.5 * 2^23 * sx) is exact (sx has 11
+                // significant bits), so fma(m, sx, bsx) = fl32((m - 1.5 * 2^23) * sx) = fl32(acc * sx)
+                const uint64_t a2 = f2pack(__int_as_float(static_cast<int>(r[e]) + 0x4B400000),
+                                           __int_as_float(static_cast<int>(r[e + 1]) + 0x4B400000));
+                const uint64_t t2 = fma2(a2, sx2, bsx2);
                 const int fi = hh * 8 + e / 2;
                 facc[fi] = fma2(t2, h ? f2pack(w4.z, w4.w) : f2pack(w4.x, w4.y), facc[fi]);   // + . * sw
               }
