@@ -43,7 +43,7 @@ def bench_config(args, world):
     """The workload description shared by both arms (svdq and --impl reference)."""
     return {"workload": "flux1-dev block linears: 1 double block (img 4096 tok + txt 512 tok: "
                         "qkv, proj, mlp_up, mlp_down) + 1 single block (4608 tok: linear1, linear2)",
-            "batch": args.batch, "hidden": 3072, "mlp": 12288, "rank": 32, "format": args.fmt,
+            "batch": args.batch, "hidden": 3072, "mlp": 12288, "rank": 16 if args.fmt == "w8a8" else 32, "format": args.fmt,
             "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
             "l2": "flushed between steps outside the per-step events (512 MiB write, then a 256 MiB read "
                   "so the flush's dirty lines are written back before the step starts)"}
@@ -154,11 +154,14 @@ def run_svdq(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     layers = flux_block_layers(args.batch)
+    if args.fmt == "w8a8":                      # the paper's 8-bit setting uses rank 16
+        import dataclasses
+        layers = [dataclasses.replace(L, r=16) for L in layers]
     quality = {}
     built = build_layers(P, torch, layers, args.fmt, dev, quality)
     flops = sum(2.0 * L.M * L.N * L.K for L in layers)
-    k1_bytes = sum(L.M * L.K * 2 + L.M * L.K * (0.5625 if args.fmt == "nvfp4" else 0.53125)
-                   + L.M * L.r * 2 for L in layers)
+    cbytes = {"nvfp4": 0.5625, "int4": 0.53125, "w8a8": 1.0}[args.fmt]
+    k1_bytes = sum(L.M * L.K * (2 + cbytes) + L.M * L.r * 2 for L in layers)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     flush_sink = torch.empty((), dtype=torch.int64, device=dev)
     stream = torch.cuda.Stream(device=dev)
@@ -505,8 +508,10 @@ def run_svdq(args, rank, world, local_rank):
     if rank != 0:
         return None
     pk, pk_kind = peaks()
-    fp4_sus = 4.0 * pk.get("bf16_tflops_sustained", pk["bf16_tflops"])     # guide: fp4 = 4 x bf16 nominal
-    fp4_burst = 4.0 * pk["bf16_tflops"]
+    # guide nominal ratios: fp4 = 4 x bf16 (9 : 2.25 PF), int8 / fp8 = 2 x bf16 (4.5 : 2.25)
+    ratio = 4.0 if args.fmt == "nvfp4" else 2.0
+    fp4_sus = ratio * pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    fp4_burst = ratio * pk["bf16_tflops"]
     k2_flops = np.array([2.0 * L.M * L.N * L.K for L in layers])
     k2_t = launch_k2_s.sum() if launch_k2_s is not None else k2_avg_s.sum()
     k1_t = launch_k1_s.sum() if launch_k1_s is not None else k1_avg_s.sum()
@@ -524,7 +529,7 @@ def run_svdq(args, rank, world, local_rank):
                           "k1_us": round(float(k1_avg_s[j] * 1e6), 2),
                           "k2_us": round(float(k2_avg_s[j] * 1e6), 2),
                           "k2_tflops": round(float(k2_flops[j] / k2_avg_s[j] / 1e12), 1),
-                          "k1_gbs": round(float((L.M * L.K * (2.5625 if args.fmt == "nvfp4" else 2.53125)
+                          "k1_gbs": round(float((L.M * L.K * (2 + cbytes)
                                                  + 2 * L.M * L.r) / k1_avg_s[j] / 1e9), 1)}
                  for j, L in enumerate(layers)}
     traffic = None
@@ -539,17 +544,23 @@ def run_svdq(args, rank, world, local_rank):
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "e2m1 x e2m1 -> f32 (NVFP4 g16 e4m3 scales) + bf16 low-rank"
-        if args.fmt == "nvfp4" else "int4 x int4 -> int32 (kind::i8) -> f32 (g64 16-bit scales) + bf16 low-rank",
+        "vs_baseline": None, "dtype": {
+            "nvfp4": "e2m1 x e2m1 -> f32 (NVFP4 g16 e4m3 scales) + bf16 low-rank",
+            "int4": "int4 x int4 -> int32 (kind::i8) -> f32 (g64 16-bit scales) + bf16 low-rank",
+            "w8a8": "int8 x int8 -> int32 (kind::i8, per-token / per-channel fp32 scales) + bf16 low-rank r16"}[args.fmt],
         "data": "synthetic (seeded; DESIGN.md input recipe), weights prepared on GPU by svdq_quantize_weights",
         "config": cfg,
         "roofline": {"bound": "tensor", "achieved": round(k2_achieved, 1), "peak": round(fp4_sus, 1),
                      "unit": "TFLOP/s", "frac": round(k2_achieved / fp4_sus, 4), "traffic": traffic,
-                     "kernel": "svdq_gemm_w4a4_lowrank_up (K2, NVFP4)",
-                     "peak_source": f"4 x {pk_kind} sustained bf16 (MEASURED_PEAKS.json), guide fp4:bf16 = 9:2.25",
+                     "kernel": f"svdq_gemm_w4a4_lowrank_up (K2, {args.fmt.upper()})",
+                     "peak_source": (f"4 x {pk_kind} sustained bf16 (MEASURED_PEAKS.json), guide fp4:bf16 = 9:2.25"
+                                     if args.fmt == "nvfp4" else
+                                     f"2 x {pk_kind} sustained bf16 (MEASURED_PEAKS.json): the kind::i8 dense "
+                                     "rate, guide int8:bf16 = 4.5:2.25"),
                      "frac_vs_burst": round(k2_achieved / fp4_burst, 4),
-                     "frac_vs_clock_peak": round(k2_achieved * 1e12 / (148 * 32768 * f_sm), 4),
-                     "clock_peak_def": "148 SMs x 32768 dense FP4 FLOP/clk x median SM clock of the timed region",
+                     "frac_vs_clock_peak": round(k2_achieved * 1e12 / (148 * 8192 * ratio * f_sm), 4),
+                     "clock_peak_def": f"148 SMs x {int(8192 * ratio)} dense FLOP/clk ({args.fmt}) x median SM clock "
+                                       "of the timed region",
                      "achieved_def": "sum 2*M*N*K over the step's linears / sum of the step's K2 launch durations "
                                      "(CUDA events around each launch of the step's own launch sequence)"},
         "k1": {"bound": "hbm", "achieved": round(k1_gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -665,7 +676,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="svdq", choices=["svdq", "reference"])
-    ap.add_argument("--fmt", default="nvfp4", choices=["nvfp4", "int4"])
+    ap.add_argument("--fmt", default="nvfp4", choices=["nvfp4", "int4", "w8a8"])
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--ref-rows", type=int, default=32)
     ap.add_argument("--cpu-rows", type=int, default=64)
