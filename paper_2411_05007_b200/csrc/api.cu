@@ -369,9 +369,16 @@ svdq_status prepare_k2(const svdq_linear *L, const uint8_t *xq, const uint8_t *x
                                     : y_dtype == SVDQ_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                                            : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const int64_t ysz = y_dtype == SVDQ_FP32 ? 4 : 2;
-    if ((st = make_map(&maps.y, Y, ydt, N, M, ldy * ysz, static_cast<uint32_t>(64 / ysz), 32,
-                       CU_TENSOR_MAP_SWIZZLE_64B)) != SVDQ_OK)
+#ifndef SVDQ_BIGSTORE
+#define SVDQ_BIGSTORE 0
+#endif
+    if (SVDQ_BIGSTORE && pair && y_dtype != SVDQ_FP32) {      // [128 rows x 64 cols] SW128 blocks
+      if ((st = make_map(&maps.y, Y, ydt, N, M, ldy * ysz, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != SVDQ_OK)
+        return st;
+    } else if ((st = make_map(&maps.y, Y, ydt, N, M, ldy * ysz, static_cast<uint32_t>(64 / ysz), 32,
+                              CU_TENSOR_MAP_SWIZZLE_64B)) != SVDQ_OK) {
       return st;
+    }
     if ((st = make_map(&maps.a, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, M, K / 2, 128, 128)) != SVDQ_OK) return st;
     if ((st = make_map(&maps.b, L->w_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, N, K / 2, 128, b_rows)) != SVDQ_OK) return st;
     if (pair) {

@@ -60,8 +60,14 @@ constexpr int kStages = SVDQ_K2P_STAGES;
 constexpr int kEpiBuf = SVDQ_K2P_EPIBUF;      // 2 KB staging buffers per epilogue warp
 constexpr int SF_COLS = 48;
 constexpr int SF_BASE = 2 * BN;
-constexpr int EPI_OFF = kStages * STAGE;                 // 4 epilogue warps x two 4 KB staging buffers
-constexpr int BAR_OFF = EPI_OFF + 8 * 2048 * kEpiBuf;
+#ifndef SVDQ_BIGSTORE
+#define SVDQ_BIGSTORE 0
+#endif
+constexpr int EPI_OFF = kStages * STAGE;                 // epilogue staging
+// 16-bit Y with SVDQ_BIGSTORE: three [128 rows x 64 cols] SW128 blocks, one TMA store each;
+// otherwise (and for fp32 Y) 8 warps x kEpiBuf 2 KB chunks
+constexpr int EPI_BYTES = SVDQ_BIGSTORE && 3 * 16384 > 8 * 2048 * kEpiBuf ? 3 * 16384 : 8 * 2048 * kEpiBuf;
+constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
 constexpr int SMEM = BAR_OFF + 256 + BN * 4 + 1024;
 static_assert(STAGE % 1024 == 0, "stage alignment");
 static_assert(SF_BASE + 2 * SF_COLS <= 512, "TMEM budget");
@@ -381,6 +387,46 @@ __global__ void __launch_bounds__(320, 1)
                                     if (lane == 0) mbar_arrive_cluster(acc_empty0 + b * 8);
                                   });
       continue;
+#endif
+#if SVDQ_BIGSTORE
+      if (p.y_dtype != 2) {
+        // drain the 3 column chunks of this warp, release the accumulator, then each 64-column
+        // block of the CTA's 128 x 192 tile is assembled by all 8 warps and stored by one TMA op
+        const int sub = (warp - 2) >> 2;
+        const uint32_t lane_addr = tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16);
+        uint32_t r[3][32];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) tmem_ld_32x32b_x32(lane_addr + (sub + 2 * i) * 32, r[i]);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(acc_empty0 + b * 8);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          uint8_t *blk = smem + EPI_OFF + i * 16384;
+          if (et == 0) bulk_wait_group_read<2>();        // this block's previous store has read it
+          named_bar(2, 256);
+          const float *bs = bias_s + (sub + 2 * i) * 32;
+          uint8_t *rowp = blk + row * 128;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float o[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = __fadd_rn(__fmul_rn(p.alpha, __uint_as_float(r[i][8 * c + e])), bs[8 * c + e]);
+            const int j = 4 * sub + c;                     // 16-byte column of the 128-byte row
+            *reinterpret_cast<uint4 *>(rowp + ((j ^ (row & 7)) * 16)) =
+                make_uint4(pack2(o[0], o[1], p.y_dtype), pack2(o[2], o[3], p.y_dtype), pack2(o[4], o[5], p.y_dtype),
+                           pack2(o[6], o[7], p.y_dtype));
+          }
+          fence_proxy_async();
+          named_bar(3, 256);
+          if (et == 0) {
+            tma_store_2d(tmY, blk, static_cast<int32_t>(n0 + 64 * i), static_cast<int32_t>(m0));
+            bulk_commit_group();
+          }
+        }
+        continue;
+      }
 #endif
       epilogue_tile<BN, 2, kEpiBuf>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
                            tmY, static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
