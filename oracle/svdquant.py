@@ -305,3 +305,33 @@ def lowrank_branch_exact(x, L1s, L2s, alpha) -> np.ndarray:
     """alpha * X L1s^T L2s^T in fp64 (no storage rounding)."""
     return float(alpha) * (np.asarray(x, np.float64) @ np.asarray(L1s, np.float64).T
                            @ np.asarray(L2s, np.float64).T)
+
+
+# --------------------------------------------------------------------------
+# Offline: migration-strength search (App. D, P:467) -- SURVEY 8(f) row 4
+# --------------------------------------------------------------------------
+def calibration_error(x_cal, w, ops: Operands) -> float:
+    """||X_cal W - forward(X_cal)||_F^2 with the deployed quantized forward (Eq. 5 with the
+    residual and activation quantizers, fp64 before output rounding, no bias) -- "the layer
+    output mean squared error (MSE) after SVD on the calibration dataset" (reading Q4)."""
+    ops_nb = replace(ops, bias=None)
+    qa = quantize_activation(x_cal, ops_nb)
+    y = gemm_reference(qa, ops_nb)
+    ref = np.asarray(x_cal, np.float64) @ np.asarray(w, np.float64)
+    return float(np.sum((y - ref) ** 2))
+
+
+def search_alpha(x_cal, w, rank: int, fmt: str, grid, gs_x=1.0, scale_dtype="bf16"):
+    """argmin over the grid of calibration_error(lambda(alpha)); ties -> the smaller alpha.
+    Returns (alpha*, lambda32(alpha*), [objective per grid point])."""
+    grid = list(grid)
+    if not grid:
+        raise ValueError("empty alpha grid")
+    errs = []
+    for a in grid:
+        lam = compute_smoothing(x_cal, w, a)
+        ops = prepare_operands(w, lam, rank, fmt, gs_x=gs_x, scale_dtype=scale_dtype)
+        errs.append(calibration_error(x_cal, w, ops))
+    best = min(range(len(grid)), key=lambda i: (errs[i], grid[i]))
+    return grid[best], compute_smoothing(x_cal, w, grid[best]), errs
+
