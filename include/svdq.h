@@ -182,6 +182,22 @@ svdq_status svdq_quantize_weights(const void *W, int32_t w_dtype, const float *l
                                   float gs_x, const float *L1_opt, const float *L2_opt,
                                   svdq_linear *dst, void *ws, size_t ws_bytes, void *stream);
 
+/* Offline migration-strength search (App. D).  For each alpha in
+ * grid ([host], n_grid values in [0, 1]): lambda_k = clamp(max|X_cal[:,k]|^alpha /
+ * max|W[k,:]|^(1-alpha), 1e-5, 1e5) (fp64, non-finite -> 1e5, stored fp32), the full weight
+ * preparation of svdq_quantize_weights, the deployed K1 -> K2 forward on X_cal without bias, and
+ * the objective ||X_cal W - Y||_F^2 (fp64 sum, reference X_cal W in fp32 cuBLAS).
+ * Returns alpha* = argmin (ties -> the smaller alpha) in *alpha_out [host], lambda(alpha*) in
+ * lambda_out [dev, K] fp32 and every objective in objective_out [host, n_grid].
+ * X_cal: [dev] [M_cal][ldx] BF16 | FP16.  W: [dev] [K][N] fp32.  ws: [dev] of
+ * svdq_search_alpha_workspace bytes.  Synchronizes `stream`.                              */
+svdq_status svdq_search_alpha_workspace(int32_t fmt, int64_t M_cal, int64_t K, int64_t N, int32_t rank,
+                                        size_t *ws_bytes);
+svdq_status svdq_search_alpha(const void *X_cal, int32_t x_dtype, int64_t M_cal, int64_t ldx, const float *W,
+                              int64_t K, int64_t N, int32_t rank, int32_t fmt, int32_t scale_dtype, float gs_x,
+                              const float *grid, int32_t n_grid, float *alpha_out, float *lambda_out,
+                              double *objective_out, void *ws, size_t ws_bytes, void *stream);
+
 /* LoRA fusion: dst->l1s = [src->l1s ; bf16(fl32(scale*A))^T] ([r+r_l][K]),
  * dst->l2s = [src->l2s | bf16(fl32(B/alpha))^T] ([N][r+r_l]); codes / scales untouched
  * (no re-quantization).  A: [dev] [K][r_l], B: [dev] [r_l][N] of ab_dtype

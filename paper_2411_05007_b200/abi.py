@@ -40,6 +40,7 @@ EXPORTS = [
     "svdq_gemm_w4a4_lowrank_up", "svdq_gemm_w4a4_lowrank_up_grouped", "svdq_linear_forward",
     "svdq_quantize_residual",
     "svdq_quantize_weights_workspace", "svdq_quantize_weights", "svdq_lora_fuse",
+    "svdq_search_alpha_workspace", "svdq_search_alpha",
     "svdq_debug_int4_group_accum", "svdq_debug_codec", "svdq_status_string", "svdq_last_error",
     "svdq_launch_count", "svdq_version",
 ]
@@ -82,6 +83,9 @@ _sig = {
     "svdq_quantize_weights": [_P, _I32, _P, _I64, _I64, _I32, _I32, _I32, C.c_float, _P, _P, _LP,
                               _P, C.c_size_t, _P],
     "svdq_lora_fuse": [_LP, _P, _P, _I32, _I32, C.c_float, _LP, _P],
+    "svdq_search_alpha_workspace": [_I32, _I64, _I64, _I64, _I32, _SZ],
+    "svdq_search_alpha": [_P, _I32, _I64, _I64, _P, _I64, _I64, _I32, _I32, _I32, C.c_float, C.POINTER(C.c_float),
+                          _I32, C.POINTER(C.c_float), _P, C.POINTER(C.c_double), _P, C.c_size_t, _P],
     "svdq_debug_int4_group_accum": [_P, _P, _I64, _I64, _I64, _P, _P],
     "svdq_debug_codec": [_P, _P, _I64, _I32, _P],
 }
@@ -331,6 +335,32 @@ def svdq_lora_fuse(layer: QuantizedLinear, A, B, scale: float = 1.0, stream=None
 
 
 # ---------------------------------------------------------------- test hooks
+def svdq_search_alpha_workspace(fmt: str, M_cal: int, K: int, N: int, rank: int) -> int:
+    wsb = C.c_size_t()
+    _check(_lib.svdq_search_alpha_workspace(FMT[fmt], M_cal, K, N, rank, C.byref(wsb)), "svdq_search_alpha_workspace")
+    return wsb.value
+
+
+def svdq_search_alpha(X_cal, W, rank: int, fmt: str, grid, scale_dtype: str = "bf16", gs_x: float = 1.0,
+                      stream=None):
+    """Offline migration-strength search (App. D) on the GPU.  X_cal: [M_cal, K] bf16/fp16,
+    W: [K, N] fp32 (CUDA).  Returns (alpha*, lambda(alpha*) [K] fp32 tensor, objectives list)."""
+    M, K = X_cal.shape
+    N = W.shape[1]
+    wsb = svdq_search_alpha_workspace(fmt, M, K, N, rank)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=X_cal.device)
+    lam = torch.empty(K, dtype=torch.float32, device=X_cal.device)
+    n = len(grid)
+    g = (C.c_float * n)(*grid)
+    obj = (C.c_double * n)()
+    a = C.c_float()
+    Wc = W.contiguous().float()
+    _check(_lib.svdq_search_alpha(_ptr(X_cal), DTYPE[DTYPE_OF_TORCH[X_cal.dtype]], M, X_cal.stride(0), _ptr(Wc), K, N,
+                                  rank, FMT[fmt], DTYPE[scale_dtype], gs_x, g, n, C.byref(a), _ptr(lam), obj,
+                                  _ptr(ws), wsb, _stream(stream)), "svdq_search_alpha")
+    return a.value, lam, list(obj)
+
+
 def svdq_debug_int4_group_accum(xq, wq, M: int, N: int, K: int, stream=None):
     acc = torch.empty((K // 64, M, N), dtype=torch.int32, device=xq.device)
     _check(_lib.svdq_debug_int4_group_accum(_ptr(xq), _ptr(wq), M, N, K, _ptr(acc), _stream(stream)),

@@ -152,6 +152,11 @@ bool use_pair_kernel(int64_t M, int64_t K) {
 
 }  // namespace
 
+namespace svdq {
+// Error reporting for the library's other translation units (offline.cu).
+svdq_status report_error(svdq_status s, const char *msg) { return fail(s, "%s", msg); }
+}  // namespace svdq
+
 extern "C" {
 
 const char *svdq_status_string(svdq_status s) {
