@@ -335,3 +335,53 @@ def search_alpha(x_cal, w, rank: int, fmt: str, grid, gs_x=1.0, scale_dtype="bf1
     best = min(range(len(grid)), key=lambda i: (errs[i], grid[i]))
     return grid[best], compute_smoothing(x_cal, w, grid[best]), errs
 
+
+
+# --------------------------------------------------------------------------
+# Offline: iterative low-rank refinement (reading Q3) -- SURVEY 8(f) row 4
+# --------------------------------------------------------------------------
+def dequantize_residual(ops: Operands) -> np.ndarray:
+    """Q(R) as values in the W_hat space, [K, N] fp64 (exact products of the stored codes and
+    scales: the per-channel dequantizers of quant.py transposed back to the paper layout)."""
+    if ops.fmt == "nvfp4":
+        v = Q.dequantize_nvfp4(ops.w_codes, ops.w_scales, ops.gs_w)
+    elif ops.fmt == "int4":
+        v = Q.dequantize_int4(ops.w_codes, ops.w_scales, ops.scale_dtype)
+    elif ops.fmt == "w8a8":
+        v = Q.dequantize_int8_rows(ops.w_codes, ops.w_scales)
+    else:
+        raise ValueError(ops.fmt)
+    return np.ascontiguousarray(v.T)
+
+
+def redecompose(w_hat, deq, r: int) -> Decomposition:
+    """One refinement step: "decomposing W - Q(R) and adjusting R accordingly", read as
+    (reading Q3) L1 L2 = the rank-r truncated SVD of W_hat - Q(R_{t-1}), R_t = W_hat - L1 L2.
+    `sigma` holds the singular values of the decomposed matrix W_hat - Q(R_{t-1})."""
+    T = np.asarray(w_hat, np.float64) - np.asarray(deq, np.float64)
+    U, s, Vt = np.linalg.svd(T, full_matrices=False)
+    L1 = U[:, :r] * s[:r][None, :]
+    L2 = Vt[:r, :]
+    return Decomposition(np.asarray(w_hat, np.float64), L1, L2, w_hat - L1 @ L2, s)
+
+
+def refine_lowrank(x_cal, w, lam32, rank: int, fmt: str, iters: int, gs_x=1.0, scale_dtype="bf16"):
+    """Iterative refinement of the low-rank branch: iterate 0 is the plain SVD split
+    (prepare_operands); iterate t >= 1 re-decomposes W_hat - Q(R_{t-1}) (redecompose) and
+    re-quantizes R_t; "then picking the result with the smallest error" -- the iterate with the
+    smallest calibration_error (the App. D objective, reading Q4); ties -> the earlier iterate.
+    Returns (best t, Operands of the best iterate, [objective per iterate], [Decomposition per iterate])."""
+    if iters < 0:
+        raise ValueError("iters must be >= 0")
+    lam32 = np.asarray(lam32, dtype=F32)
+    d = decompose(w, lam32, rank)
+    ops = prepare_operands(w, lam32, rank, fmt, gs_x=gs_x, scale_dtype=scale_dtype, decomp=d)
+    all_ops, errs, decs = [ops], [calibration_error(x_cal, w, ops)], [d]
+    for _ in range(iters):
+        d = redecompose(d.w_hat, dequantize_residual(ops), rank)
+        ops = prepare_operands(w, lam32, rank, fmt, gs_x=gs_x, scale_dtype=scale_dtype, decomp=d)
+        all_ops.append(ops)
+        errs.append(calibration_error(x_cal, w, ops))
+        decs.append(d)
+    best = min(range(len(errs)), key=lambda t: (errs[t], t))
+    return best, all_ops[best], errs, decs
