@@ -198,6 +198,23 @@ svdq_status svdq_search_alpha(const void *X_cal, int32_t x_dtype, int64_t M_cal,
                               const float *grid, int32_t n_grid, float *alpha_out, float *lambda_out,
                               double *objective_out, void *ws, size_t ws_bytes, void *stream);
 
+/* Iterative low-rank refinement (reading Q3).  Iterate 0 is
+ * svdq_quantize_weights(W, lambda); iterate t = 1..iters re-decomposes
+ * W_hat - Q(R_{t-1}) (Q(R_{t-1}) dequantized exactly to fp64 from iterate t-1's codes and
+ * scales; truncated SVD as in svdq_quantize_weights), sets R_t = W_hat - L1 L2 and re-quantizes.
+ * Each iterate is scored with the objective of svdq_search_alpha (K1 -> K2 on X_cal, no bias,
+ * ||X_cal W - Y||_F^2); "picking the result with the smallest error": the best iterate (ties ->
+ * the earlier) is written to dst (same buffer contract as svdq_quantize_weights; bias untouched),
+ * its index to *best_out [host] and all iters + 1 objectives to objective_out [host].
+ * X_cal: [dev] [M_cal][ldx] BF16 | FP16.  W: [dev] [K][N] fp32.  lambda: [dev] [K] fp32 > 0.
+ * ws: [dev] of svdq_refine_lowrank_workspace bytes.  iters >= 0.  Synchronizes `stream`. */
+svdq_status svdq_refine_lowrank_workspace(int32_t fmt, int64_t M_cal, int64_t K, int64_t N, int32_t rank,
+                                          size_t *ws_bytes);
+svdq_status svdq_refine_lowrank(const void *X_cal, int32_t x_dtype, int64_t M_cal, int64_t ldx, const float *W,
+                                const float *lambda, int64_t K, int64_t N, int32_t rank, int32_t fmt,
+                                int32_t scale_dtype, float gs_x, int32_t iters, svdq_linear *dst, int32_t *best_out,
+                                double *objective_out, void *ws, size_t ws_bytes, void *stream);
+
 /* LoRA fusion: dst->l1s = [src->l1s ; bf16(fl32(scale*A))^T] ([r+r_l][K]),
  * dst->l2s = [src->l2s | bf16(fl32(B/alpha))^T] ([N][r+r_l]); codes / scales untouched
  * (no re-quantization).  A: [dev] [K][r_l], B: [dev] [r_l][N] of ab_dtype

@@ -41,6 +41,7 @@ EXPORTS = [
     "svdq_quantize_residual",
     "svdq_quantize_weights_workspace", "svdq_quantize_weights", "svdq_lora_fuse",
     "svdq_search_alpha_workspace", "svdq_search_alpha",
+    "svdq_refine_lowrank_workspace", "svdq_refine_lowrank",
     "svdq_debug_int4_group_accum", "svdq_debug_codec", "svdq_status_string", "svdq_last_error",
     "svdq_launch_count", "svdq_version",
 ]
@@ -86,6 +87,9 @@ _sig = {
     "svdq_search_alpha_workspace": [_I32, _I64, _I64, _I64, _I32, _SZ],
     "svdq_search_alpha": [_P, _I32, _I64, _I64, _P, _I64, _I64, _I32, _I32, _I32, C.c_float, C.POINTER(C.c_float),
                           _I32, C.POINTER(C.c_float), _P, C.POINTER(C.c_double), _P, C.c_size_t, _P],
+    "svdq_refine_lowrank_workspace": [_I32, _I64, _I64, _I64, _I32, _SZ],
+    "svdq_refine_lowrank": [_P, _I32, _I64, _I64, _P, _P, _I64, _I64, _I32, _I32, _I32, C.c_float, _I32, _LP,
+                            C.POINTER(C.c_int32), C.POINTER(C.c_double), _P, C.c_size_t, _P],
     "svdq_debug_int4_group_accum": [_P, _P, _I64, _I64, _I64, _P, _P],
     "svdq_debug_codec": [_P, _P, _I64, _I32, _P],
 }
@@ -359,6 +363,36 @@ def svdq_search_alpha(X_cal, W, rank: int, fmt: str, grid, scale_dtype: str = "b
                                   rank, FMT[fmt], DTYPE[scale_dtype], gs_x, g, n, C.byref(a), _ptr(lam), obj,
                                   _ptr(ws), wsb, _stream(stream)), "svdq_search_alpha")
     return a.value, lam, list(obj)
+
+
+def svdq_refine_lowrank_workspace(fmt: str, M_cal: int, K: int, N: int, rank: int) -> int:
+    wsb = C.c_size_t()
+    _check(_lib.svdq_refine_lowrank_workspace(FMT[fmt], M_cal, K, N, rank, C.byref(wsb)),
+           "svdq_refine_lowrank_workspace")
+    return wsb.value
+
+
+def svdq_refine_lowrank(X_cal, W, lam, rank: int, fmt: str, iters: int, scale_dtype: str = "bf16",
+                        gs_x: float = 1.0, bias=None, stream=None):
+    """Iterative low-rank refinement on the GPU.  X_cal: [M_cal, K] bf16/fp16, W: [K, N] fp32,
+    lam: [K] fp32 (CUDA).  Returns (QuantizedLinear of the best iterate, best index, objectives list)."""
+    M, K = X_cal.shape
+    N = W.shape[1]
+    layer = QuantizedLinear.empty(fmt, K, N, rank, device=X_cal.device, scale_dtype=scale_dtype,
+                                  bias=bias, gs_x=gs_x)
+    wsb = svdq_refine_lowrank_workspace(fmt, M, K, N, rank)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=X_cal.device)
+    obj = (C.c_double * (iters + 1))()
+    best = C.c_int32()
+    Wc = W.contiguous().float()
+    lam = lam.contiguous().float()
+    _check(_lib.svdq_refine_lowrank(_ptr(X_cal), DTYPE[DTYPE_OF_TORCH[X_cal.dtype]], M, X_cal.stride(0), _ptr(Wc),
+                                    _ptr(lam), K, N, rank, FMT[fmt], DTYPE[scale_dtype], gs_x, iters, layer.ref,
+                                    C.byref(best), obj, _ptr(ws), wsb, _stream(stream)), "svdq_refine_lowrank")
+    layer.gs_w = layer.view.gs_w
+    layer.gs_x = layer.view.gs_x
+    del ws
+    return layer, best.value, list(obj)
 
 
 def svdq_debug_int4_group_accum(xq, wq, M: int, N: int, K: int, stream=None):

@@ -573,10 +573,17 @@ svdq_status svdq_quantize_weights_workspace(int64_t K, int64_t N, int32_t rank, 
   return SVDQ_OK;
 }
 
-svdq_status svdq_quantize_weights(const void *W, int32_t w_dtype, const float *lambda, int64_t K,
-                                  int64_t N, int32_t rank, int32_t fmt, int32_t scale_dtype,
-                                  float gs_x, const float *L1_opt, const float *L2_opt,
-                                  svdq_linear *dst, void *ws, size_t ws_bytes, void *stream) {
+}  // extern "C"
+
+namespace svdq {
+// svdq_quantize_weights with an optional refinement target (reading Q3): when `svd_sub`
+// ([K][N] fp64, Q(R_{t-1}) in the W_hat space) is given, L1 L2 is the truncated SVD of
+// W_hat - svd_sub (formed in `tgt`, [K][N] fp64 scratch) and R = W_hat - L1 L2 as usual.
+svdq_status quantize_weights_impl(const void *W, int32_t w_dtype, const float *lambda, int64_t K, int64_t N,
+                                  int32_t rank, int32_t fmt, int32_t scale_dtype, float gs_x, const float *L1_opt,
+                                  const float *L2_opt, svdq_linear *dst, void *ws, size_t ws_bytes, void *stream,
+                                  const double *svd_sub, double *tgt) {
+  if (svd_sub && (!tgt || L1_opt)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "refinement target needs tgt, no L1_opt");
   if (!W || !lambda || !dst || !ws) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null pointer");
   if (w_dtype != SVDQ_BF16 && w_dtype != SVDQ_FP16 && w_dtype != SVDQ_FP32)
     return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad W dtype");
@@ -630,11 +637,18 @@ svdq_status svdq_quantize_weights(const void *W, int32_t w_dtype, const float *l
           break;
         }
       } else {
-        // Gram matrix of the smaller side (column-major view of row-major What is What^T, N x K)
+        // SVD source: W_hat, or W_hat - Q(R_{t-1}) when refining
+        const double *Src = What;
+        if (svd_sub) {
+          if (launch_sub64(What, svd_sub, tgt, K * N, s) != cudaSuccess) { result = fail(SVDQ_ERR_CUDA, "refine target"); break; }
+          ++g_launches;
+          Src = tgt;
+        }
+        // Gram matrix of the smaller side (column-major view of row-major Src is Src^T, N x K)
         if (N <= K) {
-          if (cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, (int)N, (int)K, &one, What, (int)N, &zero, G, (int)N) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "syrk"); break; }
+          if (cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, (int)N, (int)K, &one, Src, (int)N, &zero, G, (int)N) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "syrk"); break; }
         } else {
-          if (cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, (int)K, (int)N, &one, What, (int)N, &zero, G, (int)K) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "syrk"); break; }
+          if (cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, (int)K, (int)N, &one, Src, (int)N, &zero, G, (int)K) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "syrk"); break; }
         }
         cusolverDnHandle_t hs = nullptr;
         if (cusolverDnCreate(&hs) != CUSOLVER_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "cusolverDnCreate"); break; }
@@ -644,14 +658,14 @@ svdq_status svdq_quantize_weights(const void *W, int32_t w_dtype, const float *l
         if (cs != CUSOLVER_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "syevd"); break; }
         if (launch_eig_to_factors(G, evals, P, rank, E, sigma, s) != cudaSuccess) { result = fail(SVDQ_ERR_CUDA, "eig"); break; }
         if (N <= K) {
-          // L2 = E^T (rows = right singular vectors); L1 = What E  (= U_r Sigma_r)
+          // L2 = E^T (rows = right singular vectors); L1 = Src E  (= U_r Sigma_r)
           if (cublasDgeam(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)N, rank, &one, E, rank, &zero, E, (int)N, L2d, (int)N) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "geam"); break; }
-          if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, rank, (int)K, (int)N, &one, E, rank, What, (int)N, &zero, L1d, rank) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "gemm L1"); break; }
+          if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, rank, (int)K, (int)N, &one, E, rank, Src, (int)N, &zero, L1d, rank) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "gemm L1"); break; }
         } else {
-          // L1 = E diag(sigma); L2 = diag(sigma)^-1 E^T What
+          // L1 = E diag(sigma); L2 = diag(sigma)^-1 E^T Src
           if (cudaMemcpyAsync(L1d, E, static_cast<size_t>(K) * rank * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess) { result = fail(SVDQ_ERR_CUDA, "copy"); break; }
           if (launch_scale_cols(L1d, K, rank, sigma, 0, 0, s) != cudaSuccess) { result = fail(SVDQ_ERR_CUDA, "scale"); break; }
-          if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, (int)N, rank, (int)K, &one, What, (int)N, E, rank, &zero, L2d, (int)N) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "gemm L2"); break; }
+          if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, (int)N, rank, (int)K, &one, Src, (int)N, E, rank, &zero, L2d, (int)N) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "gemm L2"); break; }
           if (launch_scale_cols(L2d, rank, N, sigma, 1, 1, s) != cudaSuccess) { result = fail(SVDQ_ERR_CUDA, "scale"); break; }
         }
         g_launches += 3;
@@ -689,6 +703,18 @@ svdq_status svdq_quantize_weights(const void *W, int32_t w_dtype, const float *l
   if (result != SVDQ_OK) return result;
   SVDQ_CUDA(cudaStreamSynchronize(s), "sync");
   return SVDQ_OK;
+}
+
+}  // namespace svdq
+
+extern "C" {
+
+svdq_status svdq_quantize_weights(const void *W, int32_t w_dtype, const float *lambda, int64_t K,
+                                  int64_t N, int32_t rank, int32_t fmt, int32_t scale_dtype,
+                                  float gs_x, const float *L1_opt, const float *L2_opt,
+                                  svdq_linear *dst, void *ws, size_t ws_bytes, void *stream) {
+  return svdq::quantize_weights_impl(W, w_dtype, lambda, K, N, rank, fmt, scale_dtype, gs_x, L1_opt, L2_opt, dst, ws,
+                                     ws_bytes, stream, nullptr, nullptr);
 }
 
 svdq_status svdq_lora_fuse(const svdq_linear *src, const void *A, const void *B, int32_t ab_dtype,

@@ -127,6 +127,10 @@ cudaError_t launch_absmax(const float *R, int64_t n, unsigned int *out_bits, cud
 cudaError_t launch_quantize_residual(const float *R, int64_t K, int64_t N, int fmt, bool scale_bf16,
                                      float gs_w, uint8_t *codes, uint8_t *scales, cudaStream_t s);
 cudaError_t launch_codec(const float *in, uint8_t *out, int64_t n, int kind, cudaStream_t s);
+// refinement step: Q(R) -> [K][N] fp64 values; out = a - b
+cudaError_t launch_dequant_residual64(const uint8_t *codes, const uint8_t *scales, int fmt, bool scale_bf16,
+                                      float gs_w, int64_t K, int64_t N, double *out, cudaStream_t s);
+cudaError_t launch_sub64(const double *a, const double *b, double *out, int64_t n, cudaStream_t s);
 cudaError_t launch_lambda_inv(const float *lam, float *lam_inv, int64_t K, cudaStream_t s);
 cudaError_t launch_smooth_weight64(const void *W, int w_dtype, const float *lam, int64_t K, int64_t N,
                                    double *What, cudaStream_t s);

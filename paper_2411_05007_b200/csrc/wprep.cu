@@ -136,6 +136,42 @@ __global__ void quant_res_int8_kernel(const float *__restrict__ R, int64_t K, in
   }
 }
 
+// Q(R) back to values in the W_hat space for the refinement step: out[k][n] (fp64, [K][N])
+// = code * scale, exact.  NVFP4: e2m1(q) * e4m3(sf) * gs_w; INT4: q * s16; W8A8: q * s32.
+__global__ void dequant_residual64_kernel(const uint8_t *__restrict__ codes, const uint8_t *__restrict__ scales,
+                                          int fmt, bool scale_bf16, float gs_w, int64_t K, int64_t N,
+                                          double *__restrict__ out) {
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < K * N;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t k = idx / N;
+    const int64_t n = idx % N;
+    double v;
+    if (fmt == 2) {
+      v = static_cast<double>(reinterpret_cast<const int8_t *>(codes)[n * K + k]) *
+          static_cast<double>(reinterpret_cast<const float *>(scales)[n]);
+    } else {
+      const uint32_t nib = (codes[n * (K / 2) + k / 2] >> (4 * (k & 1))) & 0xFu;
+      if (fmt == 0) {
+        const float mag[8] = {0.f, 0.5f, 1.f, 1.5f, 2.f, 3.f, 4.f, 6.f};
+        const double e = (nib & 8u) ? -mag[nib & 7u] : mag[nib & 7u];
+        v = e * static_cast<double>(e4m3_to_f32(scales[sf_offset(n, k / 16, K)])) * static_cast<double>(gs_w);
+      } else {
+        const uint16_t sb = reinterpret_cast<const uint16_t *>(scales)[n * (K / 64) + k / 64];
+        const float sc = scale_bf16 ? scale16_to_f32<true>(sb) : scale16_to_f32<false>(sb);
+        v = static_cast<double>(static_cast<int>(nib ^ 8u) - 8) * static_cast<double>(sc);
+      }
+    }
+    out[idx] = v;
+  }
+}
+
+__global__ void sub64_kernel(const double *__restrict__ a, const double *__restrict__ b, double *__restrict__ out,
+                             int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = a[i] - b[i];
+}
+
 __global__ void codec_kernel(const float *__restrict__ in, uint8_t *__restrict__ out, int64_t n,
                              int kind) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -250,6 +286,17 @@ cudaError_t launch_quantize_residual(const float *R, int64_t K, int64_t N, int f
       quant_res_int4_kernel<false><<<blocks_for(work, 128), 128, 0, s>>>(
           R, K, N, codes, reinterpret_cast<uint16_t *>(scales));
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dequant_residual64(const uint8_t *codes, const uint8_t *scales, int fmt, bool scale_bf16,
+                                      float gs_w, int64_t K, int64_t N, double *out, cudaStream_t s) {
+  dequant_residual64_kernel<<<blocks_for(K * N, 256), 256, 0, s>>>(codes, scales, fmt, scale_bf16, gs_w, K, N, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sub64(const double *a, const double *b, double *out, int64_t n, cudaStream_t s) {
+  sub64_kernel<<<blocks_for(n, 256), 256, 0, s>>>(a, b, out, n);
   return cudaGetLastError();
 }
 
