@@ -14,6 +14,7 @@ Modules
 -------
 formats      E2M1 / E4M3 / bf16 / fp16 codecs, nibble packing, 128x4 SF layout
 quant        Eq. (1) quantizers: NVFP4 (g16, E4M3 scales) and INT4 (g64, 16-bit)
+gptq         GPTQ quantization of the residual (App. D)
 svdquant     smoothing, SVD split (Eq. 5), operand preparation, forward, LoRA
 linalg       one-sided Jacobi SVD for tiny shapes (independent of LAPACK)
 diagnostics  Eq. (3) error, Prop. 4.1 / 4.2 checks, cost fraction
@@ -23,4 +24,4 @@ Parity unpinned: the individual factors L1, L2 (sign / rotation freedom,
 reading Q2) -- only their product and R are compared.
 """
 
-from . import formats, quant, svdquant, linalg, diagnostics  # noqa: F401
+from . import formats, quant, gptq, svdquant, linalg, diagnostics  # noqa: F401

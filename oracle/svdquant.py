@@ -24,6 +24,7 @@ from typing import Optional
 import numpy as np
 
 from . import formats as F
+from . import gptq as G
 from . import quant as Q
 
 F32 = np.float32
@@ -150,14 +151,21 @@ def quantize_residual(R32, fmt: str, scale_dtype: str = "bf16", gs_w=None):
 
 
 def prepare_operands(w, lam32, r: int, fmt: str, gs_x=1.0, scale_dtype="bf16",
-                     bias=None, svd=None, decomp: Optional[Decomposition] = None) -> Operands:
+                     bias=None, svd=None, decomp: Optional[Decomposition] = None,
+                     gptq_x=None, gptq_damp: float = G.DAMP) -> Operands:
     """Offline weight preparation: smoothing, SVD, residual
-    quantization, L1s / L2s derivation."""
+    quantization, L1s / L2s derivation.  With calibration activations `gptq_x` ([M, K], the
+    unsmoothed X), the residual is quantized by GPTQ on X_hat = fl32(x * lam_inv)
+    instead of round-to-nearest."""
     lam32 = np.asarray(lam32, dtype=F32)
     d = decomp if decomp is not None else decompose(w, lam32, r, svd=svd)
     K, N = d.w_hat.shape
     R32 = d.R.astype(F32)
-    codes, scales, gs_w = quantize_residual(R32, fmt, scale_dtype)
+    if gptq_x is None:
+        codes, scales, gs_w = quantize_residual(R32, fmt, scale_dtype)
+    else:
+        xh = Q.smooth_activation(gptq_x, lambda_inverse(lam32))
+        codes, scales, gs_w = G.gptq_quantize_residual(R32, xh, fmt, scale_dtype, gptq_damp)
     gs_x = F32(gs_x) if fmt == "nvfp4" else F32(1.0)
     lam_inv32 = lambda_inverse(lam32)
     alpha = F32(gs_x * gs_w) if fmt == "nvfp4" else F32(1.0)
