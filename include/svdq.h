@@ -215,6 +215,35 @@ svdq_status svdq_refine_lowrank(const void *X_cal, int32_t x_dtype, int64_t M_ca
                                 int32_t scale_dtype, float gs_x, int32_t iters, svdq_linear *dst, int32_t *best_out,
                                 double *objective_out, void *ws, size_t ws_bytes, void *stream);
 
+/* GPTQ quantization of the residual (App. D: "We use GPTQ to quantize the residual
+ * weights"; readings G1-G3 in DESIGN.md).  The cited method's column-by-column procedure on
+ * R^T: H = X_hat^T X_hat (fp64) with X_hat = fl32(X_cal * lambda_inv) (K1's smoothing),
+ * channels with H_kk == 0 get H_kk = 1 and a zero residual row, H += damp * mean(diag H) * I,
+ * U = upper Cholesky factor of H^-1; input channels k = 0..K-1 are quantized in order, each
+ * group's scale (NVFP4 16 / INT4 64) taken from the error-compensated values at the group start,
+ * W8A8 channel scales and the NVFP4 gs_w from the initial residual (as svdq_quantize_residual),
+ * and the error (r_k - deq(q_k)) / U_kk is propagated to the remaining channels via row k of U.
+ * Output codes / scales have exactly the layout of svdq_quantize_residual.
+ *
+ * svdq_quantize_residual_gptq: R [dev] [K][N] fp32 (paper layout, read only); lambda_inv [dev]
+ *   [K] fp32; X_cal [dev] [M_cal][ldx] BF16 | FP16; damp >= 0 (0.01 = GPTQ's default).  *gs_w
+ *   [host] receives the NVFP4 per-tensor scale (1 otherwise).  ws: [dev] of
+ *   svdq_quantize_residual_gptq_workspace bytes.  SVDQ_ERR_INVALID_ARGUMENT if H is not positive
+ *   definite after dampening.  Synchronizes `stream`.
+ * svdq_quantize_weights_gptq: svdq_quantize_weights (no L1_opt / L2_opt) with the residual
+ *   quantized by GPTQ on (X_cal, lambda); ws: [dev] of svdq_quantize_weights_gptq_workspace bytes. */
+svdq_status svdq_quantize_residual_gptq_workspace(int64_t M_cal, int64_t K, int64_t N, size_t *ws_bytes);
+svdq_status svdq_quantize_residual_gptq(const float *R, int64_t K, int64_t N, int32_t fmt, int32_t scale_dtype,
+                                        const void *X_cal, int32_t x_dtype, int64_t M_cal, int64_t ldx,
+                                        const float *lambda_inv, float damp, uint8_t *codes, uint8_t *scales,
+                                        float *gs_w, void *ws, size_t ws_bytes, void *stream);
+svdq_status svdq_quantize_weights_gptq_workspace(int64_t M_cal, int64_t K, int64_t N, int32_t rank,
+                                                 size_t *ws_bytes);
+svdq_status svdq_quantize_weights_gptq(const void *W, int32_t w_dtype, const float *lambda, int64_t K, int64_t N,
+                                       int32_t rank, int32_t fmt, int32_t scale_dtype, float gs_x, const void *X_cal,
+                                       int32_t x_dtype, int64_t M_cal, int64_t ldx, float damp, svdq_linear *dst,
+                                       void *ws, size_t ws_bytes, void *stream);
+
 /* LoRA fusion: dst->l1s = [src->l1s ; bf16(fl32(scale*A))^T] ([r+r_l][K]),
  * dst->l2s = [src->l2s | bf16(fl32(B/alpha))^T] ([N][r+r_l]); codes / scales untouched
  * (no re-quantization).  A: [dev] [K][r_l], B: [dev] [r_l][N] of ab_dtype

@@ -42,6 +42,8 @@ EXPORTS = [
     "svdq_quantize_weights_workspace", "svdq_quantize_weights", "svdq_lora_fuse",
     "svdq_search_alpha_workspace", "svdq_search_alpha",
     "svdq_refine_lowrank_workspace", "svdq_refine_lowrank",
+    "svdq_quantize_residual_gptq_workspace", "svdq_quantize_residual_gptq",
+    "svdq_quantize_weights_gptq_workspace", "svdq_quantize_weights_gptq",
     "svdq_debug_int4_group_accum", "svdq_debug_codec", "svdq_status_string", "svdq_last_error",
     "svdq_launch_count", "svdq_version",
 ]
@@ -90,6 +92,12 @@ _sig = {
     "svdq_refine_lowrank_workspace": [_I32, _I64, _I64, _I64, _I32, _SZ],
     "svdq_refine_lowrank": [_P, _I32, _I64, _I64, _P, _P, _I64, _I64, _I32, _I32, _I32, C.c_float, _I32, _LP,
                             C.POINTER(C.c_int32), C.POINTER(C.c_double), _P, C.c_size_t, _P],
+    "svdq_quantize_residual_gptq_workspace": [_I64, _I64, _I64, _SZ],
+    "svdq_quantize_residual_gptq": [_P, _I64, _I64, _I32, _I32, _P, _I32, _I64, _I64, _P, C.c_float, _P, _P,
+                                    C.POINTER(C.c_float), _P, C.c_size_t, _P],
+    "svdq_quantize_weights_gptq_workspace": [_I64, _I64, _I64, _I32, _SZ],
+    "svdq_quantize_weights_gptq": [_P, _I32, _P, _I64, _I64, _I32, _I32, _I32, C.c_float, _P, _I32, _I64, _I64,
+                                   C.c_float, _LP, _P, C.c_size_t, _P],
     "svdq_debug_int4_group_accum": [_P, _P, _I64, _I64, _I64, _P, _P],
     "svdq_debug_codec": [_P, _P, _I64, _I32, _P],
 }
@@ -393,6 +401,60 @@ def svdq_refine_lowrank(X_cal, W, lam, rank: int, fmt: str, iters: int, scale_dt
     layer.gs_x = layer.view.gs_x
     del ws
     return layer, best.value, list(obj)
+
+
+def svdq_quantize_residual_gptq_workspace(M_cal: int, K: int, N: int) -> int:
+    wsb = C.c_size_t()
+    _check(_lib.svdq_quantize_residual_gptq_workspace(M_cal, K, N, C.byref(wsb)), "svdq_quantize_residual_gptq_workspace")
+    return wsb.value
+
+
+def svdq_quantize_weights_gptq_workspace(M_cal: int, K: int, N: int, rank: int) -> int:
+    wsb = C.c_size_t()
+    _check(_lib.svdq_quantize_weights_gptq_workspace(M_cal, K, N, rank, C.byref(wsb)),
+           "svdq_quantize_weights_gptq_workspace")
+    return wsb.value
+
+
+def svdq_quantize_residual_gptq(R, X_cal, lam_inv, fmt: str, scale_dtype: str = "bf16", damp: float = 0.01,
+                                stream=None):
+    """GPTQ of the residual R ([K, N] fp32 CUDA) on X_hat = fl32(X_cal * lam_inv).
+    Returns (codes, scales, gs_w) in the layout of svdq_quantize_residual."""
+    K, N = R.shape
+    M = X_cal.shape[0]
+    codes_b, scales_b, _, _ = svdq_weight_buffer_sizes(fmt, K, N, 0)
+    codes = torch.empty(codes_b, dtype=torch.uint8, device=R.device)
+    scales = torch.zeros(scales_b, dtype=torch.uint8, device=R.device)
+    wsb = svdq_quantize_residual_gptq_workspace(M, K, N)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=R.device)
+    gs = C.c_float(0.0)
+    R = R.contiguous().float()
+    lam_inv = lam_inv.contiguous().float()
+    _check(_lib.svdq_quantize_residual_gptq(_ptr(R), K, N, FMT[fmt], DTYPE[scale_dtype], _ptr(X_cal),
+                                            DTYPE[DTYPE_OF_TORCH[X_cal.dtype]], M, X_cal.stride(0), _ptr(lam_inv),
+                                            damp, _ptr(codes), _ptr(scales), C.byref(gs), _ptr(ws), wsb,
+                                            _stream(stream)), "svdq_quantize_residual_gptq")
+    return codes, scales, gs.value
+
+
+def svdq_quantize_weights_gptq(W, lam, rank: int, fmt: str, X_cal, scale_dtype: str = "bf16", gs_x: float = 1.0,
+                               damp: float = 0.01, bias=None, stream=None) -> QuantizedLinear:
+    """svdq_quantize_weights with the residual quantized by GPTQ on the calibration batch X_cal."""
+    K, N = W.shape
+    M = X_cal.shape[0]
+    layer = QuantizedLinear.empty(fmt, K, N, rank, device=W.device, scale_dtype=scale_dtype, bias=bias, gs_x=gs_x)
+    wsb = svdq_quantize_weights_gptq_workspace(M, K, N, rank)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=W.device)
+    W = W.contiguous()
+    lam = lam.contiguous().float()
+    _check(_lib.svdq_quantize_weights_gptq(
+        _ptr(W), DTYPE[DTYPE_OF_TORCH[W.dtype]], _ptr(lam), K, N, rank, FMT[fmt], DTYPE[scale_dtype], gs_x,
+        _ptr(X_cal), DTYPE[DTYPE_OF_TORCH[X_cal.dtype]], M, X_cal.stride(0), damp, layer.ref, _ptr(ws), wsb,
+        _stream(stream)), "svdq_quantize_weights_gptq")
+    layer.gs_w = layer.view.gs_w
+    layer.gs_x = layer.view.gs_x
+    del ws
+    return layer
 
 
 def svdq_debug_int4_group_accum(xq, wq, M: int, N: int, K: int, stream=None):

@@ -14,6 +14,7 @@
 
 #include "../../include/svdq.h"
 #include "formats.cuh"
+#include "gptq.h"
 #include "k1_launch.h"
 
 using namespace svdq;
@@ -582,7 +583,10 @@ namespace svdq {
 svdq_status quantize_weights_impl(const void *W, int32_t w_dtype, const float *lambda, int64_t K, int64_t N,
                                   int32_t rank, int32_t fmt, int32_t scale_dtype, float gs_x, const float *L1_opt,
                                   const float *L2_opt, svdq_linear *dst, void *ws, size_t ws_bytes, void *stream,
-                                  const double *svd_sub, double *tgt) {
+                                  const double *svd_sub, double *tgt, const GptqArgs *gq, uint8_t *gq_ws) {
+  if (gq && (!gq->X || !gq_ws || gq->M < 1 || gq->ldx < K || !(gq->damp >= 0.f) ||
+             (gq->x_dtype != SVDQ_BF16 && gq->x_dtype != SVDQ_FP16)))
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad GPTQ calibration arguments");
   if (svd_sub && (!tgt || L1_opt)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "refinement target needs tgt, no L1_opt");
   if (!W || !lambda || !dst || !ws) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null pointer");
   if (w_dtype != SVDQ_BF16 && w_dtype != SVDQ_FP16 && w_dtype != SVDQ_FP32)
@@ -621,6 +625,14 @@ svdq_status quantize_weights_impl(const void *W, int32_t w_dtype, const float *l
   SVDQ_CUDA(launch_lambda_inv(lambda, lam_inv, K, s), "lambda_inv");
   SVDQ_CUDA(launch_smooth_weight64(W, w_dtype, lambda, K, N, What, s), "smooth W");
   g_launches += 2;
+  GptqState gst{};
+  if (gq) {   // Hessian of the residual's proxy loss on X_hat; needs lambda_inv
+    const int glw = gptq_potrf_lwork(K);
+    if (glw < 0) return fail(SVDQ_ERR_CUDA, "cusolver potrf bufferSize failed");
+    if (const char *e = gptq_hessian(*gq, lam_inv, K, glw, gq_ws, s, &gst))
+      return fail(std::strstr(e, "positive definite") ? SVDQ_ERR_INVALID_ARGUMENT : SVDQ_ERR_CUDA, "GPTQ: %s", e);
+    g_launches += 2;
+  }
 
   cublasHandle_t hb = nullptr;
   if (cublasCreate(&hb) != CUBLAS_STATUS_SUCCESS) return fail(SVDQ_ERR_CUDA, "cublasCreate");
@@ -673,12 +685,23 @@ svdq_status quantize_weights_impl(const void *W, int32_t w_dtype, const float *l
       // R = W_hat - L1 L2  (in place on What; column-major: What^T -= L2^T L1^T)
       if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)N, (int)K, rank, &mone, L2d, (int)N, L1d, rank, &one, What, (int)N) != CUBLAS_STATUS_SUCCESS) { result = fail(SVDQ_ERR_CUDA, "gemm R"); break; }
     }
+    if (gq && gptq_zero_dead(What, gst, K, N, s) != cudaSuccess) { result = fail(SVDQ_ERR_CUDA, "GPTQ dead rows"); break; }
     if (launch_f64_to_f32(What, R32, K * N, s) != cudaSuccess) { result = fail(SVDQ_ERR_CUDA, "R32"); break; }
     ++g_launches;
     float gs_w = 0.f;
     if ((result = svdq_quantize_residual(R32, K, N, fmt, scale_dtype, const_cast<uint8_t *>(dst->w_codes),
                                          const_cast<uint8_t *>(dst->w_scales), &gs_w, stream)) != SVDQ_OK)
       break;
+    if (gq) {   // GPTQ overwrites the RTN codes (and group scales); RTN supplied gs_w / W8A8 channel scales
+      if (const char *e = gptq_run(What, gst, K, N, fmt == SVDQ_FMT_NVFP4 ? 0 : (fmt == SVDQ_FMT_W8A8 ? 2 : 1),
+                                   scale_dtype == SVDQ_BF16, gs_w,
+                                   fmt == SVDQ_FMT_W8A8 ? reinterpret_cast<const float *>(dst->w_scales) : nullptr,
+                                   const_cast<uint8_t *>(dst->w_codes), const_cast<uint8_t *>(dst->w_scales), s)) {
+        result = fail(SVDQ_ERR_CUDA, "GPTQ: %s", e);
+        break;
+      }
+      g_launches += 2 * ((K + 63) / 64);
+    }
     const float gx = fmt == SVDQ_FMT_NVFP4 ? gs_x : 1.0f;
     const float alpha = fmt == SVDQ_FMT_NVFP4 ? gx * gs_w : 1.0f;
     if (rank > 0) {
@@ -714,7 +737,83 @@ svdq_status svdq_quantize_weights(const void *W, int32_t w_dtype, const float *l
                                   float gs_x, const float *L1_opt, const float *L2_opt,
                                   svdq_linear *dst, void *ws, size_t ws_bytes, void *stream) {
   return svdq::quantize_weights_impl(W, w_dtype, lambda, K, N, rank, fmt, scale_dtype, gs_x, L1_opt, L2_opt, dst, ws,
-                                     ws_bytes, stream, nullptr, nullptr);
+                                     ws_bytes, stream, nullptr, nullptr, nullptr, nullptr);
+}
+
+svdq_status svdq_quantize_residual_gptq_workspace(int64_t M_cal, int64_t K, int64_t N, size_t *ws_bytes) {
+  if (!ws_bytes) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null output");
+  if (M_cal < 1) return fail(SVDQ_ERR_SHAPE, "M_cal must be >= 1");
+  if (K <= 0 || K % 64 || N <= 0 || N % 16) return fail(SVDQ_ERR_SHAPE, "bad K/N");
+  const int glw = gptq_potrf_lwork(K);
+  if (glw < 0) return fail(SVDQ_ERR_CUDA, "cusolver potrf bufferSize failed");
+  *ws_bytes = up256(static_cast<size_t>(K) * N * 8) + up256(static_cast<size_t>(K) * N * 4) +
+              gptq_workspace_bytes(M_cal, K, N, glw);
+  return SVDQ_OK;
+}
+
+svdq_status svdq_quantize_residual_gptq(const float *R, int64_t K, int64_t N, int32_t fmt, int32_t scale_dtype,
+                                        const void *X_cal, int32_t x_dtype, int64_t M_cal, int64_t ldx,
+                                        const float *lambda_inv, float damp, uint8_t *codes, uint8_t *scales,
+                                        float *gs_w, void *ws, size_t ws_bytes, void *stream) {
+  size_t need = 0;
+  svdq_status st = svdq_quantize_residual_gptq_workspace(M_cal, K, N, &need);
+  if (st != SVDQ_OK) return st;
+  if (!R || !X_cal || !lambda_inv || !codes || !scales || !gs_w || !ws)
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "null pointer");
+  if (ws_bytes < need) return fail(SVDQ_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  if (ldx < K || !(damp >= 0.f) || (x_dtype != SVDQ_BF16 && x_dtype != SVDQ_FP16))
+    return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad GPTQ calibration arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t *base = static_cast<uint8_t *>(ws);
+  double *R64 = reinterpret_cast<double *>(base);
+  float *R32 = reinterpret_cast<float *>(base + up256(static_cast<size_t>(K) * N * 8));
+  uint8_t *gws = base + up256(static_cast<size_t>(K) * N * 8) + up256(static_cast<size_t>(K) * N * 4);
+  const svdq::GptqArgs gq{X_cal, x_dtype, M_cal, ldx, damp};
+  svdq::GptqState gst{};
+  SVDQ_CUDA(launch_f32_to_f64(R, R64, K * N, s), "R64");
+  if (const char *e = gptq_hessian(gq, lambda_inv, K, gptq_potrf_lwork(K), gws, s, &gst))
+    return fail(std::strstr(e, "positive definite") ? SVDQ_ERR_INVALID_ARGUMENT : SVDQ_ERR_CUDA, "GPTQ: %s", e);
+  SVDQ_CUDA(gptq_zero_dead(R64, gst, K, N, s), "GPTQ dead rows");
+  SVDQ_CUDA(launch_f64_to_f32(R64, R32, K * N, s), "R32");
+  *gs_w = 0.f;
+  if ((st = svdq_quantize_residual(R32, K, N, fmt, scale_dtype, codes, scales, gs_w, stream)) != SVDQ_OK) return st;
+  if (const char *e = gptq_run(R64, gst, K, N, fmt == SVDQ_FMT_NVFP4 ? 0 : (fmt == SVDQ_FMT_W8A8 ? 2 : 1),
+                               scale_dtype == SVDQ_BF16, *gs_w,
+                               fmt == SVDQ_FMT_W8A8 ? reinterpret_cast<const float *>(scales) : nullptr, codes, scales,
+                               s))
+    return fail(SVDQ_ERR_CUDA, "GPTQ: %s", e);
+  g_launches += 6 + 2 * ((K + 63) / 64);
+  SVDQ_CUDA(cudaStreamSynchronize(s), "sync");
+  return SVDQ_OK;
+}
+
+svdq_status svdq_quantize_weights_gptq_workspace(int64_t M_cal, int64_t K, int64_t N, int32_t rank,
+                                                 size_t *ws_bytes) {
+  if (!ws_bytes) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null output");
+  if (M_cal < 1) return fail(SVDQ_ERR_SHAPE, "M_cal must be >= 1");
+  size_t qw = 0;
+  svdq_status st = svdq_quantize_weights_workspace(K, N, rank, &qw);
+  if (st != SVDQ_OK) return st;
+  const int glw = gptq_potrf_lwork(K);
+  if (glw < 0) return fail(SVDQ_ERR_CUDA, "cusolver potrf bufferSize failed");
+  *ws_bytes = up256(qw) + gptq_workspace_bytes(M_cal, K, N, glw);
+  return SVDQ_OK;
+}
+
+svdq_status svdq_quantize_weights_gptq(const void *W, int32_t w_dtype, const float *lambda, int64_t K, int64_t N,
+                                       int32_t rank, int32_t fmt, int32_t scale_dtype, float gs_x, const void *X_cal,
+                                       int32_t x_dtype, int64_t M_cal, int64_t ldx, float damp, svdq_linear *dst,
+                                       void *ws, size_t ws_bytes, void *stream) {
+  size_t need = 0, qw = 0;
+  svdq_status st = svdq_quantize_weights_gptq_workspace(M_cal, K, N, rank, &need);
+  if (st != SVDQ_OK) return st;
+  if (!ws) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null workspace");
+  if (ws_bytes < need) return fail(SVDQ_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  if ((st = svdq_quantize_weights_workspace(K, N, rank, &qw)) != SVDQ_OK) return st;
+  const svdq::GptqArgs gq{X_cal, x_dtype, M_cal, ldx, damp};
+  return svdq::quantize_weights_impl(W, w_dtype, lambda, K, N, rank, fmt, scale_dtype, gs_x, nullptr, nullptr, dst,
+                                     ws, up256(qw), stream, nullptr, nullptr, &gq,
+                                     static_cast<uint8_t *>(ws) + up256(qw));
 }
 
 svdq_status svdq_lora_fuse(const svdq_linear *src, const void *A, const void *B, int32_t ab_dtype,

@@ -17,15 +17,12 @@
 #include <vector>
 
 #include "../../include/svdq.h"
+#include "gptq.h"
 #include "k1_launch.h"
 #include "sm100.cuh"
 
 namespace svdq {
 svdq_status report_error(svdq_status s, const char *msg);   // api.cu
-svdq_status quantize_weights_impl(const void *W, int32_t w_dtype, const float *lambda, int64_t K, int64_t N,
-                                  int32_t rank, int32_t fmt, int32_t scale_dtype, float gs_x, const float *L1_opt,
-                                  const float *L2_opt, svdq_linear *dst, void *ws, size_t ws_bytes, void *stream,
-                                  const double *svd_sub, double *tgt);   // api.cu
 }
 
 namespace {
@@ -338,7 +335,7 @@ svdq_status svdq_refine_lowrank(const void *X_cal, int32_t x_dtype, int64_t M_ca
       return svdq::report_error(SVDQ_ERR_CUDA, "dequantize residual");
     if ((st = svdq::quantize_weights_impl(W, SVDQ_FP32, lambda, K, N, rank, fmt, scale_dtype, gs_x, nullptr, nullptr,
                                           &L, base + w.qws, w.qws_b, stream, t > 0 ? deq : nullptr,
-                                          t > 0 ? tgt : nullptr)) != SVDQ_OK)
+                                          t > 0 ? tgt : nullptr, nullptr, nullptr)) != SVDQ_OK)
       return st;
     if ((st = objective(&L, X_cal, x_dtype, M_cal, ldx, base + w.xq, base + w.xs,
                         reinterpret_cast<uint16_t *>(base + w.xl1), y, yref, err, s, &objective_out[t])) != SVDQ_OK)
