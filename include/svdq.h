@@ -206,14 +206,17 @@ svdq_status svdq_search_alpha(const void *X_cal, int32_t x_dtype, int64_t M_cal,
  * ||X_cal W - Y||_F^2); "picking the result with the smallest error": the best iterate (ties ->
  * the earlier) is written to dst (same buffer contract as svdq_quantize_weights; bias untouched),
  * its index to *best_out [host] and all iters + 1 objectives to objective_out [host].
+ * use_gptq != 0: every iterate's residual is quantized by GPTQ on X_cal with dampening `damp`
+ * (svdq_quantize_weights_gptq) instead of round-to-nearest.
  * X_cal: [dev] [M_cal][ldx] BF16 | FP16.  W: [dev] [K][N] fp32.  lambda: [dev] [K] fp32 > 0.
  * ws: [dev] of svdq_refine_lowrank_workspace bytes.  iters >= 0.  Synchronizes `stream`. */
 svdq_status svdq_refine_lowrank_workspace(int32_t fmt, int64_t M_cal, int64_t K, int64_t N, int32_t rank,
-                                          size_t *ws_bytes);
+                                          int32_t use_gptq, size_t *ws_bytes);
 svdq_status svdq_refine_lowrank(const void *X_cal, int32_t x_dtype, int64_t M_cal, int64_t ldx, const float *W,
                                 const float *lambda, int64_t K, int64_t N, int32_t rank, int32_t fmt,
-                                int32_t scale_dtype, float gs_x, int32_t iters, svdq_linear *dst, int32_t *best_out,
-                                double *objective_out, void *ws, size_t ws_bytes, void *stream);
+                                int32_t scale_dtype, float gs_x, int32_t iters, int32_t use_gptq, float damp,
+                                svdq_linear *dst, int32_t *best_out, double *objective_out, void *ws, size_t ws_bytes,
+                                void *stream);
 
 /* GPTQ quantization of the residual (App. D: "We use GPTQ to quantize the residual
  * weights"; readings G1-G3 in DESIGN.md).  The cited method's column-by-column procedure on

@@ -373,21 +373,25 @@ def redecompose(w_hat, deq, r: int) -> Decomposition:
     return Decomposition(np.asarray(w_hat, np.float64), L1, L2, w_hat - L1 @ L2, s)
 
 
-def refine_lowrank(x_cal, w, lam32, rank: int, fmt: str, iters: int, gs_x=1.0, scale_dtype="bf16"):
+def refine_lowrank(x_cal, w, lam32, rank: int, fmt: str, iters: int, gs_x=1.0, scale_dtype="bf16",
+                   gptq: bool = False, gptq_damp: float = G.DAMP):
     """Iterative refinement of the low-rank branch: iterate 0 is the plain SVD split
     (prepare_operands); iterate t >= 1 re-decomposes W_hat - Q(R_{t-1}) (redecompose) and
     re-quantizes R_t; "then picking the result with the smallest error" -- the iterate with the
     smallest calibration_error (the App. D objective, reading Q4); ties -> the earlier iterate.
+    With gptq=True every iterate's residual is quantized by GPTQ on x_cal.
     Returns (best t, Operands of the best iterate, [objective per iterate], [Decomposition per iterate])."""
     if iters < 0:
         raise ValueError("iters must be >= 0")
     lam32 = np.asarray(lam32, dtype=F32)
     d = decompose(w, lam32, rank)
-    ops = prepare_operands(w, lam32, rank, fmt, gs_x=gs_x, scale_dtype=scale_dtype, decomp=d)
+    ops = prepare_operands(w, lam32, rank, fmt, gs_x=gs_x, scale_dtype=scale_dtype, decomp=d,
+                           gptq_x=x_cal if gptq else None, gptq_damp=gptq_damp)
     all_ops, errs, decs = [ops], [calibration_error(x_cal, w, ops)], [d]
     for _ in range(iters):
         d = redecompose(d.w_hat, dequantize_residual(ops), rank)
-        ops = prepare_operands(w, lam32, rank, fmt, gs_x=gs_x, scale_dtype=scale_dtype, decomp=d)
+        ops = prepare_operands(w, lam32, rank, fmt, gs_x=gs_x, scale_dtype=scale_dtype, decomp=d,
+                               gptq_x=x_cal if gptq else None, gptq_damp=gptq_damp)
         all_ops.append(ops)
         errs.append(calibration_error(x_cal, w, ops))
         decs.append(d)

@@ -89,9 +89,9 @@ _sig = {
     "svdq_search_alpha_workspace": [_I32, _I64, _I64, _I64, _I32, _SZ],
     "svdq_search_alpha": [_P, _I32, _I64, _I64, _P, _I64, _I64, _I32, _I32, _I32, C.c_float, C.POINTER(C.c_float),
                           _I32, C.POINTER(C.c_float), _P, C.POINTER(C.c_double), _P, C.c_size_t, _P],
-    "svdq_refine_lowrank_workspace": [_I32, _I64, _I64, _I64, _I32, _SZ],
-    "svdq_refine_lowrank": [_P, _I32, _I64, _I64, _P, _P, _I64, _I64, _I32, _I32, _I32, C.c_float, _I32, _LP,
-                            C.POINTER(C.c_int32), C.POINTER(C.c_double), _P, C.c_size_t, _P],
+    "svdq_refine_lowrank_workspace": [_I32, _I64, _I64, _I64, _I32, _I32, _SZ],
+    "svdq_refine_lowrank": [_P, _I32, _I64, _I64, _P, _P, _I64, _I64, _I32, _I32, _I32, C.c_float, _I32, _I32,
+                            C.c_float, _LP, C.POINTER(C.c_int32), C.POINTER(C.c_double), _P, C.c_size_t, _P],
     "svdq_quantize_residual_gptq_workspace": [_I64, _I64, _I64, _SZ],
     "svdq_quantize_residual_gptq": [_P, _I64, _I64, _I32, _I32, _P, _I32, _I64, _I64, _P, C.c_float, _P, _P,
                                     C.POINTER(C.c_float), _P, C.c_size_t, _P],
@@ -373,29 +373,31 @@ def svdq_search_alpha(X_cal, W, rank: int, fmt: str, grid, scale_dtype: str = "b
     return a.value, lam, list(obj)
 
 
-def svdq_refine_lowrank_workspace(fmt: str, M_cal: int, K: int, N: int, rank: int) -> int:
+def svdq_refine_lowrank_workspace(fmt: str, M_cal: int, K: int, N: int, rank: int, gptq: bool = False) -> int:
     wsb = C.c_size_t()
-    _check(_lib.svdq_refine_lowrank_workspace(FMT[fmt], M_cal, K, N, rank, C.byref(wsb)),
+    _check(_lib.svdq_refine_lowrank_workspace(FMT[fmt], M_cal, K, N, rank, int(gptq), C.byref(wsb)),
            "svdq_refine_lowrank_workspace")
     return wsb.value
 
 
 def svdq_refine_lowrank(X_cal, W, lam, rank: int, fmt: str, iters: int, scale_dtype: str = "bf16",
-                        gs_x: float = 1.0, bias=None, stream=None):
+                        gs_x: float = 1.0, bias=None, gptq: bool = False, damp: float = 0.01, stream=None):
     """Iterative low-rank refinement on the GPU.  X_cal: [M_cal, K] bf16/fp16, W: [K, N] fp32,
-    lam: [K] fp32 (CUDA).  Returns (QuantizedLinear of the best iterate, best index, objectives list)."""
+    lam: [K] fp32 (CUDA); gptq=True quantizes each iterate's residual by GPTQ.
+    Returns (QuantizedLinear of the best iterate, best index, objectives list)."""
     M, K = X_cal.shape
     N = W.shape[1]
     layer = QuantizedLinear.empty(fmt, K, N, rank, device=X_cal.device, scale_dtype=scale_dtype,
                                   bias=bias, gs_x=gs_x)
-    wsb = svdq_refine_lowrank_workspace(fmt, M, K, N, rank)
+    wsb = svdq_refine_lowrank_workspace(fmt, M, K, N, rank, gptq)
     ws = torch.empty(wsb, dtype=torch.uint8, device=X_cal.device)
     obj = (C.c_double * (iters + 1))()
     best = C.c_int32()
     Wc = W.contiguous().float()
     lam = lam.contiguous().float()
     _check(_lib.svdq_refine_lowrank(_ptr(X_cal), DTYPE[DTYPE_OF_TORCH[X_cal.dtype]], M, X_cal.stride(0), _ptr(Wc),
-                                    _ptr(lam), K, N, rank, FMT[fmt], DTYPE[scale_dtype], gs_x, iters, layer.ref,
+                                    _ptr(lam), K, N, rank, FMT[fmt], DTYPE[scale_dtype], gs_x, iters, int(gptq), damp,
+                                    layer.ref,
                                     C.byref(best), obj, _ptr(ws), wsb, _stream(stream)), "svdq_refine_lowrank")
     layer.gs_w = layer.view.gs_w
     layer.gs_x = layer.view.gs_x

@@ -257,20 +257,26 @@ svdq_status svdq_search_alpha(const void *X_cal, int32_t x_dtype, int64_t M_cal,
 
 // ---------------------------------------------------------------- iterative refinement
 svdq_status svdq_refine_lowrank_workspace(int32_t fmt, int64_t M_cal, int64_t K, int64_t N, int32_t rank,
-                                          size_t *ws_bytes) {
+                                          int32_t use_gptq, size_t *ws_bytes) {
   if (!ws_bytes) return svdq::report_error(SVDQ_ERR_INVALID_ARGUMENT, "null output");
   if (M_cal < 1) return svdq::report_error(SVDQ_ERR_SHAPE, "M_cal must be >= 1");
   AlphaWs w;
   svdq_status st = alpha_ws(fmt, M_cal, K, N, rank, &w, true);
   if (st != SVDQ_OK) return st;
   *ws_bytes = w.total;
+  if (use_gptq) {
+    const int glw = svdq::gptq_potrf_lwork(K);
+    if (glw < 0) return svdq::report_error(SVDQ_ERR_CUDA, "cusolver potrf bufferSize failed");
+    *ws_bytes += svdq::gptq_workspace_bytes(M_cal, K, N, glw);
+  }
   return SVDQ_OK;
 }
 
 svdq_status svdq_refine_lowrank(const void *X_cal, int32_t x_dtype, int64_t M_cal, int64_t ldx, const float *W,
                                 const float *lambda, int64_t K, int64_t N, int32_t rank, int32_t fmt,
-                                int32_t scale_dtype, float gs_x, int32_t iters, svdq_linear *dst, int32_t *best_out,
-                                double *objective_out, void *ws, size_t ws_bytes, void *stream) {
+                                int32_t scale_dtype, float gs_x, int32_t iters, int32_t use_gptq, float damp,
+                                svdq_linear *dst, int32_t *best_out, double *objective_out, void *ws, size_t ws_bytes,
+                                void *stream) {
   if (!X_cal || !W || !lambda || !dst || !best_out || !objective_out || !ws)
     return svdq::report_error(SVDQ_ERR_INVALID_ARGUMENT, "null pointer");
   if (iters < 0) return svdq::report_error(SVDQ_ERR_INVALID_ARGUMENT, "iters must be >= 0");
@@ -281,9 +287,12 @@ svdq_status svdq_refine_lowrank(const void *X_cal, int32_t x_dtype, int64_t M_ca
   AlphaWs w;
   svdq_status st = alpha_ws(fmt, M_cal, K, N, rank, &w, true);
   if (st != SVDQ_OK) return st;
-  if (ws_bytes < w.total) return svdq::report_error(SVDQ_ERR_WORKSPACE, "workspace too small");
+  size_t need = 0;
+  if ((st = svdq_refine_lowrank_workspace(fmt, M_cal, K, N, rank, use_gptq, &need)) != SVDQ_OK) return st;
+  if (ws_bytes < need) return svdq::report_error(SVDQ_ERR_WORKSPACE, "workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint8_t *base = static_cast<uint8_t *>(ws);
+  const svdq::GptqArgs gq{X_cal, x_dtype, M_cal, ldx, damp};
   float *y = reinterpret_cast<float *>(base + w.y);
   float *yref = reinterpret_cast<float *>(base + w.yref);
   float *xf = reinterpret_cast<float *>(base + w.xf);
@@ -335,7 +344,8 @@ svdq_status svdq_refine_lowrank(const void *X_cal, int32_t x_dtype, int64_t M_ca
       return svdq::report_error(SVDQ_ERR_CUDA, "dequantize residual");
     if ((st = svdq::quantize_weights_impl(W, SVDQ_FP32, lambda, K, N, rank, fmt, scale_dtype, gs_x, nullptr, nullptr,
                                           &L, base + w.qws, w.qws_b, stream, t > 0 ? deq : nullptr,
-                                          t > 0 ? tgt : nullptr, nullptr, nullptr)) != SVDQ_OK)
+                                          t > 0 ? tgt : nullptr, use_gptq ? &gq : nullptr,
+                                          use_gptq ? base + w.total : nullptr)) != SVDQ_OK)
       return st;
     if ((st = objective(&L, X_cal, x_dtype, M_cal, ldx, base + w.xq, base + w.xs,
                         reinterpret_cast<uint16_t *>(base + w.xl1), y, yref, err, s, &objective_out[t])) != SVDQ_OK)

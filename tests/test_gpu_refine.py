@@ -93,3 +93,18 @@ def test_refine_rank0_and_errors():
     assert best == 0 and obj[0] == obj[1] == obj[2]
     with pytest.raises(P.SvdqError):
         P.svdq_refine_lowrank(X, W, L, 16, "nvfp4", -1)
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+def test_refine_with_gptq_matches_oracle(fmt):
+    need_cuda()
+    import torch
+    import paper_2411_05007_b200 as P
+    x, w, lam = _case(7)
+    X, W, L = _dev(torch, x, w, lam)
+    layer, best, obj = P.svdq_refine_lowrank(X, W, L, 16, fmt, 2, gptq=True)
+    _, _, errs, _ = S.refine_lowrank(x, w, lam, 16, fmt, 2, gptq=True)
+    np.testing.assert_allclose(obj, errs, rtol=3e-2)
+    _, _, obj_rtn = P.svdq_refine_lowrank(X, W, L, 16, fmt, 2)
+    assert min(obj) < min(obj_rtn)
+    np.testing.assert_allclose(_objective(P, torch, layer, X, W), obj[best], rtol=1e-3)

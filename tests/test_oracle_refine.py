@@ -125,3 +125,13 @@ def test_selection_and_improvement(fmt):
         assert errs[best] == min(errs) and best == errs.index(min(errs))
         assert errs[best] < errs[0]
         assert S.calibration_error(x, w, ops) == errs[best]
+
+
+def test_refine_with_gptq_iterate0_is_gptq_split():
+    """gptq=True: iterate 0 is the plain split with the GPTQ residual, and the selection holds."""
+    x, w = _cal(seed=20)
+    lam = S.compute_smoothing(x, w, 0.5)
+    best, ops, errs, decs = S.refine_lowrank(x, w, lam, 8, "int4", 2, gptq=True)
+    ref = S.prepare_operands(w, lam, 8, "int4", gptq_x=x)
+    assert errs[0] == S.calibration_error(x, w, ref)
+    assert errs[best] == min(errs)
