@@ -167,6 +167,30 @@ svdq_status svdq_quantize_residual(const float *R, int64_t K, int64_t N, int32_t
 /* Workspace bytes for svdq_quantize_weights. */
 svdq_status svdq_quantize_weights_workspace(int64_t K, int64_t N, int32_t rank, size_t *ws_bytes);
 
+/* Layer-boundary fusion (P:165 / P:174's fusion argument carried to the next
+ * layer): grouped K2 (CTA-pair NVFP4 kernel, n = 1..4 problems) whose epilogue also runs the NEXT
+ * layer's K1 on its own output, so the next layer needs no K1 launch and no re-read of Y:
+ *   y = bf16(fl32(alpha * acc) + bias)            (this layer's output, stored to Y[i] if non-NULL)
+ *   a = y (act 0) | bf16(gelu_tanh(y)) (act 1)    (reading N1; MLP-up -> MLP-down)
+ *   xq_next / xs_next = K1's NVFP4 codes / scale factors of a with nexts[i]'s lambda_inv and gs_x
+ *   xl1_next = bf16(a L1s_next^T)                 (partial fp32 sums per 256-row block and CTA pair,
+ *                                                   reduced in fixed order by a second kernel)
+ * i.e. exactly svdq_quantize_act_lowrank_down(nexts[i], a) -- codes / scales bit-identical for
+ * act 0; xl1 within K1's tolerance.  Requirements: layers and nexts NVFP4, nexts[i]->K ==
+ * layers[i]->N, nexts[i]->rank in {0, 16, 32}; Y (if given) bf16 with ldy = N.  xq_next[i]:
+ * [dev] [M][N/2]; xs_next[i]: [dev] K1's scale-factor buffer for (M, K = N); xl1_next[i]: [dev]
+ * [M][rank_next] bf16.  ws: [dev] of svdq_gemm_fused_next_workspace bytes (0 when every
+ * next rank is 0).  Enqueue only (two launches when any next rank > 0).                  */
+svdq_status svdq_gemm_fused_next_workspace(int32_t n, const svdq_linear *const *layers, const int64_t *M,
+                                           const svdq_linear *const *nexts, size_t *ws_bytes);
+svdq_status svdq_gemm_w4a4_lowrank_up_fused_next(int32_t n, const svdq_linear *const *layers,
+                                                 const uint8_t *const *xq, const uint8_t *const *xs,
+                                                 const uint16_t *const *xl1, const int64_t *M, void *const *Y,
+                                                 const svdq_linear *const *nexts, int32_t act,
+                                                 uint8_t *const *xq_next, uint8_t *const *xs_next,
+                                                 uint16_t *const *xl1_next, void *ws, size_t ws_bytes,
+                                                 void *stream);
+
 /* Full offline weight preparation:
  *   lambda_inv = fl32(1/lambda); W_hat = diag(lambda) W;  SVD of W_hat (cuBLAS/cuSOLVER fp64
  *   Gram + eigensolver) unless L1_opt / L2_opt are given ([dev] fp32 [K][rank] / [rank][N]);

@@ -397,3 +397,31 @@ def refine_lowrank(x_cal, w, lam32, rank: int, fmt: str, iters: int, gs_x=1.0, s
         decs.append(d)
     best = min(range(len(errs)), key=lambda t: (errs[t], t))
     return best, all_ops[best], errs, decs
+
+
+# --------------------------------------------------------------------------
+# Layer boundary: the next layer's K1 applied to this layer's stored output
+# --------------------------------------------------------------------------
+def gelu_tanh(v) -> np.ndarray:
+    """GELU, tanh form (FLUX's MLP activation; the paper does not restate it), in fp64:
+    0.5 v (1 + tanh(sqrt(2/pi) (v + 0.044715 v^3)))."""
+    v = np.asarray(v, np.float64)
+    return 0.5 * v * (1.0 + np.tanh(np.sqrt(2.0 / np.pi) * (v + 0.044715 * v ** 3)))
+
+
+def next_layer_input(y_stored, act: str, dtype: str = "bf16") -> np.ndarray:
+    """The next linear's 16-bit input from this layer's stored output (reading N1): identity, or
+    round16(gelu_tanh(y)) for MLP-up -> MLP-down."""
+    if act == "none":
+        return np.asarray(y_stored, np.float64)
+    if act == "gelu_tanh":
+        return F.round16(gelu_tanh(y_stored), dtype)
+    raise ValueError(act)
+
+
+def fused_next(y64, ops_next: Operands, act: str, dtype: str = "bf16") -> QuantAct:
+    """What an epilogue-fused K2 hands to the next layer: K1 (quantize_activation) of
+    next_layer_input(round_output(y64)) -- P:165 / P:174's fusion argument carried across the
+    layer boundary."""
+    a = next_layer_input(round_output(y64, dtype), act, dtype)
+    return quantize_activation(a, ops_next)

@@ -38,6 +38,7 @@ EXPORTS = [
     "svdq_act_buffer_sizes", "svdq_weight_buffer_sizes", "svdq_quantize_act_lowrank_down",
     "svdq_quantize_act_lowrank_down_grouped",
     "svdq_gemm_w4a4_lowrank_up", "svdq_gemm_w4a4_lowrank_up_grouped", "svdq_linear_forward",
+    "svdq_gemm_fused_next_workspace", "svdq_gemm_w4a4_lowrank_up_fused_next",
     "svdq_quantize_residual",
     "svdq_quantize_weights_workspace", "svdq_quantize_weights", "svdq_lora_fuse",
     "svdq_search_alpha_workspace", "svdq_search_alpha",
@@ -78,6 +79,10 @@ _sig = {
     "svdq_gemm_w4a4_lowrank_up": [_LP, _P, _P, _P, _I64, _P, _I32, _I64, _P],
     "svdq_quantize_act_lowrank_down_grouped": [_I32, C.POINTER(_LP), C.POINTER(_P), _I32, C.POINTER(_I64),
                                                C.POINTER(_I64), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), _P],
+    "svdq_gemm_fused_next_workspace": [_I32, C.POINTER(_LP), C.POINTER(_I64), C.POINTER(_LP), _SZ],
+    "svdq_gemm_w4a4_lowrank_up_fused_next": [_I32, C.POINTER(_LP), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
+                                             C.POINTER(_I64), C.POINTER(_P), C.POINTER(_LP), _I32, C.POINTER(_P),
+                                             C.POINTER(_P), C.POINTER(_P), _P, C.c_size_t, _P],
     "svdq_gemm_w4a4_lowrank_up_grouped": [_I32, C.POINTER(_LP), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
                                           C.POINTER(_I64), C.POINTER(_P), _I32, C.POINTER(_I64), _P],
     "svdq_linear_forward": [_LP, _P, _I32, _I64, _I64, _P, _I32, _I64, _P, C.c_size_t, _P],
@@ -263,6 +268,45 @@ def svdq_gemm_w4a4_lowrank_up_grouped(layers, xq, xs, xl1, M, Y, stream=None):
         arr(_I64, list(M)), arr(_P, [y.data_ptr() for y in Y]), DTYPE[ydt.pop()],
         arr(_I64, [y.stride(0) for y in Y]), _stream(stream)), "svdq_gemm_w4a4_lowrank_up_grouped")
     return Y
+
+
+ACT = {"none": 0, "gelu_tanh": 1}
+
+
+def svdq_gemm_fused_next_workspace(layers, M, nexts) -> int:
+    n = len(layers)
+    arr = lambda T, vals: (T * n)(*vals)
+    wsb = C.c_size_t()
+    _check(_lib.svdq_gemm_fused_next_workspace(n, arr(_LP, [C.pointer(l.view) for l in layers]), arr(_I64, list(M)),
+                                               arr(_LP, [C.pointer(l.view) for l in nexts]), C.byref(wsb)),
+           "svdq_gemm_fused_next_workspace")
+    return wsb.value
+
+
+def svdq_gemm_w4a4_lowrank_up_fused_next(layers, xq, xs, xl1, M, nexts, act="none", Y=None, ws=None, stream=None):
+    """K2 of layers[i] whose epilogue also runs nexts[i]'s K1 on its (activated) bf16 output
+    (SURVEY 8(f) row 1).  Y: list of bf16 [M, N] tensors or None (no store).  Returns
+    (xq_next, xs_next, xl1_next) lists, the buffers svdq_quantize_act_lowrank_down(nexts[i], a) fills."""
+    n = len(layers)
+    dev = xq[0].device
+    outs = []
+    for L, Nx, m in zip(layers, nexts, M):
+        bq, bs, bl = svdq_act_buffer_sizes(Nx.fmt, m, Nx.K, Nx.rank)
+        outs.append((torch.empty(bq, dtype=torch.uint8, device=dev), torch.empty(bs, dtype=torch.uint8, device=dev),
+                     torch.empty(max(bl // 2, 8), dtype=torch.int16, device=dev)))
+    need = svdq_gemm_fused_next_workspace(layers, M, nexts)
+    if ws is None:
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
+    arr = lambda T, vals: (T * n)(*vals)
+    Yp = [None if Y is None or Y[i] is None else Y[i].data_ptr() for i in range(n)]
+    _check(_lib.svdq_gemm_w4a4_lowrank_up_fused_next(
+        n, arr(_LP, [C.pointer(l.view) for l in layers]), arr(_P, [x.data_ptr() for x in xq]),
+        arr(_P, [x.data_ptr() for x in xs]), arr(_P, [x.data_ptr() if x is not None else None for x in xl1]),
+        arr(_I64, list(M)), arr(_P, Yp), arr(_LP, [C.pointer(l.view) for l in nexts]), ACT[act],
+        arr(_P, [o[0].data_ptr() for o in outs]), arr(_P, [o[1].data_ptr() for o in outs]),
+        arr(_P, [o[2].data_ptr() for o in outs]), _ptr(ws), ws.numel(), _stream(stream)),
+        "svdq_gemm_w4a4_lowrank_up_fused_next")
+    return [o[0] for o in outs], [o[1] for o in outs], [o[2] for o in outs]
 
 
 def forward_workspace_bytes(layer: QuantizedLinear, M: int) -> int:

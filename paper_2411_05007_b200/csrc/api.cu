@@ -332,9 +332,10 @@ struct K2Prep {
   bool pair;
 };
 svdq_status prepare_k2(const svdq_linear *L, const uint8_t *xq, const uint8_t *xs, const uint16_t *xl1, int64_t M,
-                       void *Y, int32_t y_dtype, int64_t ldy, bool force_pair, K2Prep *out) {
+                       void *Y, int32_t y_dtype, int64_t ldy, bool force_pair, K2Prep *out, void *y_map_base = nullptr) {
   svdq_status st = check_linear(L, true);
   if (st != SVDQ_OK) return st;
+  if (!Y && y_map_base) Y = y_map_base;     // fused launch without a Y store: the map is never used
   if (!xq || !xs || !Y || (L->rank > 0 && !xl1)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null buffer");
   if (y_dtype != SVDQ_BF16 && y_dtype != SVDQ_FP16 && y_dtype != SVDQ_FP32)
     return fail(SVDQ_ERR_INVALID_ARGUMENT, "bad Y dtype");
@@ -455,6 +456,119 @@ svdq_status svdq_gemm_w4a4_lowrank_up_grouped(int32_t n, const svdq_linear *cons
   cudaError_t e = launch_k2_nvfp4_2sm_group(g, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "grouped K2 launch");
   ++g_launches;
+  return SVDQ_OK;
+}
+
+// ---------------------------------------------------------------- layer-boundary fusion
+namespace {
+// Fill the grouped launch for the fused K2 (validation shared by the workspace query and the call).
+svdq_status prepare_fused(int32_t n, const svdq_linear *const *layers, const uint8_t *const *xq,
+                          const uint8_t *const *xs, const uint16_t *const *xl1, const int64_t *M, void *const *Y,
+                          const svdq_linear *const *nexts, int32_t act, uint8_t *const *xq_next,
+                          uint8_t *const *xs_next, K2PairArgs *g, size_t *part_bytes, size_t part_off[]) {
+  if (n < 1 || n > kMaxGroup) return fail(SVDQ_ERR_INVALID_ARGUMENT, "group size must be 1..%d", kMaxGroup);
+  if (!layers || !nexts || !M) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null array");
+  if (act != 0 && act != 1) return fail(SVDQ_ERR_INVALID_ARGUMENT, "act must be 0 (identity) or 1 (GELU tanh)");
+  std::memset(g, 0, sizeof(*g));
+  g->n = n;
+  int64_t tiles = 0;
+  for (int i = 0; i < n; ++i) {
+    const svdq_linear *L = layers[i], *Nx = nexts[i];
+    if (!L || !Nx) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null layer %d", i);
+    svdq_status st = check_linear(Nx, true);
+    if (st != SVDQ_OK) return st;
+    if (L->fmt != SVDQ_FMT_NVFP4 || Nx->fmt != SVDQ_FMT_NVFP4)
+      return fail(SVDQ_ERR_UNSUPPORTED, "fused next-layer quantization is NVFP4 -> NVFP4");
+    if (Nx->K != L->N) return fail(SVDQ_ERR_SHAPE, "next->K (%lld) != N (%lld)", (long long)Nx->K, (long long)L->N);
+    if (Nx->rank != 0 && Nx->rank != 16 && Nx->rank != 32)
+      return fail(SVDQ_ERR_RANK, "fused next-layer rank must be 0, 16 or 32");
+    if (M[i] < 1) return fail(SVDQ_ERR_SHAPE, "M must be >= 1");
+    tiles += ((M[i] + 255) / 256) * ((L->N + kNvfp4PairBN - 1) / kNvfp4PairBN);
+  }
+  const int np = k2_pair_count(tiles);
+  size_t off = 0;
+  for (int i = 0; i < n; ++i) {
+    const svdq_linear *Nx = nexts[i];
+    const int64_t nt = (layers[i]->N + kNvfp4PairBN - 1) / kNvfp4PairBN;
+    const int slots = k2_next_slots(nt, tiles, np);
+    part_off[i] = off;
+    if (Nx->rank) off += (static_cast<size_t>((M[i] + 255) / 256) * slots * 2 * 256 * Nx->rank * 4 + 255) & ~size_t(255);
+    K2Params &p = g->pr[i].p;
+    p.nx_slots = slots;
+  }
+  *part_bytes = off;
+  if (!xq) return SVDQ_OK;                   // workspace query
+  if (!xs || !xl1 || !Y || !xq_next || !xs_next) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null array");
+  for (int i = 0; i < n; ++i) {
+    const svdq_linear *Nx = nexts[i];
+    if (!xq_next[i] || !xs_next[i]) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null next-layer buffer %d", i);
+    if (!aligned16(xq_next[i])) return fail(SVDQ_ERR_ALIGNMENT, "xq_next must be 16-byte aligned");
+    K2Prep k;
+    const int slots = g->pr[i].p.nx_slots;
+    svdq_status st = prepare_k2(layers[i], xq[i], xs[i], xl1[i], M[i], Y[i], SVDQ_BF16, layers[i]->N, true, &k,
+                                xq_next[i]);
+    if (st != SVDQ_OK) return st;
+    g->pr[i].a = k.maps.a;
+    g->pr[i].b = k.maps.b;
+    g->pr[i].xl1 = k.maps.xl1;
+    g->pr[i].l2 = k.maps.l2;
+    g->pr[i].sfa = k.sfa_map;
+    g->pr[i].sfb = k.sfb_map;
+    g->pr[i].y = k.maps.y;
+    K2Params &p = g->pr[i].p;
+    p = k.p;
+    p.Y = Y[i];
+    p.fuse = 1;
+    p.nx_act = act;
+    p.nx_r = Nx->rank;
+    p.nx_gs = Nx->gs_x;
+    p.nx_lam_inv = Nx->lambda_inv;
+    p.nx_l1s = Nx->l1s;
+    p.nx_xq = xq_next[i];
+    p.nx_sf = xs_next[i];
+    p.nx_slots = slots;
+  }
+  return SVDQ_OK;
+}
+}  // namespace
+
+svdq_status svdq_gemm_fused_next_workspace(int32_t n, const svdq_linear *const *layers, const int64_t *M,
+                                           const svdq_linear *const *nexts, size_t *ws_bytes) {
+  if (!ws_bytes) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null output");
+  K2PairArgs g;
+  size_t off[kMaxGroup];
+  return prepare_fused(n, layers, nullptr, nullptr, nullptr, M, nullptr, nexts, 0, nullptr, nullptr, &g, ws_bytes,
+                       off);
+}
+
+svdq_status svdq_gemm_w4a4_lowrank_up_fused_next(int32_t n, const svdq_linear *const *layers,
+                                                 const uint8_t *const *xq, const uint8_t *const *xs,
+                                                 const uint16_t *const *xl1, const int64_t *M, void *const *Y,
+                                                 const svdq_linear *const *nexts, int32_t act,
+                                                 uint8_t *const *xq_next, uint8_t *const *xs_next,
+                                                 uint16_t *const *xl1_next, void *ws, size_t ws_bytes,
+                                                 void *stream) {
+  K2PairArgs g;
+  size_t need = 0, off[kMaxGroup];
+  if (!xq) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null array");
+  svdq_status st = prepare_fused(n, layers, xq, xs, xl1, M, Y, nexts, act, xq_next, xs_next, &g, &need, off);
+  if (st != SVDQ_OK) return st;
+  if (need && (!ws || ws_bytes < need)) return fail(SVDQ_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  for (int i = 0; i < n; ++i) {
+    if (g.pr[i].p.nx_r) {
+      if (!xl1_next || !xl1_next[i]) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null xl1_next %d", i);
+      g.pr[i].p.nx_part = reinterpret_cast<float *>(static_cast<uint8_t *>(ws) + off[i]);
+    }
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = launch_k2_nvfp4_2sm_group(g, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fused K2 launch");
+  ++g_launches;
+  for (int i = 0; i < n; ++i) {
+    if (!g.pr[i].p.nx_r) continue;
+    if ((e = launch_k2_next_reduce(g, i, xl1_next[i], s)) != cudaSuccess) return cuda_fail(e, "xl1_next reduce");
+    ++g_launches;
+  }
   return SVDQ_OK;
 }
 

@@ -95,6 +95,19 @@ struct K2Params {
   int scale_bf16;         // INT4 scales
   int32_t *dbg_acc;       // INT4 debug: per-group int32 accumulators [K/64][M][N]
   int w8;                 // W8A8 (kind::i8 over the whole K; sfa / sfb are fp32 [M] / [N])
+  // Layer-boundary fusion (CTA-pair kernel only): the epilogue also runs the
+  // next layer's K1 on its own bf16 output -- NVFP4 codes / scale factors of
+  // act(Y) * lambda_inv_next and partial X L1s_next^T sums (reduced by launch_k2_next_reduce).
+  int fuse;               // 1: on (this problem's tiles are walked n-fastest)
+  int nx_act;             // 0 identity, 1 GELU (tanh form)
+  int nx_r;               // next layer's rank: 0, 16 or 32
+  float nx_gs;            // next layer's gs_x
+  const float *nx_lam_inv;    // [N]
+  const uint16_t *nx_l1s;     // [nx_r][N] bf16
+  uint8_t *nx_xq;             // [M][N/2]
+  uint8_t *nx_sf;             // 128x4 layout over (M rows, K = N)
+  float *nx_part;             // [ceil(M/256)][nx_slots][2][256][nx_r] fp32 partial sums
+  int nx_slots;
 };
 struct K2Maps {
   CUtensorMap a, b, xl1, l2, y;   // y: output store map, box {64 B of columns, 32 rows}, SW64
@@ -116,8 +129,17 @@ struct K2PairArgs {
   K2PairProblem pr[kMaxGroup];
   int n;
   int tile_begin[kMaxGroup + 1];
+  int contig;             // set by the launcher: pairs take contiguous tile ranges (fused launches)
+  int npairs;             // set by the launcher
 };
 cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &args, cudaStream_t s);
+// CTA pairs the grouped launch will use for `tiles` tiles
+int k2_pair_count(int64_t tiles);
+// Slots per 256-row block of a fused problem's partial-sum buffer (upper bound for any pair
+// count <= k2_pair_count(tiles))
+int k2_next_slots(int64_t n_tiles_of_problem, int64_t tiles, int npairs);
+// xl1_next[m][j] = bf16(sum over the partial slots of m's 256-row block, in slot order)
+cudaError_t launch_k2_next_reduce(const K2PairArgs &g, int i, uint16_t *xl1_next, cudaStream_t s);
 constexpr int kNvfp4PairBN = 192;
 constexpr int kInt4BN = 128;             // N tile of the INT4 GEMM
 cudaError_t launch_k2_int4(const K2Maps &maps, const K2Params &p, cudaStream_t s);

@@ -7,6 +7,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include "formats.cuh"
 #include "sm100.cuh"
 
 namespace svdq {
@@ -136,6 +137,119 @@ __device__ __forceinline__ void epilogue_tile_direct(uint32_t tmem_acc_lane, con
         for (int e = 0; e < 8; ++e) o[e] = __fadd_rn(__fmul_rn(alpha, __uint_as_float(r[i][8 * c + e])), bs[8 * c + e]);
         reinterpret_cast<uint4 *>(yp)[c] = make_uint4(pack2(o[0], o[1], y_dtype), pack2(o[2], o[3], y_dtype),
                                                       pack2(o[4], o[5], y_dtype), pack2(o[6], o[7], y_dtype));
+      }
+    }
+  }
+}
+
+// GELU, tanh form, in fp32 (reading N1; the oracle evaluates it in fp64)
+__device__ __forceinline__ float gelu_tanh_f(float v) {
+  const float u = 0.7978845608028654f * (v + 0.044715f * v * v * v);
+  return 0.5f * v * (1.0f + tanhf(u));
+}
+
+// epilogue_tile plus the next layer's K1.  Lane l of the warp owns row
+// row0 + l; for each of its 32-column blocks it forms the stored bf16 output y, the next
+// layer's input a = y or bf16(gelu(y)), x_hat = fl32(a * lambda_inv_next) and, per 16-column
+// group, the NVFP4 scale factor and codes with K1's exact recipe (reading Q10), and
+// accumulates xacc[j] += a * L1s_next[j][col] in fp32.  tmY == nullptr: Y is not stored.
+// lamn_s / l1n_s: the tile's 192 lambda_inv_next values (0 past N) and the [32][192] bf16 L1s
+// slice (0 past N).  Rows >= M store no codes; their scale factors (padding rows of the 128x4
+// layout) are written 0x00 (reading Q22).
+template <int NCOLS, int NWQ, int NBUF = 2, typename Release>
+__device__ __forceinline__ void epilogue_tile_next(uint32_t tmem_acc_lane, const float *bias_s, float alpha,
+                                                   const CUtensorMap *tmY, int32_t row0, int32_t col0, int sub,
+                                                   uint8_t *stage, int &buf, int lane, Release release,
+                                                   const K2Params &p, const float *lamn_s, const uint16_t *l1n_s,
+                                                   float (&xacc)[32]) {
+  constexpr int NB = NCOLS / (32 * NWQ);
+  static_assert(NCOLS % (32 * NWQ) == 0, "column split");
+  uint32_t r[NB][32];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) tmem_ld_32x32b_x32(tmem_acc_lane + (sub + i * NWQ) * 32, r[i]);
+  tmem_ld_wait();
+  release();
+  const uint32_t sw = static_cast<uint32_t>((lane >> 1) & 3);
+  const int64_t row = static_cast<int64_t>(row0) + lane;
+  const int64_t N = p.N;
+  const float t6 = __fmul_rn(__fdiv_rn(1.0f, p.nx_gs), __fdiv_rn(1.0f, 6.0f));
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const int cb = sub + i * NWQ;
+    const float *bs = bias_s + cb * 32;
+    float a[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      const float o = __fadd_rn(__fmul_rn(alpha, __uint_as_float(r[i][e])), bs[e]);
+      const float y = __bfloat162float(__float2bfloat16_rn(o));
+      r[i][e] = __float_as_uint(y);
+      a[e] = p.nx_act ? __bfloat162float(__float2bfloat16_rn(gelu_tanh_f(y))) : y;
+    }
+    if (tmY) {                                              // the layer's own output, as epilogue_tile
+      uint8_t *sb = stage + (NBUF == 2 ? buf * 2048 : 0);
+      if (lane == 0) bulk_wait_group_read<NBUF - 1>();
+      __syncwarp();
+      uint8_t *rowp = sb + lane * 64;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float *v = reinterpret_cast<const float *>(&r[i][8 * c]);
+        *reinterpret_cast<uint4 *>(rowp + ((c ^ sw) * 16)) =
+            make_uint4(pack2(v[0], v[1], 0), pack2(v[2], v[3], 0), pack2(v[4], v[5], 0), pack2(v[6], v[7], 0));
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmY, sb, col0 + cb * 32, row0);
+        bulk_commit_group();
+      }
+      buf ^= 1;
+    }
+    // next layer's NVFP4 codes and scale factors, two 16-column groups
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t gcol = static_cast<int64_t>(col0) + cb * 32 + 16 * h;
+      if (gcol >= N) break;
+      float xh[16];
+      float amax = 0.f;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        xh[e] = __fmul_rn(a[16 * h + e], lamn_s[cb * 32 + 16 * h + e]);
+        amax = fmaxf(amax, fabsf(xh[e]));
+      }
+      const uint32_t sf = e4m3_rn_sat(__fmul_rn(amax, t6));
+      const float sd = e4m3_to_f32(sf);
+      const float qinv = sd == 0.f ? 0.f : __fdiv_rn(1.0f, __fmul_rn(sd, p.nx_gs));
+      float q0[8], q1[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        q0[e] = __fmul_rn(xh[e], qinv);
+        q1[e] = __fmul_rn(xh[8 + e], qinv);
+      }
+      if (row < p.M) {
+        *reinterpret_cast<uint2 *>(p.nx_xq + row * (N / 2) + gcol / 2) = make_uint2(e2m1x8(q0), e2m1x8(q1));
+        p.nx_sf[sf_offset(row, gcol / 16, N)] = static_cast<uint8_t>(sf);
+      } else if (row < ((p.M + 127) / 128) * 128) {
+        p.nx_sf[sf_offset(row, gcol / 16, N)] = 0;
+      }
+    }
+    // partial X L1s_next^T over this block's 32 columns (zeros past N)
+    if (p.nx_r) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j >= p.nx_r) continue;
+        const uint4 *lp = reinterpret_cast<const uint4 *>(l1n_s + j * NCOLS + cb * 32);
+        float s = xacc[j];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint4 w = lp[c];
+          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            s = fmaf(a[8 * c + 2 * d], __uint_as_float(ww[d] << 16), s);
+            s = fmaf(a[8 * c + 2 * d + 1], __uint_as_float(ww[d] & 0xFFFF0000u), s);
+          }
+        }
+        xacc[j] = s;
       }
     }
   }

@@ -69,6 +69,9 @@ constexpr int EPI_OFF = kStages * STAGE;                 // epilogue staging
 constexpr int EPI_BYTES = SVDQ_BIGSTORE && 3 * 16384 > 8 * 2048 * kEpiBuf ? 3 * 16384 : 8 * 2048 * kEpiBuf;
 constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
 constexpr int SMEM = BAR_OFF + 256 + BN * 4 + 1024;
+// fused launches: + the tile's lambda_inv_next [192] fp32 and L1s_next slice [32][192] bf16
+constexpr int NEXT_OFF = BAR_OFF + 256 + BN * 4;
+constexpr int SMEM_FUSE = SMEM + BN * 4 + 32 * BN * 2;
 static_assert(STAGE % 1024 == 0, "stage alignment");
 static_assert(SF_BASE + 2 * SF_COLS <= 512, "TMEM budget");
 
@@ -109,10 +112,15 @@ __device__ __forceinline__ TileRef locate(const K2PairArgs &g, int t) {
   int i = 0;
   while (i + 1 < g.n && t >= g.tile_begin[i + 1]) ++i;
   const int lt = t - g.tile_begin[i];
+  if (g.pr[i].p.fuse) {                   // n-fastest: a pair's contiguous range stays on few row blocks
+    const int nt = static_cast<int>((g.pr[i].p.N + BN - 1) / BN);
+    return TileRef{i, static_cast<int64_t>(lt / nt) * 256, static_cast<int64_t>(lt % nt) * BN};
+  }
   const int mt = static_cast<int>((g.pr[i].p.M + 255) / 256);
   return TileRef{i, static_cast<int64_t>(lt % mt) * 256, static_cast<int64_t>(lt / mt) * BN};
 }
 
+template <bool kFuse>
 __global__ void __launch_bounds__(320, 1)
     k2_nvfp4_2sm_kernel(const __grid_constant__ K2PairArgs g) {
   extern __shared__ uint8_t smem_raw[];
@@ -131,6 +139,11 @@ __global__ void __launch_bounds__(320, 1)
   const int pair = static_cast<int>(blockIdx.x >> 1);
   const int npairs = static_cast<int>(gridDim.x >> 1);
   const int tiles = g.tile_begin[g.n];
+  // tile walk: strided (t = pair, pair + npairs, ...) or, for fused launches, the contiguous
+  // range [pair * tiles / npairs, (pair + 1) * tiles / npairs)
+  const int t_first = g.contig ? static_cast<int>(static_cast<int64_t>(pair) * tiles / npairs) : pair;
+  const int t_end = g.contig ? static_cast<int>(static_cast<int64_t>(pair + 1) * tiles / npairs) : tiles;
+  const int t_step = g.contig ? 1 : npairs;
   auto nkt_of = [&](int i) { return static_cast<int>((g.pr[i].p.K / 64 + 3) / 4); };
   auto nslab_of = [&](int i) { return (g.pr[i].p.rank + 63) / 64; };
 
@@ -175,9 +188,9 @@ __global__ void __launch_bounds__(320, 1)
 #endif
       // Weight tiles (B, SFB) of the first tile's first ring do not depend on K1: issue them
       // before the programmatic dependency resolves, so they land while K1 finishes.
-      const int pre = (SVDQ_EXP & 4) || pair >= tiles ? 0 : min(kStages, nkt_of(locate(g, pair).i));
+      const int pre = (SVDQ_EXP & 4) || t_first >= t_end ? 0 : min(kStages, nkt_of(locate(g, t_first).i));
       if (pre) {
-        const TileRef tr = locate(g, pair);
+        const TileRef tr = locate(g, t_first);
         const K2PairProblem &pr = g.pr[tr.i];
         for (int kt = 0; kt < pre; ++kt) {
           uint8_t *st = smem + kt * STAGE;
@@ -190,7 +203,7 @@ __global__ void __launch_bounds__(320, 1)
       }
       griddep_wait();                                    // xq / xs / xl1 come from K1
       bool first = true;
-      for (int t = pair; t < tiles; t += npairs) {
+      for (int t = t_first; t < t_end; t += t_step) {
         const TileRef tr = locate(g, t);
         const K2PairProblem &pr = g.pr[tr.i];
         const int nkt = nkt_of(tr.i);
@@ -250,7 +263,7 @@ __global__ void __launch_bounds__(320, 1)
       long long t_acc = 0, t_full = 0;
       const long long t_start = clock64();
 #endif
-      for (int t = pair; t < tiles; t += npairs, ++acc_i) {
+      for (int t = t_first; t < t_end; t += t_step, ++acc_i) {
         const int b = (SVDQ_EXP & 64) ? 0 : acc_i & 1;            // 64: single accumulator (ablation)
         const uint32_t acc_ph = (SVDQ_EXP & 64) ? acc_i & 1 : (acc_i >> 1) & 1;
         const TileRef tr = locate(g, t);
@@ -348,6 +361,9 @@ __global__ void __launch_bounds__(320, 1)
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
     const int et = threadIdx.x - 64;
+    float xacc[32];                                      // fused: partial X L1s_next^T of this row
+#pragma unroll
+    for (int j = 0; j < 32; ++j) xacc[j] = 0.f;
     const uint32_t acc_empty0 = mapa_u32(&acc_empty[0], 0);
     int acc_i = 0;
     int ebuf = 0;
@@ -356,7 +372,7 @@ __global__ void __launch_bounds__(320, 1)
     const long long t_estart = clock64();
 #endif
     griddep_wait();
-    for (int t = pair; t < tiles; t += npairs, ++acc_i) {
+    for (int t = t_first; t < t_end; t += t_step, ++acc_i) {
       const int b = (SVDQ_EXP & 64) ? 0 : acc_i & 1;
       const uint32_t acc_ph = (SVDQ_EXP & 64) ? acc_i & 1 : (acc_i >> 1) & 1;
       const TileRef tr = locate(g, t);
@@ -367,6 +383,15 @@ __global__ void __launch_bounds__(320, 1)
       named_bar(1, 256);
       for (int c = et; c < BN; c += 256)
         bias_s[c] = (p.bias && n0 + c < p.N) ? load_bias(p.bias, p.bias_dtype, n0 + c) : 0.f;
+      if constexpr (kFuse) {
+        float *lamn_s = reinterpret_cast<float *>(smem + NEXT_OFF);
+        uint16_t *l1n_s = reinterpret_cast<uint16_t *>(smem + NEXT_OFF + BN * 4);
+        for (int c = et; c < BN; c += 256) lamn_s[c] = n0 + c < p.N ? p.nx_lam_inv[n0 + c] : 0.f;
+        for (int c = et; c < p.nx_r * BN; c += 256) {
+          const int j = c / BN, col = c % BN;
+          l1n_s[c] = n0 + col < p.N ? p.nx_l1s[static_cast<int64_t>(j) * p.N + n0 + col] : 0;
+        }
+      }
       named_bar(1, 256);
       { K2T_BEGIN(); mbar_wait(&acc_full[b], acc_ph); K2T_ACC(t_ewait); }
       tc_fence_after();
@@ -428,6 +453,46 @@ __global__ void __launch_bounds__(320, 1)
         continue;
       }
 #endif
+      if constexpr (kFuse) {
+        if (p.fuse) {
+          epilogue_tile_next<BN, 2, kEpiBuf>(
+              tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.Y ? tmY : nullptr,
+              static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
+              smem + EPI_OFF + (warp - 2) * 2048 * kEpiBuf, ebuf, lane,
+              [&]() {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(acc_empty0 + b * 8);
+              },
+              p, reinterpret_cast<const float *>(smem + NEXT_OFF),
+              reinterpret_cast<const uint16_t *>(smem + NEXT_OFF + BN * 4), xacc);
+          // leaving this 256-row block (or the range): write the partial X L1s_next^T sums to this
+          // pair's slot; slot = pair - (first pair whose range holds a tile of the block)
+          bool flush = p.nx_r > 0 && t + t_step >= t_end;
+          if (p.nx_r > 0 && !flush) {
+            const TileRef nr = locate(g, t + t_step);
+            flush = nr.i != tr.i || nr.m0 != tr.m0;
+          }
+          if (flush) {
+            const int nt = static_cast<int>((p.N + BN - 1) / BN);
+            const int mb = static_cast<int>(tr.m0 / 256);
+            const int64_t t0 = g.tile_begin[tr.i] + static_cast<int64_t>(mb) * nt;
+            const int pf = static_cast<int>(((t0 + 1) * npairs - 1) / tiles);
+            const int sub = (warp - 2) >> 2;
+            float *dst = p.nx_part + ((((static_cast<int64_t>(mb) * p.nx_slots + (pair - pf)) * 2 + sub) * 256 +
+                                       128 * crank + quad * 32 + lane) *
+                                      p.nx_r);
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              if (j < p.nx_r) {
+                *reinterpret_cast<float4 *>(dst + j) = make_float4(xacc[j], xacc[j + 1], xacc[j + 2], xacc[j + 3]);
+                xacc[j] = xacc[j + 1] = xacc[j + 2] = xacc[j + 3] = 0.f;
+              }
+            }
+          }
+          continue;
+        }
+      }
       epilogue_tile<BN, 2, kEpiBuf>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
                            tmY, static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
                            smem + EPI_OFF + (warp - 2) * 2048 * kEpiBuf, ebuf, lane, [&]() {
@@ -455,7 +520,8 @@ __global__ void __launch_bounds__(320, 1)
 
 cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
   static_assert(SMEM <= 227 * 1024, "smem budget");
-  cudaError_t e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  static_assert(SMEM_FUSE <= 227 * 1024, "smem budget (fused)");
+  cudaError_t e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   if (e != cudaSuccess) return e;
   static int num_sms = 0;
   if (!num_sms) {
@@ -464,11 +530,62 @@ cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   g.tile_begin[0] = 0;
-  for (int i = 0; i < g.n; ++i)
+  bool fuse = false;
+  for (int i = 0; i < g.n; ++i) {
     g.tile_begin[i + 1] = g.tile_begin[i] + static_cast<int>(((g.pr[i].p.M + 255) / 256) * ((g.pr[i].p.N + BN - 1) / BN));
+    fuse = fuse || g.pr[i].p.fuse;
+  }
   const int64_t tiles = g.tile_begin[g.n];
   const int64_t pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  return launch_ex(k2_nvfp4_2sm_kernel, dim3(static_cast<unsigned>(2 * pairs)), dim3(320), SMEM, s, 2u, g);
+  g.contig = fuse ? 1 : 0;
+  g.npairs = static_cast<int>(pairs);
+  if (fuse) {
+    e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_FUSE);
+    if (e != cudaSuccess) return e;
+    return launch_ex(k2_nvfp4_2sm_kernel<true>, dim3(static_cast<unsigned>(2 * pairs)), dim3(320), SMEM_FUSE, s, 2u, g);
+  }
+  return launch_ex(k2_nvfp4_2sm_kernel<false>, dim3(static_cast<unsigned>(2 * pairs)), dim3(320), SMEM, s, 2u, g);
+}
+
+int k2_pair_count(int64_t tiles) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return static_cast<int>(tiles < sms / 2 ? tiles : sms / 2);
+}
+
+int k2_next_slots(int64_t nt, int64_t tiles, int npairs) {
+  const int64_t minlen = npairs > 0 ? tiles / npairs : 1;      // shortest contiguous range
+  return static_cast<int>((nt + (minlen > 0 ? minlen : 1) - 1) / (minlen > 0 ? minlen : 1) + 1);
+}
+
+namespace {
+__global__ void next_reduce_kernel(const float *__restrict__ part, int64_t M, int r, int nt, int slots,
+                                   int64_t tile_begin, int tiles, int npairs, uint16_t *__restrict__ out) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= M * r) return;
+  const int64_t m = idx / r;
+  const int j = static_cast<int>(idx % r);
+  const int mb = static_cast<int>(m / 256);
+  const int64_t t0 = tile_begin + static_cast<int64_t>(mb) * nt, t1 = t0 + nt - 1;
+  const int pf = static_cast<int>(((t0 + 1) * npairs - 1) / tiles);
+  const int pl = static_cast<int>(((t1 + 1) * npairs - 1) / tiles);
+  float acc = 0.f;
+  for (int sl = 0; sl <= pl - pf; ++sl)
+    for (int sub = 0; sub < 2; ++sub)
+      acc += part[(((static_cast<int64_t>(mb) * slots + sl) * 2 + sub) * 256 + (m % 256)) * r + j];
+  out[idx] = __bfloat16_as_ushort(__float2bfloat16_rn(acc));
+}
+}  // namespace
+
+cudaError_t launch_k2_next_reduce(const K2PairArgs &g, int i, uint16_t *xl1_next, cudaStream_t s) {
+  const K2Params &p = g.pr[i].p;
+  if (!p.fuse || p.nx_r == 0) return cudaSuccess;
+  const int nt = static_cast<int>((p.N + BN - 1) / BN);
+  const int64_t n = p.M * p.nx_r;
+  next_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+      p.nx_part, p.M, p.nx_r, nt, p.nx_slots, g.tile_begin[i], g.tile_begin[g.n], g.npairs, xl1_next);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_k2_nvfp4_2sm(const K2Maps &maps, const CUtensorMap &sfa, const CUtensorMap &sfb,
