@@ -283,14 +283,18 @@ def svdq_gemm_fused_next_workspace(layers, M, nexts) -> int:
     return wsb.value
 
 
-def svdq_gemm_w4a4_lowrank_up_fused_next(layers, xq, xs, xl1, M, nexts, act="none", Y=None, ws=None, stream=None):
+def svdq_gemm_w4a4_lowrank_up_fused_next(layers, xq, xs, xl1, M, nexts, act="none", Y=None, ws=None, out=None,
+                                         stream=None):
     """K2 of layers[i] whose epilogue also runs nexts[i]'s K1 on its (activated) bf16 output
     (SURVEY 8(f) row 1).  Y: list of bf16 [M, N] tensors or None (no store).  Returns
     (xq_next, xs_next, xl1_next) lists, the buffers svdq_quantize_act_lowrank_down(nexts[i], a) fills."""
     n = len(layers)
     dev = xq[0].device
     outs = []
-    for L, Nx, m in zip(layers, nexts, M):
+    for i, (L, Nx, m) in enumerate(zip(layers, nexts, M)):
+        if out is not None:
+            outs.append((out[0][i], out[1][i], out[2][i]))
+            continue
         bq, bs, bl = svdq_act_buffer_sizes(Nx.fmt, m, Nx.K, Nx.rank)
         outs.append((torch.empty(bq, dtype=torch.uint8, device=dev), torch.empty(bs, dtype=torch.uint8, device=dev),
                      torch.empty(max(bl // 2, 8), dtype=torch.int16, device=dev)))

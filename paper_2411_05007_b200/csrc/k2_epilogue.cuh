@@ -177,13 +177,10 @@ __device__ __forceinline__ void epilogue_tile_next(uint32_t tmem_acc_lane, const
   for (int i = 0; i < NB; ++i) {
     const int cb = sub + i * NWQ;
     const float *bs = bias_s + cb * 32;
-    float a[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) {
       const float o = __fadd_rn(__fmul_rn(alpha, __uint_as_float(r[i][e])), bs[e]);
-      const float y = __bfloat162float(__float2bfloat16_rn(o));
-      r[i][e] = __float_as_uint(y);
-      a[e] = p.nx_act ? __bfloat162float(__float2bfloat16_rn(gelu_tanh_f(y))) : y;
+      r[i][e] = __float_as_uint(__bfloat162float(__float2bfloat16_rn(o)));     // y, as stored
     }
     if (tmY) {                                              // the layer's own output, as epilogue_tile
       uint8_t *sb = stage + (NBUF == 2 ? buf * 2048 : 0);
@@ -203,6 +200,12 @@ __device__ __forceinline__ void epilogue_tile_next(uint32_t tmem_acc_lane, const
         bulk_commit_group();
       }
       buf ^= 1;
+    }
+    // the next layer's input a, in place of y
+    float *a = reinterpret_cast<float *>(r[i]);
+    if (p.nx_act) {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) a[e] = __bfloat162float(__float2bfloat16_rn(gelu_tanh_f(a[e])));
     }
     // next layer's NVFP4 codes and scale factors, two 16-column groups
 #pragma unroll

@@ -387,10 +387,20 @@ __global__ void __launch_bounds__(320, 1)
         float *lamn_s = reinterpret_cast<float *>(smem + NEXT_OFF);
         uint16_t *l1n_s = reinterpret_cast<uint16_t *>(smem + NEXT_OFF + BN * 4);
         for (int c = et; c < BN; c += 256) lamn_s[c] = n0 + c < p.N ? p.nx_lam_inv[n0 + c] : 0.f;
-        for (int c = et; c < p.nx_r * BN; c += 256) {
-          const int j = c / BN, col = c % BN;
-          l1n_s[c] = n0 + col < p.N ? p.nx_l1s[static_cast<int64_t>(j) * p.N + n0 + col] : 0;
+        // L1s_next slice [nx_r][192] bf16 as 16-byte vectors (8 columns; N % 16 == 0, so a vector
+        // never straddles N), all loads of a thread issued before any store
+        constexpr int V = 32 * BN / 8 / 256;           // 3 vectors per thread at rank 32
+        uint4 v[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          const int c = et + 256 * k;                  // vector index: row j = c / 24, 8-col group c % 24
+          const int j = c / (BN / 8), col = (c % (BN / 8)) * 8;
+          v[k] = (j < p.nx_r && n0 + col < p.N)
+                     ? *reinterpret_cast<const uint4 *>(p.nx_l1s + static_cast<int64_t>(j) * p.N + n0 + col)
+                     : make_uint4(0, 0, 0, 0);
         }
+#pragma unroll
+        for (int k = 0; k < V; ++k) reinterpret_cast<uint4 *>(l1n_s)[et + 256 * k] = v[k];
       }
       named_bar(1, 256);
       { K2T_BEGIN(); mbar_wait(&acc_full[b], acc_ph); K2T_ACC(t_ewait); }
