@@ -492,7 +492,7 @@ svdq_status prepare_fused(int32_t n, const svdq_linear *const *layers, const uin
     const int64_t nt = (layers[i]->N + kNvfp4PairBN - 1) / kNvfp4PairBN;
     const int slots = k2_next_slots(nt, tiles, np);
     part_off[i] = off;
-    if (Nx->rank) off += (static_cast<size_t>((M[i] + 255) / 256) * slots * 2 * 256 * Nx->rank * 4 + 255) & ~size_t(255);
+    if (Nx->rank) off += (static_cast<size_t>((M[i] + 255) / 256) * slots * 256 * Nx->rank * 4 + 255) & ~size_t(255);
     K2Params &p = g->pr[i].p;
     p.nx_slots = slots;
   }

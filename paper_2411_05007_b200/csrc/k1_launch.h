@@ -106,7 +106,7 @@ struct K2Params {
   const uint16_t *nx_l1s;     // [nx_r][N] bf16
   uint8_t *nx_xq;             // [M][N/2]
   uint8_t *nx_sf;             // 128x4 layout over (M rows, K = N)
-  float *nx_part;             // [ceil(M/256)][nx_slots][2][256][nx_r] fp32 partial sums
+  float *nx_part;             // [ceil(M/256)][nx_slots][256][nx_r] fp32 partial sums
   int nx_slots;
 };
 struct K2Maps {

@@ -142,33 +142,29 @@ __device__ __forceinline__ void epilogue_tile_direct(uint32_t tmem_acc_lane, con
   }
 }
 
-// GELU, tanh form, in fp32 (reading N1; the oracle evaluates it in fp64)
+// GELU, tanh form, in fp32 (reading N1; the oracle evaluates it in fp64):
+// 0.5 v (1 + tanh(u)) = v / (1 + exp(-2u)), u = sqrt(2/pi) (v + 0.044715 v^3) -- one ex2 and one
+// reciprocal (a few fp32 ulp; the value is then rounded to bf16)
 __device__ __forceinline__ float gelu_tanh_f(float v) {
-  const float u = 0.7978845608028654f * (v + 0.044715f * v * v * v);
-  return 0.5f * v * (1.0f + tanhf(u));
+  const float u2 = -2.0f * 0.7978845608028654f * fmaf(0.044715f * v, v * v, v);
+  return __fdividef(v, 1.0f + exp2f(u2 * 1.4426950408889634f));
 }
 
 // epilogue_tile plus the next layer's K1.  Lane l of the warp owns row
 // row0 + l; for each of its 32-column blocks it forms the stored bf16 output y, the next
 // layer's input a = y or bf16(gelu(y)), x_hat = fl32(a * lambda_inv_next) and, per 16-column
-// group, the NVFP4 scale factor and codes with K1's exact recipe (reading Q10), and
-// accumulates xacc[j] += a * L1s_next[j][col] in fp32.  tmY == nullptr: Y is not stored.
-// lamn_s / l1n_s: the tile's 192 lambda_inv_next values (0 past N) and the [32][192] bf16 L1s
-// slice (0 past N).  Rows >= M store no codes; their scale factors (padding rows of the 128x4
+// group, the NVFP4 scale factor and codes with K1's exact recipe (reading Q10), and writes a
+// into the a tile (atile, row row_l of this CTA) that the MMA warp multiplies by L1s_next.
+// tmY == nullptr: Y is not stored.  lamn_s: the tile's 192 lambda_inv_next values (0 past N).  Rows >= M store no codes; their scale factors (padding rows of the 128x4
 // layout) are written 0x00 (reading Q22).
 template <int NCOLS, int NWQ, int NBUF = 2, typename Release>
 __device__ __forceinline__ void epilogue_tile_next(uint32_t tmem_acc_lane, const float *bias_s, float alpha,
                                                    const CUtensorMap *tmY, int32_t row0, int32_t col0, int sub,
                                                    uint8_t *stage, int &buf, int lane, Release release,
-                                                   const K2Params &p, const float *lamn_s, const uint16_t *l1n_s,
-                                                   float (&xacc)[32]) {
+                                                   const K2Params &p, const float *lamn_s, uint8_t *atile,
+                                                   int row_l) {
   constexpr int NB = NCOLS / (32 * NWQ);
   static_assert(NCOLS % (32 * NWQ) == 0, "column split");
-  uint32_t r[NB][32];
-#pragma unroll
-  for (int i = 0; i < NB; ++i) tmem_ld_32x32b_x32(tmem_acc_lane + (sub + i * NWQ) * 32, r[i]);
-  tmem_ld_wait();
-  release();
   const uint32_t sw = static_cast<uint32_t>((lane >> 1) & 3);
   const int64_t row = static_cast<int64_t>(row0) + lane;
   const int64_t N = p.N;
@@ -177,10 +173,17 @@ __device__ __forceinline__ void epilogue_tile_next(uint32_t tmem_acc_lane, const
   for (int i = 0; i < NB; ++i) {
     const int cb = sub + i * NWQ;
     const float *bs = bias_s + cb * 32;
+    // one 32-column block at a time (register budget: 10 warps -> 168 per thread); the
+    // accumulator is released after the last block's load (measured: loading all blocks first
+    // and packing y to bf16 pairs, to release earlier, was 7 % slower with GELU + rank 32)
+    uint32_t rr[32];
+    tmem_ld_32x32b_x32(tmem_acc_lane + cb * 32, rr);
+    tmem_ld_wait();
+    if (i == NB - 1) release();
 #pragma unroll
     for (int e = 0; e < 32; ++e) {
-      const float o = __fadd_rn(__fmul_rn(alpha, __uint_as_float(r[i][e])), bs[e]);
-      r[i][e] = __float_as_uint(__bfloat162float(__float2bfloat16_rn(o)));     // y, as stored
+      const float o = __fadd_rn(__fmul_rn(alpha, __uint_as_float(rr[e])), bs[e]);
+      rr[e] = __float_as_uint(__bfloat162float(__float2bfloat16_rn(o)));      // y, as stored
     }
     if (tmY) {                                              // the layer's own output, as epilogue_tile
       uint8_t *sb = stage + (NBUF == 2 ? buf * 2048 : 0);
@@ -189,7 +192,7 @@ __device__ __forceinline__ void epilogue_tile_next(uint32_t tmem_acc_lane, const
       uint8_t *rowp = sb + lane * 64;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const float *v = reinterpret_cast<const float *>(&r[i][8 * c]);
+        const float *v = reinterpret_cast<const float *>(&rr[8 * c]);
         *reinterpret_cast<uint4 *>(rowp + ((c ^ sw) * 16)) =
             make_uint4(pack2(v[0], v[1], 0), pack2(v[2], v[3], 0), pack2(v[4], v[5], 0), pack2(v[6], v[7], 0));
       }
@@ -201,15 +204,18 @@ __device__ __forceinline__ void epilogue_tile_next(uint32_t tmem_acc_lane, const
       }
       buf ^= 1;
     }
-    // the next layer's input a, in place of y
-    float *a = reinterpret_cast<float *>(r[i]);
+    float *a = reinterpret_cast<float *>(rr);
+    // the next layer's input a
     if (p.nx_act) {
 #pragma unroll
       for (int e = 0; e < 32; ++e) a[e] = __bfloat162float(__float2bfloat16_rn(gelu_tanh_f(a[e])));
     }
     // next layer's NVFP4 codes and scale factors, two 16-column groups
+#ifndef SVDQ_FUSE_EXP
+#define SVDQ_FUSE_EXP 0
+#endif
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < ((SVDQ_FUSE_EXP & 1) ? 0 : 2); ++h) {
       const int64_t gcol = static_cast<int64_t>(col0) + cb * 32 + 16 * h;
       if (gcol >= N) break;
       float xh[16];
@@ -235,24 +241,16 @@ __device__ __forceinline__ void epilogue_tile_next(uint32_t tmem_acc_lane, const
         p.nx_sf[sf_offset(row, gcol / 16, N)] = 0;
       }
     }
-    // partial X L1s_next^T over this block's 32 columns (zeros past N)
-    if (p.nx_r) {
+    // a (bf16) into the CTA's a tile for the X L1s_next^T MMA: 3 chunks of [128 rows x 64 cols],
+    // K-major with the 128-byte swizzle (16-byte unit u of row r at u ^ (r & 7))
+    if (atile) {
+      uint8_t *rowp = atile + (cb >> 1) * 16384 + row_l * 128;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (j >= p.nx_r) continue;
-        const uint4 *lp = reinterpret_cast<const uint4 *>(l1n_s + j * NCOLS + cb * 32);
-        float s = xacc[j];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const uint4 w = lp[c];
-          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-          for (int d = 0; d < 4; ++d) {
-            s = fmaf(a[8 * c + 2 * d], __uint_as_float(ww[d] << 16), s);
-            s = fmaf(a[8 * c + 2 * d + 1], __uint_as_float(ww[d] & 0xFFFF0000u), s);
-          }
-        }
-        xacc[j] = s;
+      for (int c = 0; c < 4; ++c) {
+        const int u = (cb & 1) * 4 + c;
+        *reinterpret_cast<uint4 *>(rowp + ((u ^ (row_l & 7)) << 4)) =
+            make_uint4(pack2(a[8 * c], a[8 * c + 1], 0), pack2(a[8 * c + 2], a[8 * c + 3], 0),
+                       pack2(a[8 * c + 4], a[8 * c + 5], 0), pack2(a[8 * c + 6], a[8 * c + 7], 0));
       }
     }
   }

@@ -16,6 +16,7 @@
 // 2..5 epilogue (both; release the accumulator buffer to the leader's barrier).
 // TMEM per CTA: acc0 [0,192), acc1 [192,384), two SF slots of 48 columns.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -69,9 +70,22 @@ constexpr int EPI_OFF = kStages * STAGE;                 // epilogue staging
 constexpr int EPI_BYTES = SVDQ_BIGSTORE && 3 * 16384 > 8 * 2048 * kEpiBuf ? 3 * 16384 : 8 * 2048 * kEpiBuf;
 constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
 constexpr int SMEM = BAR_OFF + 256 + BN * 4 + 1024;
-// fused launches: + the tile's lambda_inv_next [192] fp32 and L1s_next slice [32][192] bf16
-constexpr int NEXT_OFF = BAR_OFF + 256 + BN * 4;
-constexpr int SMEM_FUSE = SMEM + BN * 4 + 32 * BN * 2;
+// Shared-memory layout per variant.  Fused launches (layer-boundary fusion) run a 4-stage ring
+// and add the tile's lambda_inv_next [192] fp32, the a tile (3 x [128 rows x 128 B], SW128) and
+// this CTA's half of the L1s_next rows (3 x [r/2 rows x 128 B], SW128) for the X L1s_next^T MMA.
+template <bool kFuse>
+struct Lay {
+  static constexpr int stages = kFuse ? 4 : kStages;
+  static constexpr int epi_off = stages * STAGE;
+  static constexpr int bar_off = epi_off + EPI_BYTES;
+  static constexpr int bias_off = bar_off + 256;
+  static constexpr int lamn_off = bias_off + BN * 4;
+  static constexpr int at_off = (lamn_off + BN * 4 + 1023) / 1024 * 1024;
+  static constexpr int bt_off = at_off + 3 * 16384;
+  static constexpr int smem = kFuse ? bt_off + 3 * 2048 + 1024 : SMEM;
+};
+constexpr int XL1_COL = SF_BASE + 2 * SF_COLS;   // TMEM columns [480, 512): X L1s_next^T accumulator
+static_assert(XL1_COL + 32 <= 512, "TMEM budget (fused)");
 static_assert(STAGE % 1024 == 0, "stage alignment");
 static_assert(SF_BASE + 2 * SF_COLS <= 512, "TMEM budget");
 
@@ -126,12 +140,16 @@ __global__ void __launch_bounds__(320, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~static_cast<uintptr_t>(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + BAR_OFF);
-  uint64_t *empty = full + kStages;
-  uint64_t *acc_full = empty + kStages;   // [2]
+  using LY = Lay<kFuse>;
+  constexpr int kSt = LY::stages;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + LY::bar_off);
+  uint64_t *empty = full + kSt;
+  uint64_t *acc_full = empty + kSt;       // [2]
   uint64_t *acc_empty = acc_full + 2;     // [2] (leader's copy is the one used)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
-  float *bias_s = reinterpret_cast<float *>(smem + BAR_OFF + 256);
+  uint64_t *xa_full = acc_empty + 3;      // fused: a tile written by all 16 epilogue warps (leader's)
+  uint64_t *xa_empty = acc_empty + 4;     // fused: the X L1s_next^T MMAs of the tile are done (both)
+  float *bias_s = reinterpret_cast<float *>(smem + LY::bias_off);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -148,13 +166,17 @@ __global__ void __launch_bounds__(320, 1)
   auto nslab_of = [&](int i) { return (g.pr[i].p.rank + 63) / 64; };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kSt; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], 16);                      // 8 epilogue warps x 2 CTAs
+    }
+    if (kFuse) {
+      mbar_init(xa_full, 16);
+      mbar_init(xa_empty, 1);
     }
     fence_mbar_init();
   }
@@ -188,7 +210,7 @@ __global__ void __launch_bounds__(320, 1)
 #endif
       // Weight tiles (B, SFB) of the first tile's first ring do not depend on K1: issue them
       // before the programmatic dependency resolves, so they land while K1 finishes.
-      const int pre = (SVDQ_EXP & 4) || t_first >= t_end ? 0 : min(kStages, nkt_of(locate(g, t_first).i));
+      const int pre = (SVDQ_EXP & 4) || t_first >= t_end ? 0 : min(kSt, nkt_of(locate(g, t_first).i));
       if (pre) {
         const TileRef tr = locate(g, t_first);
         const K2PairProblem &pr = g.pr[tr.i];
@@ -218,13 +240,13 @@ __global__ void __launch_bounds__(320, 1)
           if (first && kt < pre) {                         // B / SFB already in flight
             tma_load_2d_cg2(st, &pr.a, fb, kt * 128, ma);
             tma_load_3d_cg2(st + A_BYTES + B_BYTES, &pr.sfa, fb, 0, kt * 4, static_cast<int32_t>(m0 / 128 + crank));
-            if (++s == kStages) { s = 0; ph ^= 1; }
+            if (++s == kSt) { s = 0; ph ^= 1; }
             continue;
           }
           { K2T_BEGIN(); mbar_wait(&empty[s], ph ^ 1); K2T_ACC(t_pwait); }
 #if SVDQ_EXP & 4                                         // ablation: no operand traffic at all
           if (crank == 0) mbar_arrive(&full[s]);
-          if (++s == kStages) { s = 0; ph ^= 1; }
+          if (++s == kSt) { s = 0; ph ^= 1; }
           continue;
 #endif
           if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE);
@@ -233,7 +255,7 @@ __global__ void __launch_bounds__(320, 1)
           tma_load_3d_cg2(st + A_BYTES + B_BYTES, &pr.sfa, fb, 0, kt * 4, static_cast<int32_t>(m0 / 128 + crank));
           tma_load_3d_cg2(st + A_BYTES + B_BYTES + SFA_BYTES, &pr.sfb, fb, 0, kt * 4,
                           static_cast<int32_t>(n0 / 128));
-          if (++s == kStages) { s = 0; ph ^= 1; }
+          if (++s == kSt) { s = 0; ph ^= 1; }
         }
         first = false;
         for (int j = 0; j < nslab; ++j) {
@@ -243,7 +265,7 @@ __global__ void __launch_bounds__(320, 1)
           if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
           tma_load_2d_cg2(st, &pr.xl1, fb, j * 64, ma);
           tma_load_2d_cg2(st + A_BYTES, &pr.l2, fb, j * 64, nb);
-          if (++s == kStages) { s = 0; ph ^= 1; }
+          if (++s == kSt) { s = 0; ph ^= 1; }
         }
       }
 #ifdef SVDQ_TRACE
@@ -263,6 +285,27 @@ __global__ void __launch_bounds__(320, 1)
       long long t_acc = 0, t_full = 0;
       const long long t_start = clock64();
 #endif
+      // fused: xl1 += a_tile x L1s_next^T for a tile whose epilogue has filled the a / B tiles
+      int xl_prev = -1;
+      bool xl_prev_first = false;
+      uint32_t xa_ph = 0;
+      auto issue_xl1 = [&](int tp, bool first) {
+        const int r = g.pr[locate(g, tp).i].p.nx_r;
+        mbar_wait(xa_full, xa_ph);
+        xa_ph ^= 1;
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t idesc_x = idesc_bf16(256, static_cast<uint32_t>(r));
+          const uint32_t a0 = smem_u32(smem + LY::at_off), b0 = smem_u32(smem + LY::bt_off);
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              mma_bf16_cg2(tmem + XL1_COL, sdesc_kmajor_sw128(a0 + c * 16384 + 32 * i),
+                           sdesc_kmajor_sw128(b0 + c * 2048 + 32 * i), idesc_x, (!first || c || i) ? 1u : 0u);
+          tc_commit_cg2_mc(xa_empty, 0x3);
+        }
+        __syncwarp();
+      };
       for (int t = t_first; t < t_end; t += t_step, ++acc_i) {
         const int b = (SVDQ_EXP & 64) ? 0 : acc_i & 1;            // 64: single accumulator (ablation)
         const uint32_t acc_ph = (SVDQ_EXP & 64) ? acc_i & 1 : (acc_i >> 1) & 1;
@@ -329,7 +372,7 @@ __global__ void __launch_bounds__(320, 1)
           }
           __syncwarp();
           ++sf_i;
-          if (++s == kStages) { s = 0; ph ^= 1; }
+          if (++s == kSt) { s = 0; ph ^= 1; }
         }
         for (int j = 0; j < nslab; ++j) {
           mbar_wait(&full[s], ph);
@@ -345,10 +388,23 @@ __global__ void __launch_bounds__(320, 1)
             tc_commit_cg2_mc(&empty[s], 0x3);
           }
           __syncwarp();
-          if (++s == kStages) { s = 0; ph ^= 1; }
+          if (++s == kSt) { s = 0; ph ^= 1; }
         }
         if (elect_one()) tc_commit_cg2_mc(&acc_full[b], 0x3);
         __syncwarp();
+        if constexpr (kFuse) {                           // X L1s_next^T of the PREVIOUS fused tile
+          if (xl_prev >= 0) issue_xl1(xl_prev, xl_prev_first);
+          const K2Params &pt = g.pr[tr.i].p;
+          if (pt.fuse && pt.nx_r > 0) {
+            xl_prev_first = t == t_first || locate(g, t - t_step).i != tr.i || locate(g, t - t_step).m0 != tr.m0;
+            xl_prev = t;
+          } else {
+            xl_prev = -1;
+          }
+        }
+      }
+      if constexpr (kFuse) {
+        if (xl_prev >= 0) issue_xl1(xl_prev, xl_prev_first);
       }
 #ifdef SVDQ_TRACE
       if (lane == 0 && pair < 148) {
@@ -361,9 +417,8 @@ __global__ void __launch_bounds__(320, 1)
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
     const int et = threadIdx.x - 64;
-    float xacc[32];                                      // fused: partial X L1s_next^T of this row
-#pragma unroll
-    for (int j = 0; j < 32; ++j) xacc[j] = 0.f;
+    int xl_cnt = 0;                                      // fused tiles that fed the X L1s_next^T MMA
+    const uint32_t xa_full0 = mapa_u32(xa_full, 0);
     const uint32_t acc_empty0 = mapa_u32(&acc_empty[0], 0);
     int acc_i = 0;
     int ebuf = 0;
@@ -383,24 +438,28 @@ __global__ void __launch_bounds__(320, 1)
       named_bar(1, 256);
       for (int c = et; c < BN; c += 256)
         bias_s[c] = (p.bias && n0 + c < p.N) ? load_bias(p.bias, p.bias_dtype, n0 + c) : 0.f;
+      const bool fx = kFuse && p.fuse && p.nx_r > 0;   // this tile feeds the X L1s_next^T MMA
       if constexpr (kFuse) {
-        float *lamn_s = reinterpret_cast<float *>(smem + NEXT_OFF);
-        uint16_t *l1n_s = reinterpret_cast<uint16_t *>(smem + NEXT_OFF + BN * 4);
-        for (int c = et; c < BN; c += 256) lamn_s[c] = n0 + c < p.N ? p.nx_lam_inv[n0 + c] : 0.f;
-        // L1s_next slice [nx_r][192] bf16 as 16-byte vectors (8 columns; N % 16 == 0, so a vector
-        // never straddles N), all loads of a thread issued before any store
-        constexpr int V = 32 * BN / 8 / 256;           // 3 vectors per thread at rank 32
-        uint4 v[V];
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          const int c = et + 256 * k;                  // vector index: row j = c / 24, 8-col group c % 24
-          const int j = c / (BN / 8), col = (c % (BN / 8)) * 8;
-          v[k] = (j < p.nx_r && n0 + col < p.N)
-                     ? *reinterpret_cast<const uint4 *>(p.nx_l1s + static_cast<int64_t>(j) * p.N + n0 + col)
-                     : make_uint4(0, 0, 0, 0);
+        if (p.fuse) {
+          float *lamn_s = reinterpret_cast<float *>(smem + LY::lamn_off);
+          for (int c = et; c < BN; c += 256) lamn_s[c] = n0 + c < p.N ? p.nx_lam_inv[n0 + c] : 0.f;
         }
-#pragma unroll
-        for (int k = 0; k < V; ++k) reinterpret_cast<uint4 *>(l1n_s)[et + 256 * k] = v[k];
+        if (fx) {
+          // the a / B tiles are free once the previous fused tile's MMAs completed
+          if (xl_cnt > 0) mbar_wait(xa_empty, (xl_cnt - 1) & 1);
+          // this CTA's L1s_next rows [crank * r/2, +r/2) over the tile's 192 columns, SW128 K-major:
+          // 16-byte vector (row jl, 8-column group kv) at chunk kv/8, unit (kv%8) ^ (jl & 7)
+          const int rh = p.nx_r / 2;
+          uint8_t *bt = smem + LY::bt_off;
+          for (int v = et; v < rh * (BN / 8); v += 256) {
+            const int jl = v / (BN / 8), kv = v % (BN / 8);
+            const int64_t col = n0 + kv * 8;
+            const uint4 val = col < p.N ? *reinterpret_cast<const uint4 *>(
+                                              p.nx_l1s + static_cast<int64_t>(crank * rh + jl) * p.N + col)
+                                        : make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4 *>(bt + (kv >> 3) * 2048 + jl * 128 + (((kv & 7) ^ (jl & 7)) << 4)) = val;
+          }
+        }
       }
       named_bar(1, 256);
       { K2T_BEGIN(); mbar_wait(&acc_full[b], acc_ph); K2T_ACC(t_ewait); }
@@ -438,7 +497,7 @@ __global__ void __launch_bounds__(320, 1)
         if (lane == 0) mbar_arrive_cluster(acc_empty0 + b * 8);
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-          uint8_t *blk = smem + EPI_OFF + i * 16384;
+          uint8_t *blk = smem + LY::epi_off + i * 16384;
           if (et == 0) bulk_wait_group_read<2>();        // this block's previous store has read it
           named_bar(2, 256);
           const float *bs = bias_s + (sub + 2 * i) * 32;
@@ -468,44 +527,52 @@ __global__ void __launch_bounds__(320, 1)
           epilogue_tile_next<BN, 2, kEpiBuf>(
               tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.Y ? tmY : nullptr,
               static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
-              smem + EPI_OFF + (warp - 2) * 2048 * kEpiBuf, ebuf, lane,
+              smem + LY::epi_off + (warp - 2) * 2048 * kEpiBuf, ebuf, lane,
               [&]() {
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(acc_empty0 + b * 8);
               },
-              p, reinterpret_cast<const float *>(smem + NEXT_OFF),
-              reinterpret_cast<const uint16_t *>(smem + NEXT_OFF + BN * 4), xacc);
-          // leaving this 256-row block (or the range): write the partial X L1s_next^T sums to this
-          // pair's slot; slot = pair - (first pair whose range holds a tile of the block)
-          bool flush = p.nx_r > 0 && t + t_step >= t_end;
-          if (p.nx_r > 0 && !flush) {
-            const TileRef nr = locate(g, t + t_step);
-            flush = nr.i != tr.i || nr.m0 != tr.m0;
-          }
-          if (flush) {
-            const int nt = static_cast<int>((p.N + BN - 1) / BN);
-            const int mb = static_cast<int>(tr.m0 / 256);
-            const int64_t t0 = g.tile_begin[tr.i] + static_cast<int64_t>(mb) * nt;
-            const int pf = static_cast<int>(((t0 + 1) * npairs - 1) / tiles);
-            const int sub = (warp - 2) >> 2;
-            float *dst = p.nx_part + ((((static_cast<int64_t>(mb) * p.nx_slots + (pair - pf)) * 2 + sub) * 256 +
-                                       128 * crank + quad * 32 + lane) *
-                                      p.nx_r);
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              if (j < p.nx_r) {
-                *reinterpret_cast<float4 *>(dst + j) = make_float4(xacc[j], xacc[j + 1], xacc[j + 2], xacc[j + 3]);
-                xacc[j] = xacc[j + 1] = xacc[j + 2] = xacc[j + 3] = 0.f;
-              }
+              p, reinterpret_cast<const float *>(smem + LY::lamn_off), fx ? smem + LY::at_off : nullptr, row);
+          if (fx) {
+            // a / B tiles written (generic proxy) -> visible to the tensor core, then arrive on the leader
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(xa_full0);
+            // leaving this 256-row block (or the range): read the accumulated X L1s_next^T rows from
+            // TMEM once the MMAs of this tile are done, and write them to this pair's slot
+            bool flush = t + t_step >= t_end;
+            if (!flush) {
+              const TileRef nr = locate(g, t + t_step);
+              flush = nr.i != tr.i || nr.m0 != tr.m0;
             }
+            if (flush) {
+              mbar_wait(xa_empty, xl_cnt & 1);
+              tc_fence_after();
+              uint32_t xr[32];
+              tmem_ld_32x32b_x32(tmem + XL1_COL + (static_cast<uint32_t>(quad * 32) << 16), xr);
+              tmem_ld_wait();
+              if (((warp - 2) >> 2) == 0) {
+                const int nt = static_cast<int>((p.N + BN - 1) / BN);
+                const int mb = static_cast<int>(tr.m0 / 256);
+                const int64_t t0 = g.tile_begin[tr.i] + static_cast<int64_t>(mb) * nt;
+                const int pf = static_cast<int>(((t0 + 1) * npairs - 1) / tiles);
+                float *dst = p.nx_part +
+                             ((static_cast<int64_t>(mb) * p.nx_slots + (pair - pf)) * 256 + 128 * crank + row) * p.nx_r;
+                for (int j = 0; j < p.nx_r; j += 4)
+                  *reinterpret_cast<float4 *>(dst + j) = make_float4(__uint_as_float(xr[j]), __uint_as_float(xr[j + 1]),
+                                                                     __uint_as_float(xr[j + 2]), __uint_as_float(xr[j + 3]));
+              }
+              tc_fence_before();                         // the read precedes the next run's first MMA
+            }
+            ++xl_cnt;
           }
           continue;
         }
       }
       epilogue_tile<BN, 2, kEpiBuf>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
                            tmY, static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
-                           smem + EPI_OFF + (warp - 2) * 2048 * kEpiBuf, ebuf, lane, [&]() {
+                           smem + LY::epi_off + (warp - 2) * 2048 * kEpiBuf, ebuf, lane, [&]() {
                           tc_fence_before();
                           __syncwarp();
                           if (lane == 0) mbar_arrive_cluster(acc_empty0 + b * 8);
@@ -530,7 +597,7 @@ __global__ void __launch_bounds__(320, 1)
 
 cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
   static_assert(SMEM <= 227 * 1024, "smem budget");
-  static_assert(SMEM_FUSE <= 227 * 1024, "smem budget (fused)");
+  static_assert(Lay<true>::smem <= 227 * 1024, "smem budget (fused)");
   cudaError_t e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   if (e != cudaSuccess) return e;
   static int num_sms = 0;
@@ -547,12 +614,13 @@ cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
   }
   const int64_t tiles = g.tile_begin[g.n];
   const int64_t pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  g.contig = fuse ? 1 : 0;
+  static const int force_contig = [] { const char *e = std::getenv("SVDQ_K2_CONTIG"); return e ? std::atoi(e) : 0; }();
+  g.contig = (fuse || force_contig) ? 1 : 0;      // SVDQ_K2_CONTIG=1: schedule ablation
   g.npairs = static_cast<int>(pairs);
   if (fuse) {
-    e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_FUSE);
+    e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay<true>::smem);
     if (e != cudaSuccess) return e;
-    return launch_ex(k2_nvfp4_2sm_kernel<true>, dim3(static_cast<unsigned>(2 * pairs)), dim3(320), SMEM_FUSE, s, 2u, g);
+    return launch_ex(k2_nvfp4_2sm_kernel<true>, dim3(static_cast<unsigned>(2 * pairs)), dim3(320), Lay<true>::smem, s, 2u, g);
   }
   return launch_ex(k2_nvfp4_2sm_kernel<false>, dim3(static_cast<unsigned>(2 * pairs)), dim3(320), SMEM, s, 2u, g);
 }
@@ -581,9 +649,7 @@ __global__ void next_reduce_kernel(const float *__restrict__ part, int64_t M, in
   const int pf = static_cast<int>(((t0 + 1) * npairs - 1) / tiles);
   const int pl = static_cast<int>(((t1 + 1) * npairs - 1) / tiles);
   float acc = 0.f;
-  for (int sl = 0; sl <= pl - pf; ++sl)
-    for (int sub = 0; sub < 2; ++sub)
-      acc += part[(((static_cast<int64_t>(mb) * slots + sl) * 2 + sub) * 256 + (m % 256)) * r + j];
+  for (int sl = 0; sl <= pl - pf; ++sl) acc += part[((static_cast<int64_t>(mb) * slots + sl) * 256 + (m % 256)) * r + j];
   out[idx] = __bfloat16_as_ushort(__float2bfloat16_rn(acc));
 }
 }  // namespace
