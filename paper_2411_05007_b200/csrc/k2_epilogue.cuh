@@ -142,6 +142,10 @@ __device__ __forceinline__ void epilogue_tile_direct(uint32_t tmem_acc_lane, con
   }
 }
 
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
 // GELU, tanh form, in fp32 (reading N1; the oracle evaluates it in fp64):
 // 0.5 v (1 + tanh(u)) = v / (1 + exp(-2u)), u = sqrt(2/pi) (v + 0.044715 v^3) -- one ex2 and one
 // reciprocal (a few fp32 ulp; the value is then rounded to bf16)
@@ -157,13 +161,17 @@ __device__ __forceinline__ float gelu_tanh_f(float v) {
 // into the a tile (atile, row row_l of this CTA) that the MMA warp multiplies by L1s_next.
 // tmY == nullptr: Y is not stored.  lamn_s: the tile's 192 lambda_inv_next values (0 past N).  Rows >= M store no codes; their scale factors (padding rows of the 128x4
 // layout) are written 0x00 (reading Q22).
-template <int NCOLS, int NWQ, int NBUF = 2, typename Release>
+// The codes and scale factors are kept in registers and stored to global memory only after
+// `mid()` (the a-tile hand-off): a release-arrive waits for this thread's outstanding global
+// stores (ncu: ERRBAR before SYNCS.ARRIVE was the epilogue's top stall).
+template <int NCOLS, int NWQ, int NBUF = 2, typename Release, typename Mid>
 __device__ __forceinline__ void epilogue_tile_next(uint32_t tmem_acc_lane, const float *bias_s, float alpha,
                                                    const CUtensorMap *tmY, int32_t row0, int32_t col0, int sub,
                                                    uint8_t *stage, int &buf, int lane, Release release,
                                                    const K2Params &p, const float *lamn_s, uint8_t *atile,
-                                                   int row_l) {
+                                                   int row_l, Mid mid) {
   constexpr int NB = NCOLS / (32 * NWQ);
+  uint32_t cw[NB][4], sfw[NB][2];
   static_assert(NCOLS % (32 * NWQ) == 0, "column split");
   const uint32_t sw = static_cast<uint32_t>((lane >> 1) & 3);
   const int64_t row = static_cast<int64_t>(row0) + lane;
@@ -215,9 +223,7 @@ __device__ __forceinline__ void epilogue_tile_next(uint32_t tmem_acc_lane, const
 #define SVDQ_FUSE_EXP 0
 #endif
 #pragma unroll
-    for (int h = 0; h < ((SVDQ_FUSE_EXP & 1) ? 0 : 2); ++h) {
-      const int64_t gcol = static_cast<int64_t>(col0) + cb * 32 + 16 * h;
-      if (gcol >= N) break;
+    for (int h = 0; h < 2; ++h) {
       float xh[16];
       float amax = 0.f;
 #pragma unroll
@@ -234,23 +240,37 @@ __device__ __forceinline__ void epilogue_tile_next(uint32_t tmem_acc_lane, const
         q0[e] = __fmul_rn(xh[e], qinv);
         q1[e] = __fmul_rn(xh[8 + e], qinv);
       }
-      if (row < p.M) {
-        *reinterpret_cast<uint2 *>(p.nx_xq + row * (N / 2) + gcol / 2) = make_uint2(e2m1x8(q0), e2m1x8(q1));
-        p.nx_sf[sf_offset(row, gcol / 16, N)] = static_cast<uint8_t>(sf);
-      } else if (row < ((p.M + 127) / 128) * 128) {
-        p.nx_sf[sf_offset(row, gcol / 16, N)] = 0;
-      }
+      cw[i][2 * h] = e2m1x8(q0);
+      cw[i][2 * h + 1] = e2m1x8(q1);
+      sfw[i][h] = sf;
     }
     // a (bf16) into the CTA's a tile for the X L1s_next^T MMA: 3 chunks of [128 rows x 64 cols],
     // K-major with the 128-byte swizzle (16-byte unit u of row r at u ^ (r & 7))
     if (atile) {
-      uint8_t *rowp = atile + (cb >> 1) * 16384 + row_l * 128;
+      const uint32_t rowp = smem_u32(atile) + (cb >> 1) * 16384 + row_l * 128;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int u = (cb & 1) * 4 + c;
-        *reinterpret_cast<uint4 *>(rowp + ((u ^ (row_l & 7)) << 4)) =
-            make_uint4(pack2(a[8 * c], a[8 * c + 1], 0), pack2(a[8 * c + 2], a[8 * c + 3], 0),
-                       pack2(a[8 * c + 4], a[8 * c + 5], 0), pack2(a[8 * c + 6], a[8 * c + 7], 0));
+        sts128(rowp + ((u ^ (row_l & 7)) << 4), pack2(a[8 * c], a[8 * c + 1], 0), pack2(a[8 * c + 2], a[8 * c + 3], 0),
+               pack2(a[8 * c + 4], a[8 * c + 5], 0), pack2(a[8 * c + 6], a[8 * c + 7], 0));
+      }
+    }
+  }
+  mid();
+  // global stores of the next layer's codes / scale factors (rows >= M: padding scale factors 0x00)
+  const bool in_m = row < p.M, in_pad = row < ((p.M + 127) / 128) * 128;
+#pragma unroll
+  for (int i = 0; i < ((SVDQ_FUSE_EXP & 1) ? 0 : NB); ++i) {
+    const int cb = sub + i * NWQ;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t gcol = static_cast<int64_t>(col0) + cb * 32 + 16 * h;
+      if (gcol >= N) break;
+      if (in_m) {
+        *reinterpret_cast<uint2 *>(p.nx_xq + row * (N / 2) + gcol / 2) = make_uint2(cw[i][2 * h], cw[i][2 * h + 1]);
+        p.nx_sf[sf_offset(row, gcol / 16, N)] = static_cast<uint8_t>(sfw[i][h]);
+      } else if (in_pad) {
+        p.nx_sf[sf_offset(row, gcol / 16, N)] = 0;
       }
     }
   }

@@ -445,19 +445,30 @@ __global__ void __launch_bounds__(320, 1)
           for (int c = et; c < BN; c += 256) lamn_s[c] = n0 + c < p.N ? p.nx_lam_inv[n0 + c] : 0.f;
         }
         if (fx) {
-          // the a / B tiles are free once the previous fused tile's MMAs completed
-          if (xl_cnt > 0) mbar_wait(xa_empty, (xl_cnt - 1) & 1);
           // this CTA's L1s_next rows [crank * r/2, +r/2) over the tile's 192 columns, SW128 K-major:
-          // 16-byte vector (row jl, 8-column group kv) at chunk kv/8, unit (kv%8) ^ (jl & 7)
+          // 16-byte vector (row jl, 8-column group kv) at chunk kv/8, unit (kv%8) ^ (jl & 7).
+          // Global loads first (<= 2 vectors per thread at r = 32), then wait until the previous
+          // fused tile's MMAs have released the a / B tiles, then store.
           const int rh = p.nx_r / 2;
           uint8_t *bt = smem + LY::bt_off;
-          for (int v = et; v < rh * (BN / 8); v += 256) {
+          uint4 val[2];
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int v = et + 256 * k;
             const int jl = v / (BN / 8), kv = v % (BN / 8);
             const int64_t col = n0 + kv * 8;
-            const uint4 val = col < p.N ? *reinterpret_cast<const uint4 *>(
-                                              p.nx_l1s + static_cast<int64_t>(crank * rh + jl) * p.N + col)
-                                        : make_uint4(0, 0, 0, 0);
-            *reinterpret_cast<uint4 *>(bt + (kv >> 3) * 2048 + jl * 128 + (((kv & 7) ^ (jl & 7)) << 4)) = val;
+            val[k] = (v < rh * (BN / 8) && col < p.N)
+                         ? *reinterpret_cast<const uint4 *>(p.nx_l1s + static_cast<int64_t>(crank * rh + jl) * p.N + col)
+                         : make_uint4(0, 0, 0, 0);
+          }
+          if (xl_cnt > 0) mbar_wait(xa_empty, (xl_cnt - 1) & 1);
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int v = et + 256 * k;
+            const int jl = v / (BN / 8), kv = v % (BN / 8);
+            if (v < rh * (BN / 8))
+              sts128(smem_u32(bt) + (kv >> 3) * 2048 + jl * 128 + (((kv & 7) ^ (jl & 7)) << 4), val[k].x, val[k].y,
+                     val[k].z, val[k].w);
           }
         }
       }
@@ -533,12 +544,15 @@ __global__ void __launch_bounds__(320, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(acc_empty0 + b * 8);
               },
-              p, reinterpret_cast<const float *>(smem + LY::lamn_off), fx ? smem + LY::at_off : nullptr, row);
+              p, reinterpret_cast<const float *>(smem + LY::lamn_off), fx ? smem + LY::at_off : nullptr, row,
+              [&]() {
+                if (fx) {   // a / B tiles written (generic proxy) -> visible to the tensor core; arrive
+                  fence_proxy_async();
+                  __syncwarp();
+                  if (lane == 0) mbar_arrive_cluster(xa_full0);
+                }
+              });
           if (fx) {
-            // a / B tiles written (generic proxy) -> visible to the tensor core, then arrive on the leader
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(xa_full0);
             // leaving this 256-row block (or the range): read the accumulated X L1s_next^T rows from
             // TMEM once the MMAs of this tile are done, and write them to this pair's slot
             bool flush = t + t_step >= t_end;
