@@ -101,3 +101,30 @@ def test_grouped_argument_validation_before_device():
     i64 = (ctypes.c_int64 * 1)(8)
     st = lib.svdq_quantize_act_lowrank_down_grouped(1, arr, one, 1, i64, i64, one, one, one, None)
     assert st == 5
+
+
+def test_offline_and_fused_argument_validation_before_device():
+    """Layer-boundary fusion, refinement, GPTQ and alpha search reject bad arguments on the host."""
+    lib = P.abi.lib()
+    # fused next-layer K2: group size, NULL arrays, bad activation
+    assert lib.svdq_gemm_w4a4_lowrank_up_fused_next(0, None, None, None, None, None, None, None, 0, None, None, None,
+                                                    None, 0, None) == 1
+    assert lib.svdq_gemm_w4a4_lowrank_up_fused_next(5, None, None, None, None, None, None, None, 0, None, None, None,
+                                                    None, 0, None) == 1
+    wsb = ctypes.c_size_t()
+    assert lib.svdq_gemm_fused_next_workspace(1, None, None, None, ctypes.byref(wsb)) == 1
+    L = P.abi.svdq_linear()
+    arr = (ctypes.POINTER(P.abi.svdq_linear) * 1)(ctypes.pointer(L))
+    i64 = (ctypes.c_int64 * 1)(8)
+    assert lib.svdq_gemm_w4a4_lowrank_up_fused_next(1, arr, None, None, None, i64, None, arr, 7, None, None, None,
+                                                    None, 0, None) == 1
+    # refinement: negative iteration count, NULL pointers
+    best = ctypes.c_int32()
+    obj = (ctypes.c_double * 1)()
+    assert lib.svdq_refine_lowrank(None, 0, 8, 64, None, None, 64, 64, 16, 0, 0, 1.0, -1, 0, 0.01, None,
+                                   ctypes.byref(best), obj, None, 0, None) == 1
+    # GPTQ / alpha search workspaces: M_cal < 1
+    assert lib.svdq_quantize_residual_gptq_workspace(0, 64, 64, ctypes.byref(wsb)) == 2
+    assert lib.svdq_quantize_weights_gptq_workspace(0, 64, 64, 16, ctypes.byref(wsb)) == 2
+    assert lib.svdq_search_alpha_workspace(0, 0, 64, 64, 16, ctypes.byref(wsb)) == 2
+    assert lib.svdq_refine_lowrank_workspace(0, 0, 64, 64, 16, 0, ctypes.byref(wsb)) == 2
