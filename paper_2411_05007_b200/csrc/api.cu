@@ -515,6 +515,9 @@ svdq_status prepare_fused(int32_t n, const svdq_linear *const *layers, const uin
     g->pr[i].sfa = k.sfa_map;
     g->pr[i].sfb = k.sfb_map;
     g->pr[i].y = k.maps.y;
+    if ((st = make_map(&g->pr[i].nxq, xq_next[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, layers[i]->N / 2, M[i],
+                       layers[i]->N / 2, 96, 128, CU_TENSOR_MAP_SWIZZLE_NONE)) != SVDQ_OK)
+      return st;
     K2Params &p = g->pr[i].p;
     p = k.p;
     p.Y = Y[i];

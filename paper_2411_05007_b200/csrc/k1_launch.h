@@ -123,6 +123,7 @@ cudaError_t launch_k2_nvfp4_2sm(const K2Maps &maps, const CUtensorMap &sfa, cons
 constexpr int kMaxGroup = 4;
 struct K2PairProblem {
   CUtensorMap a, b, xl1, l2, sfa, sfb, y;
+  CUtensorMap nxq;        // fused: the next layer's codes [M][N/2] bytes, box {96, 128}
   K2Params p;
 };
 struct K2PairArgs {

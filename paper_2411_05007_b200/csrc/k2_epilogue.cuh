@@ -169,7 +169,7 @@ __device__ __forceinline__ void epilogue_tile_next(uint32_t tmem_acc_lane, const
                                                    const CUtensorMap *tmY, int32_t row0, int32_t col0, int sub,
                                                    uint8_t *stage, int &buf, int lane, Release release,
                                                    const K2Params &p, const float *lamn_s, uint8_t *atile,
-                                                   int row_l, Mid mid) {
+                                                   int row_l, Mid mid, uint8_t *cstage, uint8_t *sfstage, int quad) {
   constexpr int NB = NCOLS / (32 * NWQ);
   uint32_t cw[NB][4], sfw[NB][2];
   static_assert(NCOLS % (32 * NWQ) == 0, "column split");
@@ -257,23 +257,26 @@ __device__ __forceinline__ void epilogue_tile_next(uint32_t tmem_acc_lane, const
     }
   }
   mid();
-  // global stores of the next layer's codes / scale factors (rows >= M: padding scale factors 0x00)
-  const bool in_m = row < p.M, in_pad = row < ((p.M + 127) / 128) * 128;
+  // the next layer's codes / scale factors into the CTA's staging buffers (one TMA tensor store of
+  // the [128 x 96 B] code tile and one bulk copy of the tile's three 512-B scale-factor blocks of
+  // the 128x4 layout follow in the kernel): row_l's 16-column group g (0..11) -> codes at
+  // row_l * 96 + 8 g, scale factor at (g / 4) * 512 + (row_l & 31) * 16 + quad * 4 + g % 4.
+  // Rows >= M store 0x00 scale factors (padding rows, reading Q22).
+  const bool in_m = row < p.M;
 #pragma unroll
-  for (int i = 0; i < ((SVDQ_FUSE_EXP & 1) ? 0 : NB); ++i) {
+  for (int i = 0; i < NB; ++i) {
     const int cb = sub + i * NWQ;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int64_t gcol = static_cast<int64_t>(col0) + cb * 32 + 16 * h;
-      if (gcol >= N) break;
-      if (in_m) {
-        *reinterpret_cast<uint2 *>(p.nx_xq + row * (N / 2) + gcol / 2) = make_uint2(cw[i][2 * h], cw[i][2 * h + 1]);
-        p.nx_sf[sf_offset(row, gcol / 16, N)] = static_cast<uint8_t>(sfw[i][h]);
-      } else if (in_pad) {
-        p.nx_sf[sf_offset(row, gcol / 16, N)] = 0;
-      }
+      const int g = cb * 2 + h;
+      asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(smem_u32(cstage) + row_l * 96 + 8 * g),
+                   "r"(cw[i][2 * h]), "r"(cw[i][2 * h + 1]) : "memory");
+      asm volatile("st.shared.u8 [%0], %1;" ::"r"(smem_u32(sfstage) + (g >> 2) * 512 + (row_l & 31) * 16 + quad * 4 +
+                                                  (g & 3)),
+                   "r"(in_m ? sfw[i][h] : 0u) : "memory");
     }
   }
+  fence_proxy_async();
 }
 
 }  // namespace svdq

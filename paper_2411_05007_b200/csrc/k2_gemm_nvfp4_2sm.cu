@@ -75,14 +75,16 @@ constexpr int SMEM = BAR_OFF + 256 + BN * 4 + 1024;
 // this CTA's half of the L1s_next rows (3 x [r/2 rows x 128 B], SW128) for the X L1s_next^T MMA.
 template <bool kFuse>
 struct Lay {
-  static constexpr int stages = kFuse ? 4 : kStages;
+  static constexpr int stages = kFuse ? 3 : kStages;
   static constexpr int epi_off = stages * STAGE;
   static constexpr int bar_off = epi_off + EPI_BYTES;
   static constexpr int bias_off = bar_off + 256;
   static constexpr int lamn_off = bias_off + BN * 4;
   static constexpr int at_off = (lamn_off + BN * 4 + 1023) / 1024 * 1024;
   static constexpr int bt_off = at_off + 3 * 16384;
-  static constexpr int smem = kFuse ? bt_off + 3 * 2048 + 1024 : SMEM;
+  static constexpr int cs_off = bt_off + 3 * 2048;         // next-layer code tile [128 x 96 B]
+  static constexpr int sfs_off = cs_off + 128 * 96;         // next-layer scale factors, 3 x 512 B
+  static constexpr int smem = kFuse ? sfs_off + 3 * 512 + 1024 : SMEM;
 };
 constexpr int XL1_COL = SF_BASE + 2 * SF_COLS;   // TMEM columns [480, 512): X L1s_next^T accumulator
 static_assert(XL1_COL + 32 <= 512, "TMEM budget (fused)");
@@ -435,6 +437,7 @@ __global__ void __launch_bounds__(320, 1)
       const CUtensorMap *tmY = &g.pr[tr.i].y;
       const int64_t m0 = tr.m0 + 128 * crank;
       const int64_t n0 = tr.n0;
+      if (kFuse && et == 0) bulk_wait_group_read<0>();    // previous tile's code / SF staging is read
       named_bar(1, 256);
       for (int c = et; c < BN; c += 256)
         bias_s[c] = (p.bias && n0 + c < p.N) ? load_bias(p.bias, p.bias_dtype, n0 + c) : 0.f;
@@ -551,7 +554,17 @@ __global__ void __launch_bounds__(320, 1)
                   __syncwarp();
                   if (lane == 0) mbar_arrive_cluster(xa_full0);
                 }
-              });
+              },
+              smem + LY::cs_off, smem + LY::sfs_off, quad);
+          named_bar(2, 256);                             // code / SF staging complete (fenced per thread)
+          if (et == 0 && m0 < p.M) {
+            tma_store_2d(&g.pr[tr.i].nxq, smem + LY::cs_off, static_cast<int32_t>(n0 / 2), static_cast<int32_t>(m0));
+            const int64_t nkt_n = p.N / 64;              // 512-B scale-factor blocks per 128 rows
+            const int nblk = static_cast<int>(nkt_n - n0 / 64 < 3 ? nkt_n - n0 / 64 : 3);
+            bulk_store(p.nx_sf + (m0 >> 7) * nkt_n * 512 + (n0 / 64) * 512, smem + LY::sfs_off,
+                       static_cast<uint32_t>(nblk * 512));
+            bulk_commit_group();
+          }
           if (fx) {
             // leaving this 256-row block (or the range): read the accumulated X L1s_next^T rows from
             // TMEM once the MMAs of this tile are done, and write them to this pair's slot
