@@ -76,8 +76,9 @@ constexpr int SMEM = BAR_OFF + 256 + BN * 4 + 1024;
 template <bool kFuse>
 struct Lay {
   static constexpr int stages = kFuse ? 3 : kStages;
+  static constexpr int epi_w = kFuse ? 12 : 8;              // epilogue warps (3 or 2 per TMEM lane quadrant)
   static constexpr int epi_off = stages * STAGE;
-  static constexpr int bar_off = epi_off + EPI_BYTES;
+  static constexpr int bar_off = epi_off + (kFuse ? epi_w * 2048 * kEpiBuf : EPI_BYTES);
   static constexpr int bias_off = bar_off + 256;
   static constexpr int lamn_off = bias_off + BN * 4;
   static constexpr int at_off = (lamn_off + BN * 4 + 1023) / 1024 * 1024;
@@ -137,13 +138,14 @@ __device__ __forceinline__ TileRef locate(const K2PairArgs &g, int t) {
 }
 
 template <bool kFuse>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(kFuse ? 448 : 320, 1)
     k2_nvfp4_2sm_kernel(const __grid_constant__ K2PairArgs g) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~static_cast<uintptr_t>(1023));
   using LY = Lay<kFuse>;
   constexpr int kSt = LY::stages;
+  constexpr int kEpiW = LY::epi_w, kNWQ = kEpiW / 4, kEpiT = 32 * kEpiW;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + LY::bar_off);
   uint64_t *empty = full + kSt;
   uint64_t *acc_full = empty + kSt;       // [2]
@@ -174,10 +176,10 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 16);                      // 8 epilogue warps x 2 CTAs
+      mbar_init(&acc_empty[b], 2 * kEpiW);               // epilogue warps x 2 CTAs
     }
     if (kFuse) {
-      mbar_init(xa_full, 16);
+      mbar_init(xa_full, 2 * kEpiW);
       mbar_init(xa_empty, 1);
     }
     fence_mbar_init();
@@ -438,14 +440,14 @@ __global__ void __launch_bounds__(320, 1)
       const int64_t m0 = tr.m0 + 128 * crank;
       const int64_t n0 = tr.n0;
       if (kFuse && et == 0) bulk_wait_group_read<0>();    // previous tile's code / SF staging is read
-      named_bar(1, 256);
-      for (int c = et; c < BN; c += 256)
+      named_bar(1, kEpiT);
+      for (int c = et; c < BN; c += kEpiT)
         bias_s[c] = (p.bias && n0 + c < p.N) ? load_bias(p.bias, p.bias_dtype, n0 + c) : 0.f;
       const bool fx = kFuse && p.fuse && p.nx_r > 0;   // this tile feeds the X L1s_next^T MMA
       if constexpr (kFuse) {
         if (p.fuse) {
           float *lamn_s = reinterpret_cast<float *>(smem + LY::lamn_off);
-          for (int c = et; c < BN; c += 256) lamn_s[c] = n0 + c < p.N ? p.nx_lam_inv[n0 + c] : 0.f;
+          for (int c = et; c < BN; c += kEpiT) lamn_s[c] = n0 + c < p.N ? p.nx_lam_inv[n0 + c] : 0.f;
         }
         if (fx) {
           // this CTA's L1s_next rows [crank * r/2, +r/2) over the tile's 192 columns, SW128 K-major:
@@ -457,7 +459,7 @@ __global__ void __launch_bounds__(320, 1)
           uint4 val[2];
 #pragma unroll
           for (int k = 0; k < 2; ++k) {
-            const int v = et + 256 * k;
+            const int v = et + kEpiT * k;
             const int jl = v / (BN / 8), kv = v % (BN / 8);
             const int64_t col = n0 + kv * 8;
             val[k] = (v < rh * (BN / 8) && col < p.N)
@@ -467,7 +469,7 @@ __global__ void __launch_bounds__(320, 1)
           if (xl_cnt > 0) mbar_wait(xa_empty, (xl_cnt - 1) & 1);
 #pragma unroll
           for (int k = 0; k < 2; ++k) {
-            const int v = et + 256 * k;
+            const int v = et + kEpiT * k;
             const int jl = v / (BN / 8), kv = v % (BN / 8);
             if (v < rh * (BN / 8))
               sts128(smem_u32(bt) + (kv >> 3) * 2048 + jl * 128 + (((kv & 7) ^ (jl & 7)) << 4), val[k].x, val[k].y,
@@ -475,7 +477,7 @@ __global__ void __launch_bounds__(320, 1)
           }
         }
       }
-      named_bar(1, 256);
+      named_bar(1, kEpiT);
       { K2T_BEGIN(); mbar_wait(&acc_full[b], acc_ph); K2T_ACC(t_ewait); }
       tc_fence_after();
 #ifdef SVDQ_TRACE
@@ -538,7 +540,7 @@ __global__ void __launch_bounds__(320, 1)
 #endif
       if constexpr (kFuse) {
         if (p.fuse) {
-          epilogue_tile_next<BN, 2, kEpiBuf>(
+          epilogue_tile_next<BN, kNWQ, kEpiBuf>(
               tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.Y ? tmY : nullptr,
               static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
               smem + LY::epi_off + (warp - 2) * 2048 * kEpiBuf, ebuf, lane,
@@ -556,7 +558,7 @@ __global__ void __launch_bounds__(320, 1)
                 }
               },
               smem + LY::cs_off, smem + LY::sfs_off, quad);
-          named_bar(2, 256);                             // code / SF staging complete (fenced per thread)
+          named_bar(2, kEpiT);                           // code / SF staging complete (fenced per thread)
           if (et == 0 && m0 < p.M) {
             tma_store_2d(&g.pr[tr.i].nxq, smem + LY::cs_off, static_cast<int32_t>(n0 / 2), static_cast<int32_t>(m0));
             const int64_t nkt_n = p.N / 64;              // 512-B scale-factor blocks per 128 rows
@@ -597,7 +599,7 @@ __global__ void __launch_bounds__(320, 1)
           continue;
         }
       }
-      epilogue_tile<BN, 2, kEpiBuf>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
+      epilogue_tile<BN, kNWQ, kEpiBuf>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
                            tmY, static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
                            smem + LY::epi_off + (warp - 2) * 2048 * kEpiBuf, ebuf, lane, [&]() {
                           tc_fence_before();
@@ -647,7 +649,7 @@ cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
   if (fuse) {
     e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay<true>::smem);
     if (e != cudaSuccess) return e;
-    return launch_ex(k2_nvfp4_2sm_kernel<true>, dim3(static_cast<unsigned>(2 * pairs)), dim3(320), Lay<true>::smem, s, 2u, g);
+    return launch_ex(k2_nvfp4_2sm_kernel<true>, dim3(static_cast<unsigned>(2 * pairs)), dim3(448), Lay<true>::smem, s, 2u, g);
   }
   return launch_ex(k2_nvfp4_2sm_kernel<false>, dim3(static_cast<unsigned>(2 * pairs)), dim3(320), SMEM, s, 2u, g);
 }
