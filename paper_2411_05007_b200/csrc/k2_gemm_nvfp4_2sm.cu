@@ -54,6 +54,9 @@ constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;   // 34 KB
 #ifndef SVDQ_K2P_STAGES
 #define SVDQ_K2P_STAGES 5
 #endif
+#ifndef SVDQ_K2P_EPIW
+#define SVDQ_K2P_EPIW 8
+#endif
 #ifndef SVDQ_K2P_EPIBUF
 #define SVDQ_K2P_EPIBUF 2
 #endif
@@ -76,16 +79,16 @@ constexpr int SMEM = BAR_OFF + 256 + BN * 4 + 1024;
 template <bool kFuse>
 struct Lay {
   static constexpr int stages = kFuse ? 3 : kStages;
-  static constexpr int epi_w = kFuse ? 12 : 8;              // epilogue warps (3 or 2 per TMEM lane quadrant)
+  static constexpr int epi_w = kFuse ? 12 : SVDQ_K2P_EPIW;  // epilogue warps (2 or 3 per TMEM lane quadrant)
   static constexpr int epi_off = stages * STAGE;
-  static constexpr int bar_off = epi_off + (kFuse ? epi_w * 2048 * kEpiBuf : EPI_BYTES);
+  static constexpr int bar_off = epi_off + (epi_w != 8 ? epi_w * 2048 * kEpiBuf : EPI_BYTES);
   static constexpr int bias_off = bar_off + 256;
   static constexpr int lamn_off = bias_off + BN * 4;
   static constexpr int at_off = (lamn_off + BN * 4 + 1023) / 1024 * 1024;
   static constexpr int bt_off = at_off + 3 * 16384;
   static constexpr int cs_off = bt_off + 3 * 2048;         // next-layer code tile [128 x 96 B]
   static constexpr int sfs_off = cs_off + 128 * 96;         // next-layer scale factors, 3 x 512 B
-  static constexpr int smem = kFuse ? sfs_off + 3 * 512 + 1024 : SMEM;
+  static constexpr int smem = kFuse ? sfs_off + 3 * 512 + 1024 : bias_off + BN * 4 + 1024;
 };
 constexpr int XL1_COL = SF_BASE + 2 * SF_COLS;   // TMEM columns [480, 512): X L1s_next^T accumulator
 static_assert(XL1_COL + 32 <= 512, "TMEM budget (fused)");
@@ -138,7 +141,7 @@ __device__ __forceinline__ TileRef locate(const K2PairArgs &g, int t) {
 }
 
 template <bool kFuse>
-__global__ void __launch_bounds__(kFuse ? 448 : 320, 1)
+__global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
     k2_nvfp4_2sm_kernel(const __grid_constant__ K2PairArgs g) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -625,9 +628,10 @@ __global__ void __launch_bounds__(kFuse ? 448 : 320, 1)
 }  // namespace
 
 cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
-  static_assert(SMEM <= 227 * 1024, "smem budget");
+  static_assert(SMEM <= 227 * 1024 && Lay<false>::smem <= 227 * 1024, "smem budget");
   static_assert(Lay<true>::smem <= 227 * 1024, "smem budget (fused)");
-  cudaError_t e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  cudaError_t e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Lay<false>::smem);
   if (e != cudaSuccess) return e;
   static int num_sms = 0;
   if (!num_sms) {
@@ -651,7 +655,8 @@ cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     return launch_ex(k2_nvfp4_2sm_kernel<true>, dim3(static_cast<unsigned>(2 * pairs)), dim3(448), Lay<true>::smem, s, 2u, g);
   }
-  return launch_ex(k2_nvfp4_2sm_kernel<false>, dim3(static_cast<unsigned>(2 * pairs)), dim3(320), SMEM, s, 2u, g);
+  return launch_ex(k2_nvfp4_2sm_kernel<false>, dim3(static_cast<unsigned>(2 * pairs)), dim3(64 + 32 * SVDQ_K2P_EPIW),
+                   Lay<false>::smem, s, 2u, g);
 }
 
 int k2_pair_count(int64_t tiles) {
