@@ -679,7 +679,7 @@ def main():
     ap.add_argument("--fmt", default="nvfp4", choices=["nvfp4", "int4", "w8a8"])
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--ref-rows", type=int, default=32)
-    ap.add_argument("--cpu-rows", type=int, default=160)   # ~10-30 s of oracle CPU work
+    ap.add_argument("--cpu-rows", type=int, default=1024)   # ~10-30 s of oracle CPU work (weight prep is ~6 s of it)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the rank-0 overhead / library legs")
     args = ap.parse_args()

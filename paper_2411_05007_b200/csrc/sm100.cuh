@@ -288,6 +288,12 @@ __device__ __forceinline__ uint32_t mapa_u32(const void *p, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Relaxed remote arrive: no release fence (the release form waits for every outstanding memory
+// operation of the thread).  For a TMEM-buffer hand-back whose reads are already complete
+// (tcgen05.wait::ld) and ordered by tcgen05.fence::before_thread_sync.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 // 2D / 3D TMA loads issued by either CTA of a pair; bytes are accounted on the barrier at
 // `bar_cluster_addr` (the leader CTA's barrier).
 __device__ __forceinline__ void tma_load_2d_cg2(void *dst, const CUtensorMap *map, uint32_t bar_cluster_addr,
