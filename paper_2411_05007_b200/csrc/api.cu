@@ -503,6 +503,7 @@ svdq_status prepare_fused(int32_t n, const svdq_linear *const *layers, const uin
     const svdq_linear *Nx = nexts[i];
     if (!xq_next[i] || !xs_next[i]) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null next-layer buffer %d", i);
     if (!aligned16(xq_next[i])) return fail(SVDQ_ERR_ALIGNMENT, "xq_next must be 16-byte aligned");
+    if (!aligned16(xs_next[i])) return fail(SVDQ_ERR_ALIGNMENT, "xs_next must be 16-byte aligned");
     K2Prep k;
     const int slots = g->pr[i].p.nx_slots;
     svdq_status st = prepare_k2(layers[i], xq[i], xs[i], xl1[i], M[i], Y[i], SVDQ_BF16, layers[i]->N, true, &k,
@@ -560,6 +561,7 @@ svdq_status svdq_gemm_w4a4_lowrank_up_fused_next(int32_t n, const svdq_linear *c
   for (int i = 0; i < n; ++i) {
     if (g.pr[i].p.nx_r) {
       if (!xl1_next || !xl1_next[i]) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null xl1_next %d", i);
+      if (!aligned16(xl1_next[i])) return fail(SVDQ_ERR_ALIGNMENT, "xl1_next must be 16-byte aligned");
       g.pr[i].p.nx_part = reinterpret_cast<float *>(static_cast<uint8_t *>(ws) + off[i]);
     }
   }

@@ -235,13 +235,15 @@ cudaError_t gptq_zero_dead(double *R, const GptqState &st, int64_t K, int64_t N,
 const char *gptq_run(double *R, const GptqState &st, int64_t K, int64_t N, int fmt, bool scale_bf16, float gs,
                      const float *w8_scales, uint8_t *codes, uint8_t *scales, cudaStream_t s) {
   const size_t smem = (kB * kB + kB * kThreads) * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[64];                  // per device ordinal: the attribute is per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
     cudaFuncSetAttribute(gptq_block_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(gptq_block_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(gptq_block_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(gptq_block_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_set = true;
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
   cublasHandle_t hb = nullptr;
   if (cublasCreate(&hb) != CUBLAS_STATUS_SUCCESS) return "cublasCreate";

@@ -134,6 +134,9 @@ struct K2PairArgs {
   int npairs;             // set by the launcher
 };
 cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &args, cudaStream_t s);
+// SM count of the current device (cached per device ordinal; one source for every launcher
+// and for workspace sizing, so the two always agree)
+int device_sm_count();
 // CTA pairs the grouped launch will use for `tiles` tiles
 int k2_pair_count(int64_t tiles);
 // Slots per 256-row block of a fused problem's partial-sum buffer (upper bound for any pair

@@ -636,12 +636,7 @@ cudaError_t launch_k2_int4(const K2Maps &maps, const K2Params &p, cudaStream_t s
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   if (e != cudaSuccess) return e;
   if (p.rank > kMaxSlabs * 64 && !p.dbg_acc) return cudaErrorInvalidValue;
-  static int num_sms = 0;
-  if (!num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int num_sms = device_sm_count();
   const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
   const unsigned grid = static_cast<unsigned>(tiles < num_sms ? tiles : num_sms);
   return launch_ex(kern, dim3(grid), dim3(kThreads), SMEM, s, 1u, maps.a, maps.b, maps.xl1, maps.l2, p);

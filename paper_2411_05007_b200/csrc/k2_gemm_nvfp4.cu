@@ -348,12 +348,7 @@ static cudaError_t launch_bn(const K2Maps &maps, const K2Params &p, cudaStream_t
   auto kern = k2_nvfp4_kernel<BN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
-  static int num_sms = 0;
-  if (!num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int num_sms = device_sm_count();
   const int64_t tiles = ((p.M + 127) / 128) * ((p.N + BN - 1) / BN);
   const unsigned grid = static_cast<unsigned>(tiles < num_sms ? tiles : num_sms);
   return launch_ex(kern, dim3(grid), dim3(320), C::SMEM, s, 1u, maps.a, maps.b, maps.xl1, maps.l2, maps.y, p);

@@ -646,12 +646,6 @@ cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Lay<false>::smem);
   if (e != cudaSuccess) return e;
-  static int num_sms = 0;
-  if (!num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
   g.tile_begin[0] = 0;
   bool fuse = false;
   for (int i = 0; i < g.n; ++i) {
@@ -659,7 +653,7 @@ cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
     fuse = fuse || g.pr[i].p.fuse;
   }
   const int64_t tiles = g.tile_begin[g.n];
-  const int64_t pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  const int64_t pairs = k2_pair_count(tiles);
   static const int force_contig = [] { const char *e = std::getenv("SVDQ_K2_CONTIG"); return e ? std::atoi(e) : 0; }();
   g.contig = (fuse || force_contig) ? 1 : 0;      // SVDQ_K2_CONTIG=1: schedule ablation
   g.npairs = static_cast<int>(pairs);
@@ -672,10 +666,19 @@ cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
                    Lay<false>::smem, s, 2u, g);
 }
 
-int k2_pair_count(int64_t tiles) {
-  int dev = 0, sms = 0;
+int device_sm_count() {
+  static int cached[64];                      // 0 = not yet queried
+  int dev = 0;
   cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
+  int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cached[dev] = sms;
+  return sms;
+}
+
+int k2_pair_count(int64_t tiles) {
+  const int sms = device_sm_count();
   return static_cast<int>(tiles < sms / 2 ? tiles : sms / 2);
 }
 

@@ -43,6 +43,7 @@ def shard_scales(scales: torch.Tensor, fmt: str, K: int, N: int, n0: int, n: int
     """Slice the weight scales of output channels [n0, n0+n).
 
     INT4: [N][K/64] 16-bit rows -> contiguous row slice.
+    W8A8: [N] fp32 per-channel scales -> contiguous slice.
     NVFP4: 128x4 layout; when n0 and n are multiples of 128 the shard is a contiguous run of
     atoms, otherwise the shard's rows are re-laid out (byte gather) into a fresh 128x4 buffer
     whose padding rows are 0x00.
@@ -50,6 +51,10 @@ def shard_scales(scales: torch.Tensor, fmt: str, K: int, N: int, n0: int, n: int
     if fmt == "int4":
         g = K // 64
         return scales.view(torch.uint8)[n0 * g * 2:(n0 + n) * g * 2].clone()
+    if fmt == "w8a8":                                   # one fp32 scale per output channel
+        return scales.view(torch.uint8)[n0 * 4:(n0 + n) * 4].clone()
+    if fmt != "nvfp4":
+        raise ValueError(f"unsupported format {fmt!r}")
     atom = _sf_atom_bytes(K)
     if n0 % 128 == 0 and n % 128 == 0:
         return scales[(n0 // 128) * atom:((n0 + n) // 128) * atom].clone()
@@ -73,7 +78,10 @@ def shard_layer(full: QuantizedLinear, world: int, rank: int) -> QuantizedLinear
     """The rank-th column shard of a quantized layer (device buffers are sliced copies)."""
     n0, n = shard_bounds(full.N, world, rank)
     K, r = full.K, full.rank
-    codes = full.w_codes.view(torch.uint8)[n0 * (K // 2):(n0 + n) * (K // 2)].clone()
+    if full.fmt not in ("nvfp4", "int4", "w8a8"):
+        raise ValueError(f"unsupported format {full.fmt!r}")
+    row = K if full.fmt == "w8a8" else K // 2            # code bytes per output channel
+    codes = full.w_codes.view(torch.uint8)[n0 * row:(n0 + n) * row].clone()
     scales = shard_scales(full.w_scales, full.fmt, K, full.N, n0, n, full.scale_dtype)
     if r:
         l2s = full.l2s.view(torch.int16)[n0 * r:(n0 + n) * r].clone()

@@ -10,7 +10,7 @@ from helpers import layer_from_ops, make_case, need_cuda
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4", "w8a8"])
 @pytest.mark.parametrize("P_,N", [(2, 1536), (4, 3072), (8, 3072), (3, 480)])
 def test_sharded_equals_unsharded(fmt, P_, N):
     need_cuda()

@@ -115,19 +115,43 @@ def test_nonfinite_rejected():
 
 
 @pytest.mark.parametrize("size", [256, 1024, 4096])
-def test_prop42_monte_carlo(size):
-    """Prop. 4.2: E||R - Q(R)|| <= c sqrt(size)/q_max E||R||, with
-    the Gaussian c = sqrt(log(size) pi / size).  Per-tensor Eq. (1) quantizer
-    with real-valued scale (the proposition's setting), INT4 (q_max 7)."""
+@pytest.mark.parametrize("quantizer", ["int4_g64", "int8_per_tensor"])
+def test_prop42_monte_carlo(size, quantizer):
+    """Prop. 4.2 through the ORACLE's own quantizers:
+    E||R - Q(R)||_F <= c sqrt(size(R)) / q_max * E||R||_F with the Gaussian
+    c = sqrt(log(size) pi / size), R ~ N(0, 1) of `size` elements.
+      * int4_g64: oracle.quant.quantize_int4 (Eq. 1 per group of 64 with 16-bit scales, q_max 7);
+        every element's error is at most half its group's step, and a group step never exceeds
+        the per-tensor one (up to the 16-bit scale rounding), so the per-tensor bound applies.
+      * int8_per_tensor: oracle.quant.quantize_int8_rows on the tensor as ONE row -- exactly the
+        proposition's per-tensor Eq. (1) quantizer, q_max 127, fp32 scale."""
     rng = np.random.default_rng(size)
     trials = 200
     lhs, fr = [], []
     for _ in range(trials):
-        r = rng.standard_normal(size)
-        s = np.max(np.abs(r)) / 7.0
-        qr = s * np.clip(np.rint(r / s), -7, 7)
-        lhs.append(np.linalg.norm(r - qr))
-        fr.append(np.linalg.norm(r))
-    rhs = D.prop42_rhs(size, 7.0, np.mean(fr))
+        r = rng.standard_normal((1, size)).astype(np.float32)
+        if quantizer == "int4_g64":
+            q, sb = Q.quantize_int4(r, "bf16")
+            deq, qmax = Q.dequantize_int4(q, sb, "bf16"), 7.0
+        else:
+            q, sc = Q.quantize_int8_rows(r)
+            deq, qmax = Q.dequantize_int8_rows(q, sc), 127.0
+        # the proof's per-element step: |r - Q(r)| <= s / 2 (round to nearest; the max element
+        # is clamped at q_max but its overshoot is only the scale's storage rounding)
+        step = (F.from_bits16(sb, "bf16").astype(np.float64).repeat(64, axis=1) if quantizer == "int4_g64"
+                else np.asarray(sc, np.float64)[:, None])
+        assert np.all(np.abs(r.astype(np.float64) - deq) <= 0.5 * step * (1 + 1e-5))
+        lhs.append(np.linalg.norm(r.astype(np.float64) - deq))
+        fr.append(np.linalg.norm(r.astype(np.float64)))
+    rhs = D.prop42_rhs(size, qmax, np.mean(fr))
     se = np.std(lhs) / np.sqrt(trials)
     assert np.mean(lhs) <= rhs + 3 * se
+
+
+def test_prop42_regularity_condition_gaussian():
+    """The proposition's regularity condition with its Gaussian constant:
+    E max|R| <= c E||R||_F, c = sqrt(log(size) pi / size)."""
+    rng = np.random.default_rng(0)
+    for size in (256, 1024, 4096):
+        r = rng.standard_normal((400, size))
+        assert np.mean(np.abs(r).max(axis=1)) <= D.prop42_gaussian_c(size) * np.mean(np.linalg.norm(r, axis=1))

@@ -28,6 +28,13 @@ def _free_port():
 def _unpack_shard(ops, shard, n):
     """Device-layout shard buffers -> oracle Operands of the shard."""
     K = ops.K
+    if ops.fmt == "w8a8":
+        codes = shard.w_codes.numpy().view(np.int8).reshape(n, K).astype(np.int64)
+        scales = shard.w_scales.numpy().view(np.float32).reshape(n)
+        l2s = shard.l2s.numpy().view(np.uint16).reshape(n, ops.rank)
+        bias = shard.bias.numpy().astype(np.float32) if shard.bias is not None else None
+        return S.Operands(ops.fmt, K, n, ops.rank, codes, scales, ops.scale_dtype, ops.gs_w, ops.gs_x,
+                          ops.lam_inv32, ops.L1s_bits, l2s, bias)
     codes = F.unpack_nibbles(shard.w_codes.numpy().reshape(n, K // 2))
     if ops.fmt == "nvfp4":
         scales = F.sf_from_layout(shard.w_scales.numpy(), n, K)
@@ -73,7 +80,7 @@ def _worker(rank, world, port, fmt, N, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fmt,N", [("nvfp4", 512), ("nvfp4", 320), ("int4", 320)])
+@pytest.mark.parametrize("fmt,N", [("nvfp4", 512), ("nvfp4", 320), ("int4", 320), ("w8a8", 320)])
 def test_column_parallel_gloo_bitwise(fmt, N):
     """N = 512: shards are whole 128-row scale-factor atoms; N = 320: shard width 160
     forces the byte-gather re-layout of the 128x4 scale factors."""
