@@ -111,16 +111,20 @@ svdq_status svdq_weight_buffer_sizes(int32_t fmt, int64_t K, int64_t N, int32_t 
  * X: [dev] [M][ldx] of x_dtype (BF16 | FP16), ldx >= K elements, ldx % 8 == 0.
  * xq: [dev] [M][K/2]; xs: [dev] (see sizes); xl1: [dev] [M][rank] (may be NULL if rank == 0).
  * Bit-exact contract: xq and xs equal the oracle's codes / scales for the same X,
- * lambda_inv and gs_x, including the 0x00 padding rows of the NVFP4 layout.      */
+ * lambda_inv and gs_x, including the 0x00 padding rows of the NVFP4 layout.
+ * Implementation (k1_rows.cu): one CTA per 16/32/64/128 whole rows, TMA-staged X, the
+ * down-projection on tcgen05 (fp16 X as exact bf16 hi + lo parts); xl1 is deterministic.  */
 svdq_status svdq_quantize_act_lowrank_down(const svdq_linear *L, const void *X, int32_t x_dtype,
                                            int64_t M, int64_t ldx, uint8_t *xq, uint8_t *xs,
                                            uint16_t *xl1, void *stream);
 
-/* Grouped K1: n (1..4) independent problems (bf16 X; layers sharing format, rank and INT4
- * scale dtype) in ONE launch whose row tiles are the concatenation of the problems' row tiles.
- * Problem i is exactly svdq_quantize_act_lowrank_down(layers[i], X[i], BF16, M[i], ldx[i],
- * xq[i], xs[i], xl1[i]) (bit-identical outputs).  Arrays are [host], n entries each.
- * SVDQ_ERR_UNSUPPORTED for fp16 X or mixed format / rank.                             */
+/* Grouped K1: n (1..4) independent problems (bf16 or fp16 X; layers sharing format, rank and
+ * INT4 scale dtype; no W8A8) in ONE launch whose row tiles are the concatenation of the
+ * problems' row tiles.  Problem i computes svdq_quantize_act_lowrank_down(layers[i], X[i],
+ * x_dtype, M[i], ldx[i], xq[i], xs[i], xl1[i]): xq / xs bit-identical; xl1 bit-identical when
+ * the single launch uses the same row tile (the kernel sizes its row tile -- and with it the
+ * fp32 summation order of xl1 -- from the launch's total rows), else within the xl1 tolerance.
+ * Arrays are [host], n entries each.  SVDQ_ERR_UNSUPPORTED for mixed format / rank or W8A8.  */
 svdq_status svdq_quantize_act_lowrank_down_grouped(int32_t n, const svdq_linear *const *layers,
                                                    const void *const *X, int32_t x_dtype, const int64_t *M,
                                                    const int64_t *ldx, uint8_t *const *xq, uint8_t *const *xs,
@@ -295,6 +299,10 @@ const char *svdq_last_error(void);
 /* Number of this library's kernel launches issued by the calling thread (for bench claims). */
 uint64_t svdq_launch_count(void);
 int32_t svdq_version(void);
+/* Rows per CTA (16 / 32 / 64 / 128) the K1 kernel uses on the current device for a launch over
+ * `rows_padded` rows (sum of ceil(M_i/128)*128 over a group) at this rank: the smallest tile whose
+ * CTA count still fits one wave of SMs with 128/tile * rank <= 256.  Host-only query.          */
+int32_t svdq_k1_row_tile(int64_t rows_padded, int32_t rank);
 
 #ifdef __cplusplus
 }

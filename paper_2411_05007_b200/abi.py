@@ -46,7 +46,7 @@ EXPORTS = [
     "svdq_quantize_residual_gptq_workspace", "svdq_quantize_residual_gptq",
     "svdq_quantize_weights_gptq_workspace", "svdq_quantize_weights_gptq",
     "svdq_debug_int4_group_accum", "svdq_debug_codec", "svdq_status_string", "svdq_last_error",
-    "svdq_launch_count", "svdq_version",
+    "svdq_launch_count", "svdq_version", "svdq_k1_row_tile",
 ]
 
 
@@ -118,6 +118,8 @@ _lib.svdq_launch_count.argtypes = []
 _lib.svdq_launch_count.restype = C.c_uint64
 _lib.svdq_version.argtypes = []
 _lib.svdq_version.restype = C.c_int32
+_lib.svdq_k1_row_tile.argtypes = [C.c_int64, C.c_int32]
+_lib.svdq_k1_row_tile.restype = C.c_int32
 
 
 def _check(status: int, where: str):
@@ -154,6 +156,11 @@ def svdq_launch_count() -> int:
 
 def svdq_version() -> int:
     return int(_lib.svdq_version())
+
+
+def svdq_k1_row_tile(rows_padded: int, rank: int) -> int:
+    """Rows per CTA the K1 kernel uses for a launch over `rows_padded` rows (host-only query)."""
+    return int(_lib.svdq_k1_row_tile(rows_padded, rank))
 
 
 def svdq_act_buffer_sizes(fmt: str, M: int, K: int, rank: int):

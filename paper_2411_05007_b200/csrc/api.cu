@@ -121,6 +121,22 @@ svdq_status make_map(CUtensorMap *map, const void *base, CUtensorMapDataType dt,
   return SVDQ_OK;
 }
 
+// 3-D view of a row-major 16-bit activation X [rows][ldx]: {64 cols, K/64 blocks, rows}, box
+// {64, q, rt}, 128-byte swizzle (the row-tile K1's stage: q blocks of rt rows).
+svdq_status make_x3_map(CUtensorMap *map, const void *base, CUtensorMapDataType dt, int64_t K, int64_t rows,
+                        int64_t ldx_bytes, uint32_t q, uint32_t rt) {
+  auto fn = encode_fn();
+  if (!fn) return fail(SVDQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(K / 64), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(ldx_bytes)};
+  cuuint32_t box[3] = {64, q, rt};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, dt, 3, const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SVDQ_ERR_CUDA, "cuTensorMapEncodeTiled (X 3-D) failed (%d)", (int)r);
+  return SVDQ_OK;
+}
+
 // 3-D uint64 view of a 128x4 scale-factor buffer: [rows/128][K/64][512 B], box {64, 4, atoms}.
 svdq_status make_sf_map(CUtensorMap *map, const void *base, int64_t rows, int64_t K, uint32_t atoms) {
   auto fn = encode_fn();
@@ -177,7 +193,8 @@ const char *svdq_status_string(svdq_status s) {
 
 const char *svdq_last_error(void) { return g_err; }
 uint64_t svdq_launch_count(void) { return g_launches; }
-int32_t svdq_version(void) { return 1; }
+int32_t svdq_version(void) { return 2; }
+int32_t svdq_k1_row_tile(int64_t rows_padded, int32_t rank) { return k1_rows_rt(rows_padded, rank); }
 
 svdq_status svdq_act_buffer_sizes(int32_t fmt, int64_t M, int64_t K, int32_t rank, size_t *xq,
                                   size_t *xs, size_t *xl1) {
@@ -219,9 +236,9 @@ svdq_status svdq_weight_buffer_sizes(int32_t fmt, int64_t K, int64_t N, int32_t 
 }  // extern "C"
 
 namespace {
-// Validation, launch parameters and (bf16 X) tensor maps of one K1 problem.
+// Validation, launch parameters and tensor maps of one K1 problem (`out` may alias maps->p).
 svdq_status prepare_k1(const svdq_linear *L, const void *X, int32_t x_dtype, int64_t M, int64_t ldx, uint8_t *xq,
-                       uint8_t *xs, uint16_t *xl1, K1Params *out, K1Maps *maps) {
+                       uint8_t *xs, uint16_t *xl1, K1Params *out, K1Problem *maps, int rt) {
   svdq_status st = check_linear(L, false);
   if (st != SVDQ_OK) return st;
   if (!X || !xq || !xs || (L->rank > 0 && !xl1)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null buffer");
@@ -249,19 +266,22 @@ svdq_status prepare_k1(const svdq_linear *L, const void *X, int32_t x_dtype, int
   p.xq = xq;
   p.xs = xs;
   p.xl1 = xl1;
-  std::memset(maps, 0, sizeof(*maps));
-  if (p.x_bf16) {
-    // TMA + tcgen05 path: X tiles [128 x 64] and L1s tiles [rank x 64], 128-B swizzle
-    if ((st = make_map(&maps->x, X, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->K, M, ldx * 2, 64, 128)) != SVDQ_OK)
-      return st;
-    if (L->rank > 0 &&
-        (st = make_map(&maps->l1s, L->l1s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->K, L->rank, L->K * 2, 64,
-                       static_cast<uint32_t>(L->rank))) != SVDQ_OK)
-      return st;
-    if ((st = make_map(&maps->lam, L->lambda_inv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 32, L->K / 32, 128, 32, 2)) !=
-        SVDQ_OK)
-      return st;
-  }
+  std::memset(&maps->x, 0, sizeof(maps->x));
+  std::memset(&maps->l1s, 0, sizeof(maps->l1s));
+  std::memset(&maps->lam, 0, sizeof(maps->lam));
+  // row-tile kernel (k1_rows.cu): X boxes {64, 128/rt blocks, rt rows}, L1s tiles [rank x 64],
+  // lambda_inv rows of 32 fp32 (two per 64-wide block), all 128-B swizzled
+  const uint32_t q = static_cast<uint32_t>(128 / rt);
+  if ((st = make_x3_map(&maps->x, X, p.x_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                        L->K, M, ldx * 2, q, static_cast<uint32_t>(rt))) != SVDQ_OK)
+    return st;
+  if (L->rank > 0 &&
+      (st = make_map(&maps->l1s, L->l1s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->K, L->rank, L->K * 2, 64,
+                     static_cast<uint32_t>(L->rank))) != SVDQ_OK)
+    return st;
+  if ((st = make_map(&maps->lam, L->lambda_inv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 32, L->K / 32, 128, 32, 2 * q)) !=
+      SVDQ_OK)
+    return st;
   return SVDQ_OK;
 }
 }  // namespace
@@ -271,14 +291,16 @@ extern "C" {
 svdq_status svdq_quantize_act_lowrank_down(const svdq_linear *L, const void *X, int32_t x_dtype,
                                            int64_t M, int64_t ldx, uint8_t *xq, uint8_t *xs,
                                            uint16_t *xl1, void *stream) {
-  K1Params p;
-  K1Maps maps;
-  svdq_status st = prepare_k1(L, X, x_dtype, M, ldx, xq, xs, xl1, &p, &maps);
+  K1Args g;
+  std::memset(&g, 0, sizeof(g));
+  g.n = 1;
+  const int rt = k1_rows_rt(((M + 127) / 128) * 128, L ? L->rank : 0);
+  svdq_status st = prepare_k1(L, X, x_dtype, M, ldx, xq, xs, xl1, &g.pr[0].p, &g.pr[0], rt);
   if (st != SVDQ_OK) return st;
+  const K1Params &p = g.pr[0].p;
   cudaError_t e = cudaSuccess;
-  if (p.fmt != 2 || p.rank > 0) {      // W8A8: these kernels run the down-projection only
-    e = p.x_bf16 ? launch_k1_tc(maps, p, static_cast<cudaStream_t>(stream))
-                 : launch_k1(p, static_cast<cudaStream_t>(stream));
+  if (p.fmt != 2 || p.rank > 0) {      // W8A8: the row-tile kernel runs the down-projection only
+    e = launch_k1_rows_group(g, rt, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "K1 launch");
     ++g_launches;
   }
@@ -296,25 +318,23 @@ svdq_status svdq_quantize_act_lowrank_down_grouped(int32_t n, const svdq_linear 
                                                    uint16_t *const *xl1, void *stream) {
   if (n < 1 || n > kMaxGroup1) return fail(SVDQ_ERR_INVALID_ARGUMENT, "group size must be 1..%d", kMaxGroup1);
   if (!layers || !X || !M || !ldx || !xq || !xs || !xl1) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null array");
-  if (x_dtype != SVDQ_BF16) return fail(SVDQ_ERR_UNSUPPORTED, "grouped K1 needs bf16 activations");
   for (int i = 0; i < n; ++i)
     if (layers[i] && layers[i]->fmt == SVDQ_FMT_W8A8) return fail(SVDQ_ERR_UNSUPPORTED, "grouped K1: no W8A8");
   K1Args g;
   std::memset(&g, 0, sizeof(g));
   g.n = n;
+  int64_t rows_total = 0;
+  for (int i = 0; i < n; ++i) rows_total += ((M[i] + 127) / 128) * 128;
+  const int rt = k1_rows_rt(rows_total, layers[0] ? layers[0]->rank : 0);
   for (int i = 0; i < n; ++i) {
     if (!layers[i]) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null layer %d", i);
     if (layers[i]->fmt != layers[0]->fmt || layers[i]->rank != layers[0]->rank ||
         (layers[i]->fmt == SVDQ_FMT_INT4 && layers[i]->scale_dtype != layers[0]->scale_dtype))
       return fail(SVDQ_ERR_UNSUPPORTED, "grouped K1: layers must share format, rank and scale dtype");
-    K1Maps maps;
-    svdq_status st = prepare_k1(layers[i], X[i], x_dtype, M[i], ldx[i], xq[i], xs[i], xl1[i], &g.pr[i].p, &maps);
+    svdq_status st = prepare_k1(layers[i], X[i], x_dtype, M[i], ldx[i], xq[i], xs[i], xl1[i], &g.pr[i].p, &g.pr[i], rt);
     if (st != SVDQ_OK) return st;
-    g.pr[i].x = maps.x;
-    g.pr[i].l1s = maps.l1s;
-    g.pr[i].lam = maps.lam;
   }
-  cudaError_t e = launch_k1_tc_group(g, static_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_k1_rows_group(g, rt, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "grouped K1 launch");
   ++g_launches;
   return SVDQ_OK;

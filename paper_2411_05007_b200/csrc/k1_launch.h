@@ -58,12 +58,7 @@ struct K1Params {
   uint8_t *xs;
   uint16_t *xl1;
 };
-cudaError_t launch_k1(const K1Params &p, cudaStream_t s);       // mma.sync path (fp16 X)
 cudaError_t launch_k1_int8_rows(const K1Params &p, cudaStream_t s);   // W8A8 per-token INT8 codes
-struct K1Maps {
-  CUtensorMap x, l1s, lam;    // lam: lambda_inv viewed as [K/32][32] fp32, box {32, 2}, 128-B swizzle
-};
-cudaError_t launch_k1_tc(const K1Maps &maps, const K1Params &p, cudaStream_t s);   // bf16 X
 // Grouped K1: up to kMaxGroup1 problems (same fmt, scale dtype and rank) in one launch; the
 // grid's row-tile axis runs over the concatenated row tiles.
 constexpr int kMaxGroup1 = 4;
@@ -76,8 +71,16 @@ struct K1Args {
   int n;
   int tile_begin[kMaxGroup1 + 1];
 };
-cudaError_t launch_k1_tc_group(K1Args &g, cudaStream_t s);
-int k1_tc_ksplit(int64_t Mpad, int64_t K);
+// Row-tile K1 (k1_rows.cu, round 2): each CTA owns `rt` whole rows over the full K; maps: X as the
+// 3-D view {64 cols, K/64 blocks, M rows} with box {64, 128/rt, rt}, L1s box {64, rank}, lambda_inv
+// as [K/32][32] with box {32, 2 * 128/rt}.  bf16 or fp16 X.
+struct K1RowLayout {
+  int rt, q, x_bytes, l1_bytes, stage_bytes, stages;
+  size_t bar_off, smem;
+};
+K1RowLayout k1_row_layout(int rt, int rank, bool x16);
+int k1_rows_rt(int64_t rows_total, int rank);            // row tile for `rows_total` padded rows
+cudaError_t launch_k1_rows_group(K1Args &g, int rt, cudaStream_t s);
 
 struct K2Params {
   int64_t M, N, K, Npad;

@@ -1,0 +1,478 @@
+// K1 (round 2): smoothing + activation quantization + low-rank down-projection on ONE read of X
+// ("Fused Quantize + Down Projection", Fig. 5(b)), row-tile design.
+//
+// Every CTA owns RT whole rows of X (RT = 16 / 32 / 64 / 128, chosen so that one wave covers all
+// 148 SMs) and streams them over the full K -- so no CTA ever needs another CTA's partial sums:
+// no cluster, no distributed-shared-memory reduction, no trailing cluster barrier.
+//
+//   stage i = Q = 128 / RT consecutive 64-wide K blocks of the CTA's RT rows, staged by ONE 3-D TMA
+//             box {64 cols, Q blocks, RT rows} (128-B swizzle) as a [128 rows x 128 B] K-major tile
+//             whose row m * Q + q holds block q of row m;
+//   warp 0    TMA producer (X box, Q L1s tiles [r x 64], lambda_inv of the Q blocks);
+//   warp 1    TMEM allocator + MMA issuer: D[128 x Q*r] += A[128 x 64] . B[Q*r x 64]^T with
+//             B row q' * r + t = L1s[t, block q'] (tcgen05.mma kind::f16, fp32 in TMEM).  The
+//             diagonal entries D[m Q + q, q r + t] accumulate sum_k X[m, k] L1s[t, k] over the k of
+//             block q of every stage; the off-diagonal products are discarded (the MMA is ~1/3 of
+//             the HBM time, so the Q-fold extra tensor work is free);
+//   warps 2..17  quantizers, one 16-element NVFP4 group (a quarter of an INT4 group) per lane per
+//             stage: x_hat = fl32(x * lambda_inv), App. B recipe bit-exact, codes + scales stored.
+//             fp16 X: they also split the tile into bf16 hi (in place) + lo parts, X = hi + lo
+//             exactly, and the MMA warp issues hi . L1s^T + lo . L1s^T (kind::f16 takes one type).
+//   tail      xl1[m, t] = bf16(sum_q D[m Q + q, q r + t]) in fixed q order (deterministic).
+// X rows >= M are zero-filled by TMA, so the NVFP4 padding rows of the 128x4 scale layout get 0x00.
+#include <cstdint>
+#include <cstdlib>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "formats.cuh"
+#include "k1_launch.h"
+#include "sm100.cuh"
+
+#ifndef SVDQ_K1REXP
+#define SVDQ_K1REXP 0   // ablation bits: 1 no quantizer math / stores, 2 no MMA, 4 no L1s loads
+#endif
+#ifndef SVDQ_K1R_PF
+#define SVDQ_K1R_PF 0   // 1: quantizer lanes L2-prefetch X S + 2 stages ahead (measured slower)
+#endif
+
+#ifdef SVDQ_TRACE
+namespace svdq { __device__ unsigned long long g_k1r_trace[256]; }
+extern "C" int svdq_k1r_trace_read(unsigned long long *host) {
+  return cudaMemcpyFromSymbol(host, svdq::g_k1r_trace, sizeof(unsigned long long) * 256) == cudaSuccess ? 0 : 1;
+}
+__device__ __forceinline__ unsigned long long k1r_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define RTRACE(slot) \
+  do { if (blockIdx.x == 0) svdq::g_k1r_trace[(slot)] = k1r_gtime(); } while (0)
+#else
+#define RTRACE(slot) do {} while (0)
+#endif
+
+namespace svdq {
+
+namespace {
+
+constexpr int kQuantWarps = 16;
+constexpr int kThreads = 32 * (2 + kQuantWarps);
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {     // sm_100a packed FMUL2
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t pack64(uint32_t lo, uint32_t hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "r"(lo), "r"(hi));
+  return d;
+}
+__device__ __forceinline__ float lo32(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); }
+__device__ __forceinline__ float hi32(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
+// two 16-bit activations in one word -> fp32 pair (exact), low element in the low word
+template <bool kX16>
+__device__ __forceinline__ uint64_t x2_to_f32x2(uint32_t w) {
+  if constexpr (kX16) {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&w));
+    return pack64(__float_as_uint(f.x), __float_as_uint(f.y));
+  } else {
+    return pack64(w << 16, w & 0xFFFF0000u);
+  }
+}
+__device__ __forceinline__ void lds_v2x64(uint32_t addr, uint64_t &a, uint64_t &b) {
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(addr));
+}
+// four packed fp32 pairs -> 32 bits of E2M1 (pair j -> byte j, low element in the low nibble)
+__device__ __forceinline__ uint32_t e2m1x8_pairs(uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+  uint32_t r;
+  asm("{\n\t.reg .b8 b0, b1, b2, b3;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b0, %2, %1;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b1, %4, %3;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b2, %6, %5;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b3, %8, %7;\n\t"
+      "mov.b32 %0, {b0, b1, b2, b3};\n\t}\n"
+      : "=r"(r)
+      : "f"(lo32(a)), "f"(hi32(a)), "f"(lo32(b)), "f"(hi32(b)), "f"(lo32(c)), "f"(hi32(c)), "f"(lo32(d)),
+        "f"(hi32(d)));
+  return r;
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  return static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(lo))) |
+         (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(hi))) << 16);
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int32_t c0, int32_t c1,
+                                            int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *map, int32_t c0, int32_t c1, int32_t c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
+}  // namespace
+
+K1RowLayout k1_row_layout(int rt, int rank, bool x16) {
+  K1RowLayout L;
+  L.rt = rt;
+  L.q = 128 / rt;
+  L.x_bytes = x16 ? 32768 : 16384;                   // fp16 X: + the bf16 low parts (hi stays in place)
+  L.l1_bytes = L.q * rank * 128;
+  L.stage_bytes = (L.x_bytes + L.l1_bytes + L.q * 256 + 1023) / 1024 * 1024;
+  int s = (200 * 1024) / L.stage_bytes;
+  L.stages = s > 8 ? 8 : (s < 2 ? 2 : s);
+  L.bar_off = static_cast<size_t>(L.stages) * L.stage_bytes;
+  L.smem = L.bar_off + 256 + 1024 + 1024;            // barriers, 256-entry qinv table, alignment slack
+  return L;
+}
+
+namespace {
+
+template <int kFmt, bool kScaleBf16, bool kX16>
+__global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_constant__ K1Args g, K1RowLayout Ly) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~static_cast<uintptr_t>(1023));
+  int pi = 0;                                                  // problem of this row tile
+  while (pi + 1 < g.n && static_cast<int>(blockIdx.x) >= g.tile_begin[pi + 1]) ++pi;
+  const K1Params &p = g.pr[pi].p;
+  const CUtensorMap &tmX = g.pr[pi].x, &tmL = g.pr[pi].l1s, &tmLam = g.pr[pi].lam;
+  const int r = p.rank;
+  const int RT = Ly.rt, Q = Ly.q, S = Ly.stages;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + Ly.bar_off);
+  uint64_t *empty = full + 8;
+  uint64_t *conv = empty + 8;                                  // fp16 X: hi / lo tiles written
+  uint64_t *dfull = conv + 8;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dfull + 1);
+  float *qinv_lut = reinterpret_cast<float *>(smem + Ly.bar_off + 256);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t K = p.K;
+  const int nkb = static_cast<int>(K / 64);
+  const int nsteps = (nkb + Q - 1) / Q;                        // the last stage may hold < Q blocks
+  const int64_t row0 = static_cast<int64_t>(static_cast<int>(blockIdx.x) - g.tile_begin[pi]) * RT;
+  uint32_t tcols = 32;
+  while (tcols < static_cast<uint32_t>(Q * r)) tcols <<= 1;
+
+  if (threadIdx.x == 0) RTRACE(0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kQuantWarps + (r ? 1 : 0));
+      mbar_init(&conv[s], kQuantWarps);
+    }
+    mbar_init(dfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmX);
+    if (r) tma_prefetch(&tmL);
+    tma_prefetch(&tmLam);
+  }
+  if (warp == 1 && r) tmem_alloc_n(tmem_slot, tcols);
+  if (kFmt == 0 && threadIdx.x >= 64 && threadIdx.x < 64 + 256) {
+    const uint32_t code = threadIdx.x - 64;                   // UE4M3 byte; 0x7F.. never produced
+    const float sfd = e4m3_to_f32(code & 0x7F);
+    qinv_lut[code] = sfd == 0.f ? 0.f : __frcp_rn(__fmul_rn(sfd, p.gs_x));
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = r ? *tmem_slot : 0;
+  if (threadIdx.x == 0) RTRACE(1);
+  griddep_launch_dependents();                                 // the next kernel may start its prologue
+
+  if (warp == 0) {
+    // -------------------------------------------------------------------- producer
+    if (elect_one()) {
+      // every box is loaded whole: blocks past K are zero-filled by TMA (and counted), so the
+      // last stage's unused B rows are zeros, never stale smem
+      const uint32_t stage_tx = static_cast<uint32_t>(16384 + ((SVDQ_K1REXP & 4) ? 0 : Q * r * 128) + Q * 256);
+      auto load_weights = [&](int i) {
+        const int s = i % S;
+        uint8_t *st = smem + s * Ly.stage_bytes;
+        mbar_arrive_expect_tx(&full[s], stage_tx);
+        for (int q = 0; q < Q && r && !(SVDQ_K1REXP & 4); ++q)
+          tma_load_2d(st + Ly.x_bytes + q * r * 128, &tmL, &full[s], (i * Q + q) * 64, 0);
+        // lambda_inv of the nb blocks as [2 nb][32] fp32 rows, 128-B swizzle (conflict-free broadcasts)
+        tma_load_2d(st + Ly.x_bytes + Q * r * 128, &tmLam, &full[s], 0, (i * Q) * 2);
+      };
+      // Before the programmatic dependency resolves (the previous kernel may still run and may
+      // write X): stage the first ring's L1s / lambda tiles (no kernel of this stream writes them).
+      // X itself is warmed in L2 by the quantizer lanes' prefetches (LSU, not the TMA queue).
+      for (int i = 0; i < nsteps && i < S; ++i) load_weights(i);
+      griddep_wait();
+      for (int i = 0; i < nsteps; ++i) {
+        const int s = i % S;
+        if (i >= S) {
+          mbar_wait_spin(&empty[s], ((i / S) & 1) ^ 1);
+          load_weights(i);
+        }
+        if (i < 64) RTRACE(2 + i);
+        // X box {64 cols, Q blocks, RT rows}; blocks past K / rows past M are zero-filled (and
+        // still counted in the transaction bytes)
+        tma_load_3d(smem + s * Ly.stage_bytes, &tmX, &full[s], 0, i * Q, static_cast<int32_t>(row0));
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------------------- MMA issuer
+    if (r) {
+      const uint32_t idesc = idesc_bf16(128, static_cast<uint32_t>(Q * r));
+      for (int i = 0; i < nsteps; ++i) {
+        const int s = i % S;
+        mbar_wait_spin(&full[s], (i / S) & 1);
+        if (kX16) mbar_wait_spin(&conv[s], (i / S) & 1);      // hi / lo bf16 tiles written
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t xa = smem_u32(smem + s * Ly.stage_bytes);
+          const uint32_t la = xa + Ly.x_bytes;
+#pragma unroll
+          for (int j = 0; j < ((SVDQ_K1REXP & 2) ? 0 : 4); ++j)
+            mma_bf16(tmem, sdesc_kmajor_sw128(xa + 32 * j), sdesc_kmajor_sw128(la + 32 * j), idesc,
+                     (i | j) != 0);
+          if (kX16) {                                            // + X_lo . L1s^T (X = hi + lo exactly)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              mma_bf16(tmem, sdesc_kmajor_sw128(xa + 16384 + 32 * j), sdesc_kmajor_sw128(la + 32 * j), idesc, 1u);
+          }
+          tc_commit(&empty[s]);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) tc_commit(dfull);
+      __syncwarp();
+    }
+  } else {
+    // -------------------------------------------------------------------- quantizers
+    const int qw = warp - 2;
+    const int R = qw * 8 + (lane >> 2);                         // staged tile row = m * Q + qb
+    const int q4 = lane & 3;                                    // 16-element group within the block
+    const int m = R / Q;                                        // row within the tile
+    const int qb = R % Q;                                       // K block within the stage
+    const int64_t row = row0 + m;
+    const bool rvalid = row < p.M;
+    const float t6 = __fmul_rn(__frcp_rn(p.gs_x), __frcp_rn(6.0f));
+    uint2 *xq_ptr = reinterpret_cast<uint2 *>(p.xq + row * (K / 2) + static_cast<int64_t>(qb) * 32) + q4;
+    uint8_t *sf_ptr = p.xs + sf_offset(row, 0, K) + static_cast<int64_t>(qb) * 512 + q4;
+    uint16_t *s16_ptr = reinterpret_cast<uint16_t *>(p.xs) + row * (K / 64) + qb;
+    // L2 prefetch of this lane's future X lines (one 128-B line per staged row, issued by the q4 == 0
+    // lane): kPf stages ahead, so the TMA loads find X in L2 instead of paying the DRAM round trip
+    // with only S stages in flight.  An L2 prefetch never returns stale data, so the first ones go
+    // out before the programmatic dependency resolves.
+    const char *xrow = static_cast<const char *>(p.X) + (row < p.M ? row : p.M - 1) * p.ldx * 2 + qb * 128;
+    const int pf_dist = S + 2;
+    auto x_prefetch = [&](int st) {
+      if (SVDQ_K1R_PF && q4 == 0 && st < nsteps && st * Q + qb < nkb)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(xrow + static_cast<int64_t>(st) * Q * 128));
+    };
+    for (int st = 0; st < pf_dist; ++st) x_prefetch(st);
+    const uint32_t swz = static_cast<uint32_t>(R & 7);
+    const uint32_t lut = smem_u32(qinv_lut);
+    const uint32_t stage0 = smem_u32(smem);
+    // lambda row j = 2 qb + (q4 >> 1) of the swizzled [2Q][128 B] block; chunk (q4 & 1) * 4 + t
+    const int jl = 2 * qb + (q4 >> 1);
+    uint32_t lam_off[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      lam_off[t] = static_cast<uint32_t>(jl * 128 + ((((q4 & 1) * 4 + t) ^ (jl & 7)) * 16));
+    const uint32_t lam_base = static_cast<uint32_t>(Ly.x_bytes + Q * r * 128);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < nsteps; ++i, xq_ptr += Q * 4, sf_ptr += Q * 512, s16_ptr += Q) {
+      x_prefetch(i + pf_dist);
+      mbar_wait(&full[s], ph);
+      if (qw == 0 && lane == 0 && i < 64) RTRACE(110 + i);
+      const bool active = i * Q + qb < nkb;                     // this lane's block exists (last stage)
+      if (kFmt == 2 && !kX16) {                                 // W8A8: the MMA warp alone uses the tile
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == S) { s = 0; ph ^= 1; }
+        continue;
+      }
+      const uint32_t sbase = stage0 + s * Ly.stage_bytes;
+      const uint32_t xa = sbase + R * 128;
+      const uint32_t la = sbase + lam_base;
+      uint64_t xh[8];                                           // x_hat pairs = fl32(x * lambda_inv)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint64_t l0, l1, l2, l3;
+        lds_v2x64(la + lam_off[2 * c], l0, l1);
+        lds_v2x64(la + lam_off[2 * c + 1], l2, l3);
+        const uint32_t xaddr = xa + ((static_cast<uint32_t>(2 * q4 + c) ^ swz) * 16);
+        const uint4 v = lds128(xaddr);
+        const uint64_t x0 = x2_to_f32x2<kX16>(v.x), x1 = x2_to_f32x2<kX16>(v.y);
+        const uint64_t x2 = x2_to_f32x2<kX16>(v.z), x3 = x2_to_f32x2<kX16>(v.w);
+        if constexpr (kX16) {
+          // fp16 X -> hi = bf16(x) (in place) + lo = bf16(x - hi) (the lo tile): both exact, so the
+          // bf16 x bf16 MMAs reproduce X . L1s^T (kind::f16 takes one A/B type)
+          uint32_t hw[4], lw[4];
+          const uint64_t xs4[4] = {x0, x1, x2, x3};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float a = lo32(xs4[t]), b = hi32(xs4[t]);
+            const uint32_t h = pack_bf16x2(a, b);
+            hw[t] = h;
+            lw[t] = pack_bf16x2(a - __uint_as_float(h << 16), b - __uint_as_float(h & 0xFFFF0000u));
+          }
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(xaddr), "r"(hw[0]), "r"(hw[1]), "r"(hw[2]),
+                       "r"(hw[3]) : "memory");
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(xaddr + 16384), "r"(lw[0]), "r"(lw[1]),
+                       "r"(lw[2]), "r"(lw[3]) : "memory");
+        }
+        xh[4 * c + 0] = fmul2(x0, l0);
+        xh[4 * c + 1] = fmul2(x1, l1);
+        xh[4 * c + 2] = fmul2(x2, l2);
+        xh[4 * c + 3] = fmul2(x3, l3);
+      }
+      if constexpr (kX16) {
+        fence_proxy_async();                                    // generic smem writes -> tcgen05 reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);                   // tile consumed: values in registers
+      if (++s == S) { s = 0; ph ^= 1; }
+      if constexpr (kFmt == 2) continue;                        // W8A8 (fp16 X): conversion only
+      if (SVDQ_K1REXP & 1) {
+        if (xh[0] == 12345ull) p.xq[0] = 1;                     // keep the loads alive
+        continue;
+      }
+      float am[8];                                              // |x_hat| max as a tree (short chain)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) am[j] = fmaxf(fabsf(lo32(xh[j])), fabsf(hi32(xh[j])));
+      float amax = fmaxf(fmaxf(fmaxf(am[0], am[1]), fmaxf(am[2], am[3])), fmaxf(fmaxf(am[4], am[5]), fmaxf(am[6], am[7])));
+      if constexpr (kFmt == 0) {
+        const uint32_t sf = e4m3_rn_sat(__fmul_rn(amax, t6));
+        float qinv;
+        asm("ld.shared.f32 %0, [%1];" : "=f"(qinv) : "r"(lut + sf * 4));
+        const uint64_t q2 = pack64(__float_as_uint(qinv), __float_as_uint(qinv));
+        const uint32_t w0 = e2m1x8_pairs(fmul2(xh[0], q2), fmul2(xh[1], q2), fmul2(xh[2], q2), fmul2(xh[3], q2));
+        const uint32_t w1 = e2m1x8_pairs(fmul2(xh[4], q2), fmul2(xh[5], q2), fmul2(xh[6], q2), fmul2(xh[7], q2));
+        if (active) {
+          if (rvalid) *xq_ptr = make_uint2(w0, w1);
+          *sf_ptr = static_cast<uint8_t>(sf);                   // padding rows (>= M) get 0x00
+        }
+      } else {
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+        const uint16_t sc = scale16_rn_sat<kScaleBf16>(__fdiv_rn(amax, 7.0f));
+        const float sd = scale16_to_f32<kScaleBf16>(sc);
+        const float qinv = sd == 0.f ? 0.f : __frcp_rn(sd);
+        const uint64_t q2 = pack64(__float_as_uint(qinv), __float_as_uint(qinv));
+        uint32_t w[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint64_t t = fmul2(xh[4 * c + j], q2);
+            const int v0 = max(-7, min(7, __float2int_rn(lo32(t))));
+            const int v1 = max(-7, min(7, __float2int_rn(hi32(t))));
+            word |= ((static_cast<uint32_t>(v0) & 0xFu) | ((static_cast<uint32_t>(v1) & 0xFu) << 4)) << (8 * j);
+          }
+          w[c] = word;
+        }
+        if (rvalid && active) {
+          *xq_ptr = make_uint2(w[0], w[1]);
+          if (q4 == 0) *s16_ptr = sc;
+        }
+      }
+    }
+  }
+
+  if (threadIdx.x == 64) RTRACE(100);                          // quantizer 0 done
+  if (r == 0) return;
+  // ---------------------------------------------------------------------- xl1 = sum_q diag blocks
+  __syncthreads();                                             // every stage consumed: ring reusable
+  float *red = reinterpret_cast<float *>(smem);                // [Q][RT][r + 4] fp32 (<= 68 KB)
+  const int rs = r + 4;                                        // padded row stride: fewer bank conflicts
+  if (warp >= 2 && warp < 6) {
+    const int qd = warp & 3;                                   // TMEM lane quadrant of this warp
+    const int d = 32 * qd + lane;                              // D row = m * Q + q
+    const int q = d % Q, mm = d / Q;
+    mbar_wait_spin(dfull, 0);
+    tc_fence_after();
+    for (int qq = 0; qq < Q; ++qq) {
+      for (int c = 0; c < r; c += 16) {
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(32 * qd) << 16) + qq * r + c, v);
+        tmem_ld_wait();
+        if (qq == q) {                                         // the diagonal block of this lane's row
+          float *dst = red + (q * RT + mm) * rs + c;
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4 *>(dst + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                                               __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc_n(tmem, tcols);
+  for (int idx = threadIdx.x; idx < RT * (r / 2); idx += kThreads) {
+    const int mm = idx / (r / 2);
+    const int col = 2 * (idx % (r / 2));
+    float s0 = 0.f, s1 = 0.f;
+    for (int q = 0; q < Q; ++q) {                              // fixed block order: deterministic
+      const float2 v = *reinterpret_cast<const float2 *>(red + (q * RT + mm) * rs + col);
+      s0 += v.x;
+      s1 += v.y;
+    }
+    const int64_t row = row0 + mm;
+    if (row < p.M) *reinterpret_cast<uint32_t *>(p.xl1 + row * r + col) = pack_bf16x2(s0, s1);
+  }
+  if (threadIdx.x == 64) RTRACE(101);
+}
+
+template <int kFmt, bool kScaleBf16, bool kX16>
+cudaError_t launch_t(K1Args &g, const K1RowLayout &Ly, cudaStream_t s) {
+  auto kern = k1_rows_kernel<kFmt, kScaleBf16, kX16>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Ly.smem));
+  if (e != cudaSuccess) return e;
+  return launch_ex(kern, dim3(static_cast<unsigned>(g.tile_begin[g.n])), dim3(kThreads, 1, 1), Ly.smem, s, 1u, g, Ly);
+}
+
+}  // namespace
+
+int k1_rows_rt(int64_t rows_total, int rank) {
+  // smallest row tile (most CTAs) whose tile count still fits one wave; Q * rank <= 256 (MMA N)
+  const int sms = device_sm_count();
+  int rt = 128;
+  for (int cand = 64; cand >= 16; cand /= 2) {
+    if ((128 / cand) * rank > 256) break;
+    if (rows_total / cand > sms) break;
+    rt = cand;
+  }
+  return rt;
+}
+
+cudaError_t launch_k1_rows_group(K1Args &g, int rt, cudaStream_t s) {
+  const K1Params &p = g.pr[0].p;
+  const K1RowLayout Ly = k1_row_layout(rt, p.rank, !p.x_bf16);
+  g.tile_begin[0] = 0;
+  for (int i = 0; i < g.n; ++i) g.tile_begin[i + 1] = g.tile_begin[i] + static_cast<int>(g.pr[i].p.Mpad / rt);
+  if (p.x_bf16) {
+    if (p.fmt == 2) return launch_t<2, true, false>(g, Ly, s);
+    if (p.fmt == 0) return launch_t<0, true, false>(g, Ly, s);
+    return p.scale_bf16 ? launch_t<1, true, false>(g, Ly, s) : launch_t<1, false, false>(g, Ly, s);
+  }
+  if (p.fmt == 2) return launch_t<2, true, true>(g, Ly, s);
+  if (p.fmt == 0) return launch_t<0, true, true>(g, Ly, s);
+  return p.scale_bf16 ? launch_t<1, true, true>(g, Ly, s) : launch_t<1, false, true>(g, Ly, s);
+}
+
+}  // namespace svdq

@@ -93,14 +93,14 @@ def test_grouped_argument_validation_before_device():
     assert st == 1
     st = lib.svdq_quantize_act_lowrank_down_grouped(9, None, None, 0, None, None, None, None, None, None)
     assert st == 1
-    # fp16 activations are not supported by the grouped K1 (bf16 TMA path only)
+    # fp16 activations are accepted by the grouped K1 (row-tile kernel); the NULL X is rejected
     L = P.abi.svdq_linear()
     L.fmt, L.K, L.N, L.rank = 0, 128, 64, 16
     arr = (ctypes.POINTER(P.abi.svdq_linear) * 1)(ctypes.pointer(L))
     one = (ctypes.c_void_p * 1)(None)
     i64 = (ctypes.c_int64 * 1)(8)
     st = lib.svdq_quantize_act_lowrank_down_grouped(1, arr, one, 1, i64, i64, one, one, one, None)
-    assert st == 5
+    assert st == 1
 
 
 def test_offline_and_fused_argument_validation_before_device():

@@ -80,20 +80,25 @@ def test_k1_flux_qkv_full(fmt):
     run_k1(fmt, 4608, 3072, 64, 32, seed=4)
 
 
-@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
-def test_k1_grouped_equals_single(fmt):
-    """svdq_quantize_act_lowrank_down_grouped: every problem's codes, scales and xl1 are
-    bit-identical to its own single launch, and match the oracle bit-exactly (codes/scales)."""
+@pytest.mark.parametrize("fmt,dt,shapes", [
+    ("nvfp4", "bf16", [(300, 1152, 32), (64, 1152, 32), (129, 3072, 32)]),
+    ("int4", "bf16", [(300, 1152, 32), (64, 1152, 32), (129, 3072, 32)]),
+    ("nvfp4", "fp16", [(300, 640, 48), (64, 640, 48)]),
+    ("nvfp4", "bf16", [(4096, 1152, 32), (512, 1152, 32)]),     # row tile differs from the single launches
+])
+def test_k1_grouped_equals_single(fmt, dt, shapes):
+    """svdq_quantize_act_lowrank_down_grouped: every problem's codes and scales are bit-identical
+    to its own single launch and to the oracle; xl1 bit-identical when the row tile matches, else
+    within 1e-3 (fp32 summation order follows the launch's row tile)."""
     need_cuda()
     import torch
     import paper_2411_05007_b200 as P
     dev = torch.device("cuda")
-    shapes = [(300, 1152, 32), (64, 1152, 32), (129, 3072, 32)]
     layers, X, outs, refs = [], [], [], []
     for i, (M, K, r) in enumerate(shapes):
-        x, w, lam, ops = make_case(fmt, M, K, 128, r, seed=90 + i)
+        x, w, lam, ops = make_case(fmt, M, K, 128, r, dt=dt, seed=90 + i)
         layers.append(layer_from_ops(P, ops, dev))
-        X.append(torch.from_numpy(x).to(dev).to(torch.bfloat16))
+        X.append(torch.from_numpy(x).to(dev).to(P.TORCH_DTYPE[dt]))
         bq, bs, bl = P.svdq_act_buffer_sizes(fmt, M, K, r)
         outs.append((torch.zeros(bq, dtype=torch.uint8, device=dev), torch.zeros(bs, dtype=torch.uint8, device=dev),
                      torch.zeros(bl // 2, dtype=torch.int16, device=dev)))
@@ -104,7 +109,14 @@ def test_k1_grouped_equals_single(fmt):
     for i, (M, K, r) in enumerate(shapes):
         sq, ss, sl = P.svdq_quantize_act_lowrank_down(layers[i], X[i])
         torch.cuda.synchronize()
-        assert torch.equal(outs[i][0], sq) and torch.equal(outs[i][1], ss) and torch.equal(outs[i][2], sl)
+        assert torch.equal(outs[i][0], sq) and torch.equal(outs[i][1], ss)
+        same_tile = P.svdq_k1_row_tile(sum((m + 127) // 128 * 128 for m, _, _ in shapes), r) == \
+            P.svdq_k1_row_tile((M + 127) // 128 * 128, r)
+        if same_tile:
+            assert torch.equal(outs[i][2], sl)
+        else:
+            g = F.bf16_from_bits(outs[i][2].cpu().numpy().view(np.uint16))
+            assert rel_fro(g, F.bf16_from_bits(sl.cpu().numpy().view(np.uint16))) <= 1e-3
         ops, x = refs[i]
         qa = S.quantize_activation(x, ops)
         ref_q = F.pack_nibbles(qa.codes if fmt == "nvfp4" else F.int4_to_nibble(qa.codes))

@@ -97,7 +97,7 @@ int main() {
   cudaMemset(pool, 1, pool_bytes);
   unsigned long long *sink;
   cudaMalloc(&sink, 8);
-  cudaFuncSetAttribute(rd_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 16384);
+  cudaFuncSetAttribute(rd_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 16384);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
