@@ -10,9 +10,12 @@ TFLOPS counts 2*M*N*K per linear (the low-rank FLOPs are overhead).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl svdq|reference]
 
-N > 1 (torchrun): every rank runs the same step on its own GPU (replicas,
-weak scaling, no collective on the data path); value = all ranks' FLOPs /
-max-over-ranks time.  Prints one JSON line on rank 0.
+N > 1 (torchrun, NCCL): by default the step runs TENSOR PARALLEL over the ranks
+(BASELINE config C5; column-parallel over N, Variant 2 packed
+all-gathers where a layer's input is the previous column-parallel output;
+strong scaling, value = the step's FLOPs / max-over-ranks time); --mode
+replicas runs an independent copy of the step per GPU instead (weak scaling).
+Prints one JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -156,11 +159,14 @@ def flux_step_grouped(P, bl, st, ev1=None, ev2=None, launch_groups=None):
 
 
 # ------------------------------------------------------------------ svdq arm
-def build_layers(P, torch, layers, fmt, dev, quality=None):
+def build_layers(P, torch, layers, fmt, dev, quality=None, seed_index=None):
     """Synthetic FLUX-shaped layers (DESIGN.md input recipe), weights prepared on the GPU
-    by svdq_quantize_weights (fp64 Gram + eigensolver SVD, residual quantization)."""
+    by svdq_quantize_weights (fp64 Gram + eigensolver SVD, residual quantization).  Layer i draws
+    from synth.rng(4, i, t); `seed_index` overrides i for a one-layer list."""
     out = []
     for i, L in enumerate(layers):
+        if seed_index is not None:
+            i = seed_index
         g = torch.Generator(device="cpu").manual_seed(4000 + i)
         w = synth.gen_w(L.K, L.N, synth.rng(4, i, 1))
         xcal = torch.from_numpy(synth.gen_x(256, L.K, synth.rng(4, i, 2))).to(dev).to(torch.bfloat16)
@@ -598,6 +604,169 @@ def run_svdq(args, rank, world, local_rank):
     }
 
 
+# ------------------------------------------------------------------ tensor-parallel arm (C5)
+# Layers whose input is the output of a column-parallel predecessor (attention-out input, MLP-down
+# input after GELU, single-block linear2 input): the rank holds only its K-shard of the input and
+# the layer runs SURVEY 8(e) Variant 2 (K1 on the slice, one packed all-gather, assemble, K2 on the
+# N-shard).  The other inputs (qkv, MLP-up, linear1: from the norm of the replicated residual
+# stream; attention / norms / GELU are pre-generated inputs) are replicated, so
+# their K1 runs on every rank and K2 on the shard.  Outputs stay N-sharded.
+SHARDED_INPUT = ("proj", "mlp_down", "linear2")
+
+
+def run_tp(args, rank, world, local_rank, backend):
+    import torch
+    import torch.distributed as dist
+    import paper_2411_05007_b200 as P
+    from paper_2411_05007_b200 import tp
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    layers = flux_block_layers(args.batch)
+    net = []
+    for i, L in enumerate(layers):
+        (_, full, b), = build_layers(P, torch, [L], args.fmt, dev, seed_index=i)
+        cp = tp.ColumnParallelSVDQLinear(full, world=world, rank=rank)
+        sharded = L.name.endswith(SHARDED_INPUT)
+        n = cp.local.N
+        e = dict(L=L, cp=cp, sharded=sharded, y=torch.empty(L.M, n, dtype=torch.bfloat16, device=dev))
+        if sharded:
+            k0, kp = tp.kslice_bounds(L.K, world, rank)
+            e["x"] = b["x"][:, k0:k0 + kp].contiguous()
+            nb = P.svdq_tp_slice_sizes(args.fmt, L.M, kp, L.r)[3]
+            e["slice"] = torch.empty(nb, dtype=torch.uint8, device=dev)
+            e["k0"] = k0
+        else:
+            e["x"] = b["x"]
+        e["xq"], e["xs"], e["xl1"] = b["xq"], b["xs"], b["xl1"]
+        del full, b
+        net.append(e)
+    torch.cuda.synchronize()
+    by = {e["L"].name: e for e in net}
+    groups = [[by[f"double_{s_}_{k}"] for s_ in ("img", "txt")] for k in ("qkv", "proj", "mlp_up", "mlp_down")]
+    groups += [[by["single_linear1"]], [by["single_linear2"]]]
+    # one packed all-gather per sharded group: the img and txt slices travel together
+    gbuf = {}
+    for gi, grp in enumerate(groups):
+        if grp[0]["sharded"]:
+            tot = sum(e["slice"].numel() for e in grp)
+            gbuf[gi] = (torch.empty(tot, dtype=torch.uint8, device=dev),
+                        torch.empty(world * tot, dtype=torch.uint8, device=dev))
+    stream = torch.cuda.Stream(device=dev)
+    comm_ev = []
+
+    def step(st, record=None):
+        for gi, grp in enumerate(groups):
+            if grp[0]["sharded"]:
+                send, recv = gbuf[gi]
+                off = 0
+                for e in grp:
+                    nb = e["slice"].numel()
+                    P.svdq_quantize_act_lowrank_down_kslice(e["cp"].local, e["k0"], e["x"], send[off:off + nb], stream=st)
+                    off += nb
+                if record is not None:
+                    record[gi][0].record(st)
+                if world > 1:
+                    tp.all_gather(recv, send)
+                else:
+                    recv.copy_(send)
+                if record is not None:
+                    record[gi][1].record(st)
+                tot = send.numel()
+                off = 0
+                for e in grp:                    # rank p's slice of this layer at recv[p * tot + off]
+                    P.svdq_tp_assemble_act(args.fmt, world, e["L"].M, e["L"].K, e["L"].r, recv[off:], e["xq"], e["xs"],
+                                           e["xl1"], slice_stride=tot, stream=st)
+                    off += e["slice"].numel()
+            elif len(grp) > 1:
+                P.svdq_quantize_act_lowrank_down_grouped([e["cp"].local for e in grp], [e["x"] for e in grp],
+                                                         [e["xq"] for e in grp], [e["xs"] for e in grp],
+                                                         [e["xl1"] for e in grp], stream=st)
+            else:
+                e = grp[0]
+                P.svdq_quantize_act_lowrank_down(e["cp"].local, e["x"], e["xq"], e["xs"], e["xl1"], stream=st)
+            P.svdq_gemm_w4a4_lowrank_up_grouped([e["cp"].local for e in grp], [e["xq"] for e in grp],
+                                                [e["xs"] for e in grp], [e["xl1"] for e in grp],
+                                                [e["L"].M for e in grp], [e["y"] for e in grp], stream=st)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step(stream)
+    torch.cuda.synchronize()
+    graph, graph_err = None, None
+    if backend == "nccl" or world == 1:
+        try:                                     # NCCL collectives inside CUDA-graph capture
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                step(stream)
+            torch.cuda.synchronize()
+            with torch.cuda.stream(stream):
+                graph.replay()
+            torch.cuda.synchronize()
+        except Exception as ex:  # noqa: BLE001  (capture unsupported here: eager launches instead)
+            graph, graph_err = None, f"{type(ex).__name__}: {str(ex)[:120]}"
+            torch.cuda.synchronize()
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    step_ev = [(ev(), ev()) for _ in range(args.steps)]
+    barrier = dist.barrier if world > 1 else (lambda: None)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        with torch.cuda.stream(stream):
+            for s in range(args.steps):
+                step_ev[s][0].record(stream)
+                if graph is not None:
+                    graph.replay()
+                else:
+                    step(stream)
+                step_ev[s][1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    total_ms = float(sum(a.elapsed_time(b) for a, b in step_ev))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    # communication share: eager step with events around every all-gather
+    rec = {gi: (ev(), ev()) for gi in gbuf}
+    nrep = max(3, min(args.steps, 10))
+    comm = []
+    for _ in range(nrep):
+        barrier()
+        with torch.cuda.stream(stream):
+            a, b = ev(), ev()
+            a.record(stream)
+            step(stream, rec)
+            b.record(stream)
+        torch.cuda.synchronize()
+        comm.append((sum(x.elapsed_time(y) for x, y in rec.values()), a.elapsed_time(b)))
+    comm_ms, eager_ms = (float(np.mean([c[0] for c in comm])), float(np.mean([c[1] for c in comm])))
+    if rank != 0:
+        return None
+    flops = sum(2.0 * L.M * L.N * L.K for L in layers)
+    gathered_bytes = sum(world * gbuf[gi][0].numel() for gi in gbuf)
+    cfg = bench_config(args, world)
+    cfg["parallelism"] = f"tp{world} (column-parallel over N; SURVEY 8(e) Variant 2 packed all-gathers)"
+    cfg["block_latency_ms"] = round(total_ms / args.steps, 4)
+    return {
+        "metric": METRIC, "value": round(flops * args.steps / (total_ms / 1e3) / 1e12, 2), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "e2m1 x e2m1 -> f32 (NVFP4 g16 e4m3 scales) + bf16 low-rank" if args.fmt == "nvfp4" else args.fmt,
+        "data": "synthetic (seeded; DESIGN.md input recipe), weights prepared on GPU by svdq_quantize_weights, "
+                "column-sharded", "config": cfg,
+        "tp": {"backend": backend, "graph": graph is not None, "graph_error": graph_err,
+               "comm_ms_per_step": round(comm_ms, 4), "eager_step_ms": round(eager_ms, 4),
+               "comm_fraction_eager": round(comm_ms / eager_ms, 4) if eager_ms else None,
+               "gathered_bytes_per_rank_per_step": int(gathered_bytes),
+               "sharded_input_layers": [L.name for L in layers if L.name.endswith(SHARDED_INPUT)],
+               "note": "value = the full block-pair FLOPs (sum 2MNK over all linears) / max-over-ranks step time "
+                       "(strong scaling: the total work is fixed); comm from events around each all-gather in an "
+                       "eager replay of the step"},
+        "clocks": clk.summary(),
+    }
+
+
 # ------------------------------------------------------------------ oracle timings
 def oracle_operands(L, i, fmt):
     """Valid stored operands of the layer's shape for TIMING the oracle forward: random
@@ -712,6 +881,10 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=1024)   # ~10-30 s of oracle CPU work (weight prep is ~6 s of it)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the rank-0 overhead / library legs")
+    ap.add_argument("--mode", default="auto", choices=["auto", "tp", "replicas"],
+                    help="N > 1: tensor parallel over N (C5, default) or independent replicas")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: multi-process tests on one GPU (NCCL refuses two ranks per device)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "svdq":
         args.warmup = 3
@@ -725,11 +898,26 @@ def main():
             print(json.dumps(run_reference(args)))
         return
 
+    mode = ("tp" if world > 1 else "single") if args.mode == "auto" else args.mode
     if world > 1:
         import torch
         import torch.distributed as dist
+        if args.backend == "gloo":                 # test mode: ranks may share the box's one GPU
+            local_rank %= max(1, torch.cuda.device_count())
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
+    if mode == "tp":                           # world 1: the TP code path with P = 1 (functional check)
+        if args.fmt == "w8a8":
+            raise SystemExit("TP mode: W8A8's per-token scales need the whole row (use --mode replicas)")
+        out = run_tp(args, rank, world, local_rank, args.backend if world > 1 else "none")
+        if rank == 0:
+            print(json.dumps(out))
+        if world > 1:
+            dist.destroy_process_group()
+        return
     out = run_svdq(args, rank, world, local_rank)
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:

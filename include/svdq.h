@@ -130,6 +130,37 @@ svdq_status svdq_quantize_act_lowrank_down_grouped(int32_t n, const svdq_linear 
                                                    const int64_t *ldx, uint8_t *const *xq, uint8_t *const *xs,
                                                    uint16_t *const *xl1, void *stream);
 
+/* ---------------------------------------------------------------- tensor parallelism (C5)
+ * SURVEY 8(e) Variant 2, "quantize, then gather" (north star: column-parallel over the 8xB200
+ * box, all-gather only where the next layer needs the full activation; the paper itself is
+ * single-GPU).  A layer whose input X [M][K] is held column-sharded over P ranks (rank p
+ * holds X[:, p Kp : (p+1) Kp), Kp = K/P, e.g. its shard of the previous column-parallel layer's
+ * output) runs K1 on its slice, the ranks all-gather the packed slices (0.5625 B per element + an
+ * fp32 [M][rank] partial, instead of 2 B per element for a bf16 gather), and every rank assembles
+ * the full K1 outputs -- then K2 runs on its own N-shard.  Codes and scales equal those of K1 on
+ * the full X bit for bit (groups never straddle slices: Kp % 64 == 0); xl1 = bf16 of the fp32
+ * partials summed in rank order (deterministic, identical on every rank).  NVFP4 / INT4 only
+ * (W8A8's per-token scale needs the whole row: SVDQ_ERR_UNSUPPORTED).
+ *
+ * Slice layout (one rank's contribution, `slice_bytes`): codes [M][Kp/2] at xq_off, scales at
+ * xs_off (NVFP4: the 128x4 layout over (M, Kp); INT4: [M][Kp/64] 16-bit), fp32 partial
+ * X_p L1s[:, slice]^T [M][rank] at part_off; offsets 256-byte aligned.                        */
+svdq_status svdq_tp_slice_sizes(int32_t fmt, int64_t M, int64_t Kp, int32_t rank, size_t *xq_off, size_t *xs_off,
+                                size_t *part_off, size_t *slice_bytes);
+/* K1 of layer L (full K: lambda_inv, l1s are the replicated full operands) on input channels
+ * [k0, k0 + Kp): X [dev] [M][ldx] holds those Kp channels; writes one slice [dev] (layout above).
+ * k0, Kp multiples of 64.                                                                       */
+svdq_status svdq_quantize_act_lowrank_down_kslice(const svdq_linear *L, int64_t k0, int64_t Kp, const void *X,
+                                                  int32_t x_dtype, int64_t M, int64_t ldx, uint8_t *slice,
+                                                  void *stream);
+/* gathered [dev] = the P slices in rank order, slice p at gathered + p * slice_stride (0 = slice_bytes:
+ * back to back, as all_gather_into_tensor of one slice per rank leaves them; larger when several
+ * layers' slices travel in one gather); writes the full xq [M][K/2], xs and xl1 [M][rank] bf16
+ * exactly as K1 on the full X would lay them out (K = P Kp).                                    */
+svdq_status svdq_tp_assemble_act(int32_t fmt, int32_t P, int64_t M, int64_t K, int32_t rank, const uint8_t *gathered,
+                                 size_t slice_bytes, size_t slice_stride, uint8_t *xq, uint8_t *xs, uint16_t *xl1,
+                                 void *stream);
+
 /* K2: 4-bit GEMM with the low-rank up-projection folded into the same accumulator.
  *   NVFP4: acc[m,n] = sum_g f(sfa[m,g]) f(sfb[n,g]) sum_{k in g} e2m1(qa) e2m1(qb)
  *                     + sum_t xl1[m,t] l2s[n,t]          (tcgen05 kind::mxf4nvf4 + kind::f16)

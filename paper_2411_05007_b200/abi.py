@@ -47,6 +47,7 @@ EXPORTS = [
     "svdq_quantize_weights_gptq_workspace", "svdq_quantize_weights_gptq",
     "svdq_debug_int4_group_accum", "svdq_debug_codec", "svdq_status_string", "svdq_last_error",
     "svdq_launch_count", "svdq_version", "svdq_k1_row_tile",
+    "svdq_tp_slice_sizes", "svdq_quantize_act_lowrank_down_kslice", "svdq_tp_assemble_act",
 ]
 
 
@@ -105,6 +106,9 @@ _sig = {
                                    C.c_float, _LP, _P, C.c_size_t, _P],
     "svdq_debug_int4_group_accum": [_P, _P, _I64, _I64, _I64, _P, _P],
     "svdq_debug_codec": [_P, _P, _I64, _I32, _P],
+    "svdq_tp_slice_sizes": [_I32, _I64, _I64, _I32, _SZ, _SZ, _SZ, _SZ],
+    "svdq_quantize_act_lowrank_down_kslice": [_LP, _I64, _I64, _P, _I32, _I64, _I64, _P, _P],
+    "svdq_tp_assemble_act": [_I32, _I32, _I64, _I64, _I32, _P, C.c_size_t, C.c_size_t, _P, _P, _P, _P],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -156,6 +160,41 @@ def svdq_launch_count() -> int:
 
 def svdq_version() -> int:
     return int(_lib.svdq_version())
+
+
+def svdq_tp_slice_sizes(fmt: str, M: int, Kp: int, rank: int):
+    """(xq_off, xs_off, part_off, slice_bytes) of one rank's packed K1 slice (tensor parallel)."""
+    o = [C.c_size_t() for _ in range(4)]
+    _check(_lib.svdq_tp_slice_sizes(FMT[fmt], M, Kp, rank, *[C.byref(x) for x in o]), "svdq_tp_slice_sizes")
+    return tuple(x.value for x in o)
+
+
+def svdq_quantize_act_lowrank_down_kslice(layer: "QuantizedLinear", k0: int, X, slice_buf=None, stream=None):
+    """K1 of `layer` on its input channels [k0, k0 + X.shape[1]) (X: this rank's column shard of the
+    layer input).  Returns the packed slice buffer (uint8, svdq_tp_slice_sizes layout)."""
+    M, Kp = X.shape
+    nb = svdq_tp_slice_sizes(layer.fmt, M, Kp, layer.rank)[3]
+    if slice_buf is None:
+        slice_buf = torch.empty(nb, dtype=torch.uint8, device=X.device)
+    _check(_lib.svdq_quantize_act_lowrank_down_kslice(layer.ref, k0, Kp, _ptr(X), DTYPE[DTYPE_OF_TORCH[X.dtype]], M,
+                                                      X.stride(0), _ptr(slice_buf), _stream(stream)),
+           "svdq_quantize_act_lowrank_down_kslice")
+    return slice_buf
+
+
+def svdq_tp_assemble_act(fmt: str, P: int, M: int, K: int, rank: int, gathered, xq=None, xs=None, xl1=None,
+                         slice_stride: int = 0, stream=None):
+    """Full K1 outputs (xq, xs, xl1) from the P gathered slices: slice p at byte p * slice_stride of
+    `gathered` (0: back to back, the all_gather_into_tensor output of one slice per rank)."""
+    bq, bs, bl = svdq_act_buffer_sizes(fmt, M, K, rank)
+    dev = gathered.device
+    xq = torch.empty(bq, dtype=torch.uint8, device=dev) if xq is None else xq
+    xs = torch.empty(bs, dtype=torch.uint8, device=dev) if xs is None else xs
+    xl1 = torch.empty(max(bl // 2, 8), dtype=torch.int16, device=dev) if xl1 is None else xl1
+    nb = svdq_tp_slice_sizes(fmt, M, K // P, rank)[3]
+    _check(_lib.svdq_tp_assemble_act(FMT[fmt], P, M, K, rank, _ptr(gathered), nb, slice_stride, _ptr(xq), _ptr(xs),
+                                     _ptr(xl1), _stream(stream)), "svdq_tp_assemble_act")
+    return xq, xs, xl1
 
 
 def svdq_k1_row_tile(rows_padded: int, rank: int) -> int:

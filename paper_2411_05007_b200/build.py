@@ -20,7 +20,7 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr"]
-SOURCES = ["k1_rows.cu", "k1_int8.cu", "k2_gemm_nvfp4.cu", "k2_gemm_nvfp4_2sm.cu", "k2_gemm_int4.cu", "wprep.cu", "offline.cu", "gptq.cu", "api.cu"]
+SOURCES = ["k1_rows.cu", "tp.cu", "k1_int8.cu", "k2_gemm_nvfp4.cu", "k2_gemm_nvfp4_2sm.cu", "k2_gemm_int4.cu", "wprep.cu", "offline.cu", "gptq.cu", "api.cu"]
 
 
 def _needs(obj: str, deps) -> bool:

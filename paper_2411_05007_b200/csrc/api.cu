@@ -238,7 +238,8 @@ svdq_status svdq_weight_buffer_sizes(int32_t fmt, int64_t K, int64_t N, int32_t 
 namespace {
 // Validation, launch parameters and tensor maps of one K1 problem (`out` may alias maps->p).
 svdq_status prepare_k1(const svdq_linear *L, const void *X, int32_t x_dtype, int64_t M, int64_t ldx, uint8_t *xq,
-                       uint8_t *xs, uint16_t *xl1, K1Params *out, K1Problem *maps, int rt) {
+                       uint8_t *xs, uint16_t *xl1, K1Params *out, K1Problem *maps, int rt,
+                       int64_t l1s_pitch = 0) {
   svdq_status st = check_linear(L, false);
   if (st != SVDQ_OK) return st;
   if (!X || !xq || !xs || (L->rank > 0 && !xl1)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null buffer");
@@ -276,8 +277,8 @@ svdq_status prepare_k1(const svdq_linear *L, const void *X, int32_t x_dtype, int
                         L->K, M, ldx * 2, q, static_cast<uint32_t>(rt))) != SVDQ_OK)
     return st;
   if (L->rank > 0 &&
-      (st = make_map(&maps->l1s, L->l1s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->K, L->rank, L->K * 2, 64,
-                     static_cast<uint32_t>(L->rank))) != SVDQ_OK)
+      (st = make_map(&maps->l1s, L->l1s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->K, L->rank,
+                     (l1s_pitch > 0 ? l1s_pitch : L->K) * 2, 64, static_cast<uint32_t>(L->rank))) != SVDQ_OK)
     return st;
   if ((st = make_map(&maps->lam, L->lambda_inv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 32, L->K / 32, 128, 32, 2 * q)) !=
       SVDQ_OK)
@@ -336,6 +337,75 @@ svdq_status svdq_quantize_act_lowrank_down_grouped(int32_t n, const svdq_linear 
   }
   cudaError_t e = launch_k1_rows_group(g, rt, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "grouped K1 launch");
+  ++g_launches;
+  return SVDQ_OK;
+}
+
+svdq_status svdq_tp_slice_sizes(int32_t fmt, int64_t M, int64_t Kp, int32_t rank, size_t *xq_off, size_t *xs_off,
+                                size_t *part_off, size_t *slice_bytes) {
+  if (!xq_off || !xs_off || !part_off || !slice_bytes) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null output");
+  if (fmt != SVDQ_FMT_NVFP4 && fmt != SVDQ_FMT_INT4)
+    return fail(fmt == SVDQ_FMT_W8A8 ? SVDQ_ERR_UNSUPPORTED : SVDQ_ERR_INVALID_ARGUMENT,
+                "K-sliced K1 needs NVFP4 or INT4 (W8A8 per-token scales need the whole row)");
+  if (M < 1) return fail(SVDQ_ERR_SHAPE, "M must be >= 1");
+  if (Kp <= 0 || Kp % 64) return fail(SVDQ_ERR_SHAPE, "slice width must be a positive multiple of 64");
+  if (rank < 0 || rank > 128 || rank % 16) return fail(SVDQ_ERR_RANK, "bad rank");
+  const TpSliceLayout L = tp_slice_layout(fmt, M, Kp, rank);
+  *xq_off = static_cast<size_t>(L.xq_off);
+  *xs_off = static_cast<size_t>(L.xs_off);
+  *part_off = static_cast<size_t>(L.part_off);
+  *slice_bytes = static_cast<size_t>(L.bytes);
+  return SVDQ_OK;
+}
+
+svdq_status svdq_quantize_act_lowrank_down_kslice(const svdq_linear *L, int64_t k0, int64_t Kp, const void *X,
+                                                  int32_t x_dtype, int64_t M, int64_t ldx, uint8_t *slice,
+                                                  void *stream) {
+  svdq_status st = check_linear(L, false);
+  if (st != SVDQ_OK) return st;
+  size_t oq, os, op, nb;
+  if ((st = svdq_tp_slice_sizes(L->fmt, M, Kp, L->rank, &oq, &os, &op, &nb)) != SVDQ_OK) return st;
+  if (k0 < 0 || k0 % 64 || k0 + Kp > L->K) return fail(SVDQ_ERR_SHAPE, "K-slice [%lld, %lld) outside [0, K)",
+                                                       (long long)k0, (long long)(k0 + Kp));
+  if (!slice) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null slice buffer");
+  if (!aligned16(slice)) return fail(SVDQ_ERR_ALIGNMENT, "slice buffer must be 16-byte aligned");
+  svdq_linear V = *L;                        // the layer restricted to input channels [k0, k0 + Kp)
+  V.K = Kp;
+  V.lambda_inv = L->lambda_inv + k0;
+  V.l1s = L->rank ? L->l1s + k0 : L->l1s;
+  K1Args g;
+  std::memset(&g, 0, sizeof(g));
+  g.n = 1;
+  const int rt = k1_rows_rt(((M + 127) / 128) * 128, L->rank);
+  float *part = reinterpret_cast<float *>(slice + op);
+  st = prepare_k1(&V, X, x_dtype, M, ldx, slice + oq, slice + os, reinterpret_cast<uint16_t *>(part), &g.pr[0].p,
+                  &g.pr[0], rt, L->K);
+  if (st != SVDQ_OK) return st;
+  g.pr[0].p.xl1 = nullptr;
+  g.pr[0].p.xl1_f32 = L->rank ? part : nullptr;
+  cudaError_t e = launch_k1_rows_group(g, rt, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "K-sliced K1 launch");
+  ++g_launches;
+  return SVDQ_OK;
+}
+
+svdq_status svdq_tp_assemble_act(int32_t fmt, int32_t P, int64_t M, int64_t K, int32_t rank, const uint8_t *gathered,
+                                 size_t slice_bytes, size_t slice_stride, uint8_t *xq, uint8_t *xs, uint16_t *xl1,
+                                 void *stream) {
+  if (P < 1) return fail(SVDQ_ERR_INVALID_ARGUMENT, "P must be >= 1");
+  if (K <= 0 || K % (64 * static_cast<int64_t>(P))) return fail(SVDQ_ERR_SHAPE, "K must be a multiple of 64 P");
+  size_t oq, os, op, nb;
+  svdq_status st = svdq_tp_slice_sizes(fmt, M, K / P, rank, &oq, &os, &op, &nb);
+  if (st != SVDQ_OK) return st;
+  if (slice_bytes != nb) return fail(SVDQ_ERR_SHAPE, "slice_bytes %zu != %zu", slice_bytes, nb);
+  if (slice_stride == 0) slice_stride = slice_bytes;
+  if (slice_stride < slice_bytes || slice_stride % 16) return fail(SVDQ_ERR_SHAPE, "bad slice_stride %zu", slice_stride);
+  if (!gathered || !xq || !xs || (rank && !xl1)) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null buffer");
+  if (!aligned16(gathered) || !aligned16(xq) || !aligned16(xs)) return fail(SVDQ_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
+  if ((st = check_device()) != SVDQ_OK) return st;
+  cudaError_t e = launch_tp_assemble(fmt, P, M, K, rank, gathered, static_cast<int64_t>(slice_stride), xq, xs, xl1,
+                                     static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "TP assemble launch");
   ++g_launches;
   return SVDQ_OK;
 }

@@ -57,6 +57,7 @@ struct K1Params {
   uint8_t *xq;
   uint8_t *xs;
   uint16_t *xl1;
+  float *xl1_f32;     // tensor-parallel K-slice: fp32 partial X L1s^T [M][rank] instead of bf16 xl1
 };
 cudaError_t launch_k1_int8_rows(const K1Params &p, cudaStream_t s);   // W8A8 per-token INT8 codes
 // Grouped K1: up to kMaxGroup1 problems (same fmt, scale dtype and rank) in one launch; the
@@ -150,6 +151,14 @@ cudaError_t launch_k2_next_reduce(const K2PairArgs &g, int i, uint16_t *xl1_next
 constexpr int kNvfp4PairBN = 192;
 constexpr int kInt4BN = 128;             // N tile of the INT4 GEMM
 cudaError_t launch_k2_int4(const K2Maps &maps, const K2Params &p, cudaStream_t s);
+
+// tensor-parallel assembly (tp.cu, SURVEY 8(e) Variant 2): P gathered K-slices -> full K1 outputs
+struct TpSliceLayout {
+  int64_t xq_off, xs_off, part_off, bytes;   // byte offsets inside one rank's slice
+};
+TpSliceLayout tp_slice_layout(int fmt, int64_t M, int64_t Kp, int rank);
+cudaError_t launch_tp_assemble(int fmt, int P, int64_t M, int64_t K, int rank, const uint8_t *gathered,
+                               int64_t slice_stride, uint8_t *xq, uint8_t *xs, uint16_t *xl1, cudaStream_t s);
 
 // weight-side kernels (wprep.cu)
 cudaError_t launch_absmax(const float *R, int64_t n, unsigned int *out_bits, cudaStream_t s);

@@ -433,7 +433,10 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
       s1 += v.y;
     }
     const int64_t row = row0 + mm;
-    if (row < p.M) *reinterpret_cast<uint32_t *>(p.xl1 + row * r + col) = pack_bf16x2(s0, s1);
+    if (row < p.M) {
+      if (p.xl1_f32) *reinterpret_cast<float2 *>(p.xl1_f32 + row * r + col) = make_float2(s0, s1);
+      else *reinterpret_cast<uint32_t *>(p.xl1 + row * r + col) = pack_bf16x2(s0, s1);
+    }
   }
   if (threadIdx.x == 64) RTRACE(101);
 }

@@ -1,6 +1,7 @@
 """Tensor parallelism for the SVDQuant linear (BASELINE.json north_star:
 "tensor-parallel over the 8xB200 box, sharding weights and L2 along output channels, with
-an NCCL all-gather over NVLink only where the next layer needs the full activation").
+an NCCL all-gather over NVLink only where the next layer needs the full activation").  The
+paper itself is single-GPU; this is the north star's extension.
 
 Column-parallel over the output channels N: every column of
     Y = alpha (Q(X_hat) Q(R) + xl1 L2s^T) + bias
@@ -9,19 +10,27 @@ full X.  So rank p of P holds
     sharded   : residual codes [N/P, K/2], their scales, l2s [N/P, r], bias [N/P]
     replicated: lambda_inv [K], l1s [r, K], gs_x, and gs_w (computed over the FULL residual
                 before sharding, so every shard reproduces the unsharded output bit for bit)
-K1 runs on the replicated X (its outputs are identical on every rank), K2 on the shard, and
-`all_gather_into_tensor` (NCCL over NVLink / NVSwitch; gloo in the CPU tests) assembles Y
-where the consumer needs the full feature dimension.
 
-Only plumbing lives here: slicing device buffers and calling torch.distributed.  All
-arithmetic runs in libsvdq's kernels.
+Two ways to feed a layer whose input is needed in full:
+  Variant 1 (`forward`): X replicated on every rank, K1 runs redundantly, K2 on the N-shard;
+      `all_gather_into_tensor` of the bf16 Y shards where a consumer needs the full output.
+  Variant 2 (`forward_from_shard`, SURVEY 8(e) "quantize, then gather"): rank p holds only
+      X[:, p Kp:(p+1) Kp] (its shard of the previous column-parallel layer's output); it runs K1 on
+      that K-slice (svdq_quantize_act_lowrank_down_kslice), ONE all-gather moves the packed slices
+      (codes + scale factors + an fp32 [M, r] partial X L1s^T: 0.5625 B per element instead of 2),
+      svdq_tp_assemble_act rebuilds the full K1 outputs (partials summed in rank order), and K2 runs
+      on the N-shard.  K1's work is split P ways instead of replicated.
+
+Only plumbing lives here: slicing device buffers, caching them, and calling torch.distributed.
+All arithmetic runs in libsvdq's kernels.
 """
 from __future__ import annotations
 
 import torch
 import torch.distributed as dist
 
-from .abi import QuantizedLinear, svdq_linear_forward
+from .abi import (QuantizedLinear, svdq_act_buffer_sizes, svdq_gemm_w4a4_lowrank_up, svdq_linear_forward,
+                  svdq_quantize_act_lowrank_down_kslice, svdq_tp_assemble_act, svdq_tp_slice_sizes)
 
 
 def _sf_atom_bytes(K: int) -> int:
@@ -39,6 +48,15 @@ def shard_bounds(N: int, world: int, rank: int):
     return rank * n, n
 
 
+def kslice_bounds(K: int, world: int, rank: int):
+    """Rank's input-channel slice for Variant 2: Kp = K/P must be a multiple of 64 so no
+    quantization group (NVFP4 16, INT4 64) straddles two ranks."""
+    if K % world or (K // world) % 64:
+        raise ValueError(f"K={K} does not split into {world} slices of a multiple of 64")
+    kp = K // world
+    return rank * kp, kp
+
+
 def shard_scales(scales: torch.Tensor, fmt: str, K: int, N: int, n0: int, n: int, scale_dtype: str):
     """Slice the weight scales of output channels [n0, n0+n).
 
@@ -51,7 +69,7 @@ def shard_scales(scales: torch.Tensor, fmt: str, K: int, N: int, n0: int, n: int
     if fmt == "int4":
         g = K // 64
         return scales.view(torch.uint8)[n0 * g * 2:(n0 + n) * g * 2].clone()
-    if fmt == "w8a8":                                   # one fp32 scale per output channel
+    if fmt == "w8a8":
         return scales.view(torch.uint8)[n0 * 4:(n0 + n) * 4].clone()
     if fmt != "nvfp4":
         raise ValueError(f"unsupported format {fmt!r}")
@@ -99,22 +117,81 @@ def assemble_columns(blocks: torch.Tensor, world: int) -> torch.Tensor:
     return blocks.view(world, m, n).permute(1, 0, 2).reshape(m, world * n)
 
 
+def all_gather(out: torch.Tensor, inp: torch.Tensor, group=None):
+    """all_gather_into_tensor; NCCL takes device tensors directly, a gloo group (the CPU / one-GPU
+    multi-process tests) is fed through host copies."""
+    if inp.is_cuda and dist.get_backend(group) == "gloo":
+        tmp = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_gather_into_tensor(tmp, inp.cpu(), group=group)
+        out.copy_(tmp)
+        return out
+    dist.all_gather_into_tensor(out, inp, group=group)
+    return out
+
+
 class ColumnParallelSVDQLinear:
-    """Column-parallel layer: K1 + K2 on the local shard, optional all-gather of Y."""
+    """Column-parallel layer.  `world` / `rank` default to the process group's; passing them
+    explicitly (no process group) gives the single-GPU shard emulation the tests use."""
 
-    def __init__(self, full: QuantizedLinear, group=None):
+    def __init__(self, full: QuantizedLinear, group=None, world: int | None = None, rank: int | None = None):
         self.group = group
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.N = full.N
+        live = dist.is_available() and dist.is_initialized()
+        self.world = world if world is not None else (dist.get_world_size(group) if live else 1)
+        self.rank = rank if rank is not None else (dist.get_rank(group) if live else 0)
+        self.N, self.K, self.fmt, self.r = full.N, full.K, full.fmt, full.rank
         self.local = shard_layer(full, self.world, self.rank)
+        self._bufs = {}
 
+    # ------------------------------------------------------------------ Variant 1
     def forward(self, X: torch.Tensor, gather: bool = True, out_dtype=None):
+        """Replicated X -> this rank's Y shard (gather=False) or the full Y (bf16 all-gather)."""
         y = svdq_linear_forward(self.local, X, out_dtype=out_dtype)
         if not gather or self.world == 1:
             return y
-        blocks = torch.empty((self.world * y.shape[0], y.shape[1]), dtype=y.dtype, device=y.device)
-        dist.all_gather_into_tensor(blocks, y.contiguous(), group=self.group)
+        blocks = self._buf(("yblocks", y.shape[0], y.dtype), (self.world * y.shape[0], y.shape[1]), y.dtype, y.device)
+        all_gather(blocks, y.contiguous(), self.group)
         return assemble_columns(blocks, self.world)
 
     __call__ = forward
+
+    # ------------------------------------------------------------------ Variant 2
+    def quantize_slice(self, x_shard: torch.Tensor, stream=None) -> torch.Tensor:
+        """K1 on this rank's input channels: the packed slice this rank contributes."""
+        M = x_shard.shape[0]
+        k0, kp = kslice_bounds(self.K, self.world, self.rank)
+        if x_shard.shape[1] != kp:
+            raise ValueError(f"rank {self.rank} expects a [M, {kp}] input shard, got {tuple(x_shard.shape)}")
+        nb = svdq_tp_slice_sizes(self.fmt, M, kp, self.r)[3]
+        buf = self._buf(("slice", M), (nb,), torch.uint8, x_shard.device)
+        return svdq_quantize_act_lowrank_down_kslice(self.local, k0, x_shard, buf, stream=stream)
+
+    def assemble(self, gathered: torch.Tensor, M: int, stream=None):
+        """Full K1 outputs (xq, xs, xl1) from the P gathered slices."""
+        bq, bs, bl = svdq_act_buffer_sizes(self.fmt, M, self.K, self.r)
+        dev = gathered.device
+        xq = self._buf(("xq", M), (bq,), torch.uint8, dev)
+        xs = self._buf(("xs", M), (bs,), torch.uint8, dev)
+        xl1 = self._buf(("xl1", M), (max(bl // 2, 8),), torch.int16, dev)
+        return svdq_tp_assemble_act(self.fmt, self.world, M, self.K, self.r, gathered, xq, xs, xl1, stream=stream)
+
+    def gather_slices(self, local_slice: torch.Tensor) -> torch.Tensor:
+        nb = int(local_slice.numel())
+        out = self._buf(("gathered", nb), (self.world * nb,), torch.uint8, local_slice.device)
+        if self.world == 1:
+            out.copy_(local_slice)
+            return out
+        return all_gather(out, local_slice, self.group)
+
+    def forward_from_shard(self, x_shard: torch.Tensor, Y: torch.Tensor | None = None, stream=None):
+        """Column-sharded input -> this rank's Y shard [M, N/P] (Variant 2)."""
+        M = x_shard.shape[0]
+        gathered = self.gather_slices(self.quantize_slice(x_shard, stream=stream))
+        xq, xs, xl1 = self.assemble(gathered, M, stream=stream)
+        return svdq_gemm_w4a4_lowrank_up(self.local, xq, xs, xl1 if self.r else None, M, Y=Y, stream=stream)
+
+    def _buf(self, key, shape, dtype, device):
+        t = self._bufs.get(key)
+        if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype or t.device != device:
+            t = torch.empty(shape, dtype=dtype, device=device)
+            self._bufs[key] = t
+        return t

@@ -30,3 +30,64 @@ def test_sharded_equals_unsharded(fmt, P_, N):
     y_cat = torch.cat(parts, dim=1)
     torch.cuda.synchronize()
     assert torch.equal(y_cat.view(torch.int16), y_full.view(torch.int16))
+
+
+# ---------------------------------------------------------------------------------------------
+# Variant 2 (SURVEY 8(e) "quantize, then gather"), single-GPU emulation of P ranks: each rank's
+# K1 runs on its K-slice of the input, the packed slices are concatenated (what
+# all_gather_into_tensor leaves on every rank), every rank assembles the full K1 outputs and runs
+# K2 on its N-shard.  Codes / scales equal the unsharded K1's bit for bit; xl1 (partials summed in
+# rank order) within the K1 tolerance; every rank assembles identical bytes; Y vs the oracle.
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+@pytest.mark.parametrize("P_,M,K,N,r", [(2, 384, 1024, 1536, 32), (4, 300, 3072, 1024, 32), (8, 129, 3072, 512, 16),
+                                        (3, 200, 576, 480, 0), (8, 256, 12288, 384, 32)])
+def test_variant2_emulated(fmt, P_, M, K, N, r):
+    need_cuda()
+    import torch
+    import paper_2411_05007_b200 as P
+    from paper_2411_05007_b200 import tp
+    from helpers import pack_act, rel_fro
+    from oracle import formats as F
+    from oracle import svdquant as S
+    x, w, lam, ops = make_case(fmt, M, K, N, r, seed=P_ + K, cfg=24)
+    dev = torch.device("cuda")
+    full = layer_from_ops(P, ops, dev)
+    X = torch.from_numpy(x).to(dev).to(torch.bfloat16)
+    ranks = [tp.ColumnParallelSVDQLinear(full, world=P_, rank=p) for p in range(P_)]
+    kp = K // P_
+    slices = [ranks[p].quantize_slice(X[:, p * kp:(p + 1) * kp].contiguous()).clone() for p in range(P_)]
+    gathered = torch.cat(slices)
+    outs, ys = [], []
+    for p in range(P_):
+        xq, xs, xl1 = ranks[p].assemble(gathered, M)
+        outs.append((xq.clone(), xs.clone(), xl1.clone()))
+        ys.append(P.svdq_gemm_w4a4_lowrank_up(ranks[p].local, xq, xs, xl1 if r else None, M))
+    torch.cuda.synchronize()
+    for o in outs[1:]:                          # (xl1 is not written at rank 0)
+        assert all(torch.equal(a, b) for a, b in zip(o[:3 if r else 2], outs[0])), "ranks assembled different bytes"
+    sq, ss, sl = P.svdq_quantize_act_lowrank_down(full, X)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], sq), "codes differ from the unsharded K1"
+    assert torch.equal(outs[0][1], ss), "scales differ from the unsharded K1"
+    qa = S.quantize_activation(x, ops)
+    ref_q, ref_s = pack_act(fmt, qa, K)
+    np.testing.assert_array_equal(outs[0][0].cpu().numpy().reshape(M, K // 2), ref_q)
+    if r:
+        g = F.bf16_from_bits(outs[0][2][: M * r].cpu().numpy().view(np.uint16).reshape(M, r))
+        assert rel_fro(g, F.bf16_from_bits(qa.xl1_bits)) <= 1e-3
+    y = torch.cat(ys, dim=1).float().cpu().numpy()
+    y_ref = S.round_output(S.gemm_reference(qa, ops), "bf16")
+    assert rel_fro(y, y_ref) <= 1e-3
+
+
+def test_variant2_rejects_w8a8_and_bad_slices():
+    need_cuda()
+    import torch
+    import paper_2411_05007_b200 as P
+    from paper_2411_05007_b200 import tp
+    with pytest.raises(ValueError):
+        tp.kslice_bounds(3072, 5, 0)
+    with pytest.raises(P.SvdqError) as e:
+        P.svdq_tp_slice_sizes("w8a8", 64, 384, 16)
+    assert e.value.status == 5

@@ -113,3 +113,78 @@ def test_assemble_columns():
     out = tp.assemble_columns(a, 2)
     assert out.shape == (3, 8)
     assert out[1].tolist() == [4, 5, 6, 7, 16, 17, 18, 19]
+
+
+# ---------------------------------------------------------------------------------------------
+# Variant 2 slice contract (world_size 2, gloo, CPU): each rank packs ITS K-slice's K1 outputs --
+# computed here by the ORACLE standing in for svdq_quantize_act_lowrank_down_kslice -- at the
+# offsets svdq_tp_slice_sizes reports; one all_gather_into_tensor; rank 0 re-assembles with the
+# layout rules svdq_tp_assemble_act implements (codes concatenated along K, NVFP4 scale-factor
+# 512-B chunks interleaved per row tile, INT4 scales concatenated per row, fp32 partials summed in
+# rank order) and must reproduce the oracle's K1 of the FULL input: codes / scales bit for bit
+# (groups never straddle slices), xl1 within the K1 tolerance.
+# ---------------------------------------------------------------------------------------------
+def _v2_worker(rank, world, port, fmt, q):
+    import dataclasses
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2411_05007_b200 as P
+        from paper_2411_05007_b200 import tp
+        M, K, N, r = 200, 512, 128, 32
+        x, w, lam, ops = make_case(fmt, M, K, N, r, seed=7, cfg=22)
+        k0, kp = tp.kslice_bounds(K, world, rank)
+        sl = dataclasses.replace(ops, K=kp, lam_inv32=ops.lam_inv32[k0:k0 + kp].copy(),
+                                 L1s_bits=np.ascontiguousarray(ops.L1s_bits[:, k0:k0 + kp]))
+        qa = S.quantize_activation(x[:, k0:k0 + kp], sl)
+        oq, os_, op, nb = P.svdq_tp_slice_sizes(fmt, M, kp, r)
+        buf = np.zeros(nb, np.uint8)
+        if fmt == "nvfp4":
+            codes, scales = F.pack_nibbles(qa.codes), F.sf_to_layout(qa.scales, kp)
+        else:
+            codes = F.pack_nibbles(F.int4_to_nibble(qa.codes))
+            scales = np.ascontiguousarray(qa.scales).view(np.uint8)
+        buf[oq:oq + codes.size] = codes.reshape(-1)
+        buf[os_:os_ + scales.size] = scales.reshape(-1)
+        part = qa.xl1_exact.astype(np.float32)
+        buf[op:op + part.nbytes] = part.view(np.uint8).reshape(-1)
+        gathered = torch.empty(world * nb, dtype=torch.uint8)
+        dist.all_gather_into_tensor(gathered, torch.from_numpy(buf))
+        if rank == 0:
+            g = gathered.numpy().reshape(world, nb)
+            cs = [F.unpack_nibbles(g[p, oq:oq + M * kp // 2].reshape(M, kp // 2)) for p in range(world)]
+            if fmt == "nvfp4":
+                ss = [F.sf_from_layout(g[p, os_:os_ + F.sf_swizzled_size(M, kp)], M, kp) for p in range(world)]
+            else:
+                cs = [F.nibble_to_int4(c) for c in cs]
+                ss = [g[p, os_:os_ + M * (kp // 64) * 2].view(np.uint16).reshape(M, kp // 64) for p in range(world)]
+            acc = np.zeros((M, r), np.float32)
+            for p in range(world):                               # rank order
+                acc = acc + g[p, op:op + M * r * 4].view(np.float32).reshape(M, r)
+            q.put(("ok", (np.concatenate(cs, 1), np.concatenate(ss, 1), F.bf16_round(acc)),
+                   S.quantize_activation(x, ops)))
+    except Exception as e:  # pragma: no cover - surfaced through the queue
+        q.put(("err", repr(e), None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+def test_variant2_slice_contract_gloo(fmt):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world, port = 2, _free_port()
+    procs = [ctx.Process(target=_v2_worker, args=(r, world, port, fmt, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    status, got, ref = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+    assert status == "ok", got
+    codes, scales, xl1 = got
+    np.testing.assert_array_equal(codes, ref.codes)
+    np.testing.assert_array_equal(scales, ref.scales)
+    d = np.linalg.norm(xl1.astype(np.float64) - F.bf16_from_bits(ref.xl1_bits))
+    assert d / np.linalg.norm(F.bf16_from_bits(ref.xl1_bits)) <= 1e-3

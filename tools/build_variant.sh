@@ -7,7 +7,7 @@ name=$1; shift
 out=_build_exp/$name; mkdir -p $out
 C=paper_2411_05007_b200/csrc
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 --expt-relaxed-constexpr $*"
-for s in k1_rows k1_int8 k2_gemm_nvfp4 k2_gemm_nvfp4_2sm k2_gemm_int4 wprep offline gptq api; do
+for s in k1_rows tp k1_int8 k2_gemm_nvfp4 k2_gemm_nvfp4_2sm k2_gemm_int4 wprep offline gptq api; do
   nvcc $F -c $C/$s.cu -o $out/$s.o &
 done
 wait
