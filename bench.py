@@ -645,24 +645,44 @@ def run_tp(args, rank, world, local_rank, backend):
     by = {e["L"].name: e for e in net}
     groups = [[by[f"double_{s_}_{k}"] for s_ in ("img", "txt")] for k in ("qkv", "proj", "mlp_up", "mlp_down")]
     groups += [[by["single_linear1"]], [by["single_linear2"]]]
-    # one packed all-gather per sharded group: the img and txt slices travel together
-    gbuf = {}
+    # one packed all-gather per sharded group: the img and txt slices travel together.  --tp-gather
+    # fused: no collective -- K1 stores each slice into every rank's symmetric-memory buffer
+    # (SURVEY 8(f) row 2), then one device-side barrier (CUDA IPC + host barrier for gloo tests)
+    gbuf, sgs = {}, {}
+    fused = args.tp_gather == "fused" and world > 1
     for gi, grp in enumerate(groups):
         if grp[0]["sharded"]:
-            tot = sum(e["slice"].numel() for e in grp)
-            gbuf[gi] = (torch.empty(tot, dtype=torch.uint8, device=dev),
-                        torch.empty(world * tot, dtype=torch.uint8, device=dev))
+            if fused:
+                specs = [(args.fmt, e["L"].M, e["L"].K, e["L"].r) for e in grp]
+                sgs[gi] = (tp.IpcGather if backend == "gloo" else tp.SymmetricGather)(specs, dev)
+                gbuf[gi] = (None, sgs[gi].buf)
+            else:
+                tot = sum(e["slice"].numel() for e in grp)
+                gbuf[gi] = (torch.empty(tot, dtype=torch.uint8, device=dev),
+                            torch.empty(world * tot, dtype=torch.uint8, device=dev))
     stream = torch.cuda.Stream(device=dev)
     comm_ev = []
 
     def step(st, record=None):
         for gi, grp in enumerate(groups):
-            if grp[0]["sharded"]:
+            if grp[0]["sharded"] and fused:
+                if record is not None:
+                    record[gi][0].record(st)
+                for j, e in enumerate(grp):         # K1 stores straight into every rank's buffer
+                    sgs[gi].fill(j, e["cp"].local, e["k0"], e["x"], stream=st)
+                sgs[gi].sync()
+                if record is not None:
+                    record[gi][1].record(st)
+                for j, e in enumerate(grp):
+                    e["xq"], e["xs"], e["xl1"] = sgs[gi].outputs(j, stream=st)
+            elif grp[0]["sharded"]:
                 send, recv = gbuf[gi]
+                tot = recv.numel() // world
                 off = 0
                 for e in grp:
                     nb = e["slice"].numel()
-                    P.svdq_quantize_act_lowrank_down_kslice(e["cp"].local, e["k0"], e["x"], send[off:off + nb], stream=st)
+                    P.svdq_quantize_act_lowrank_down_kslice(e["cp"].local, e["k0"], e["x"], send[off:off + nb],
+                                                            stream=st)
                     off += nb
                 if record is not None:
                     record[gi][0].record(st)
@@ -672,7 +692,6 @@ def run_tp(args, rank, world, local_rank, backend):
                     recv.copy_(send)
                 if record is not None:
                     record[gi][1].record(st)
-                tot = send.numel()
                 off = 0
                 for e in grp:                    # rank p's slice of this layer at recv[p * tot + off]
                     P.svdq_tp_assemble_act(args.fmt, world, e["L"].M, e["L"].K, e["L"].r, recv[off:], e["xq"], e["xs"],
@@ -744,7 +763,7 @@ def run_tp(args, rank, world, local_rank, backend):
     if rank != 0:
         return None
     flops = sum(2.0 * L.M * L.N * L.K for L in layers)
-    gathered_bytes = sum(world * gbuf[gi][0].numel() for gi in gbuf)
+    gathered_bytes = sum(gbuf[gi][1].numel() for gi in gbuf)
     cfg = bench_config(args, world)
     cfg["parallelism"] = f"tp{world} (column-parallel over N; SURVEY 8(e) Variant 2 packed all-gathers)"
     cfg["block_latency_ms"] = round(total_ms / args.steps, 4)
@@ -755,8 +774,11 @@ def run_tp(args, rank, world, local_rank, backend):
         "dtype": "e2m1 x e2m1 -> f32 (NVFP4 g16 e4m3 scales) + bf16 low-rank" if args.fmt == "nvfp4" else args.fmt,
         "data": "synthetic (seeded; DESIGN.md input recipe), weights prepared on GPU by svdq_quantize_weights, "
                 "column-sharded", "config": cfg,
-        "tp": {"backend": backend, "graph": graph is not None, "graph_error": graph_err,
+        "tp": {"backend": backend, "gather": "fused K1 peer stores (symmetric memory)" if fused else "all_gather_into_tensor",
+               "graph": graph is not None, "graph_error": graph_err,
                "comm_ms_per_step": round(comm_ms, 4), "eager_step_ms": round(eager_ms, 4),
+               "comm_def": "fused: the K1 launches that store into every rank's buffer + the barrier; else the "
+                           "all-gathers",
                "comm_fraction_eager": round(comm_ms / eager_ms, 4) if eager_ms else None,
                "gathered_bytes_per_rank_per_step": int(gathered_bytes),
                "sharded_input_layers": [L.name for L in layers if L.name.endswith(SHARDED_INPUT)],
@@ -883,6 +905,9 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip the rank-0 overhead / library legs")
     ap.add_argument("--mode", default="auto", choices=["auto", "tp", "replicas"],
                     help="N > 1: tensor parallel over N (C5, default) or independent replicas")
+    ap.add_argument("--tp-gather", default="nccl", choices=["nccl", "fused"],
+                    help="TP packed-slice gather: one all_gather_into_tensor, or K1 storing into every rank's "
+                         "symmetric-memory buffer (SURVEY 8(f) row 2)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: multi-process tests on one GPU (NCCL refuses two ranks per device)")
     args = ap.parse_args()

@@ -153,6 +153,25 @@ svdq_status svdq_tp_slice_sizes(int32_t fmt, int64_t M, int64_t Kp, int32_t rank
 svdq_status svdq_quantize_act_lowrank_down_kslice(const svdq_linear *L, int64_t k0, int64_t Kp, const void *X,
                                                   int32_t x_dtype, int64_t M, int64_t ldx, uint8_t *slice,
                                                   void *stream);
+/* Fused packed all-gather: no collective.  Every rank owns a GATHER buffer
+ * (svdq_tp_gather_sizes: the full K1 outputs xq [M][K/2] at xq_off and xs at xs_off, laid out exactly
+ * like svdq_quantize_act_lowrank_down's, then P fp32 partial slots [P][M][rank] at part_off).
+ * svdq_quantize_act_lowrank_down_kslice_fused runs K1 on input channels [k0, k0 + Kp) and stores
+ * its codes / scales at their place in the full-K layout and its partial in slot p of EVERY buffer
+ * bufs[0..nbuf) (16-byte aligned device addresses: with symmetric memory, the ranks' buffers mapped
+ * over NVLink), so the gather happens inside K1.  After a cross-rank barrier (system-scope
+ * release/acquire; the caller's) svdq_tp_reduce_partials sums the P slots in rank order into the
+ * bf16 xl1 and K2 reads xq / xs from the gather buffer: codes / scales bit-identical to K1 on the
+ * full X, xl1 identical to the all-gather path's.                                                 */
+svdq_status svdq_tp_gather_sizes(int32_t fmt, int64_t M, int64_t K, int32_t rank, int32_t P, size_t *xq_off,
+                                 size_t *xs_off, size_t *part_off, size_t *bytes);
+svdq_status svdq_quantize_act_lowrank_down_kslice_fused(const svdq_linear *L, int64_t k0, int64_t Kp, const void *X,
+                                                        int32_t x_dtype, int64_t M, int64_t ldx, int32_t P,
+                                                        int32_t p, uint8_t *const *bufs, int32_t nbuf,
+                                                        void *stream);
+/* xl1 [dev] [M][rank] bf16 = bf16(sum_{p < P} parts[p][M][rank]) summed in p order.               */
+svdq_status svdq_tp_reduce_partials(int32_t P, int64_t M, int32_t rank, const float *parts, uint16_t *xl1,
+                                    void *stream);
 /* gathered [dev] = the P slices in rank order, slice p at gathered + p * slice_stride (0 = slice_bytes:
  * back to back, as all_gather_into_tensor of one slice per rank leaves them; larger when several
  * layers' slices travel in one gather); writes the full xq [M][K/2], xs and xl1 [M][rank] bf16

@@ -48,6 +48,7 @@ EXPORTS = [
     "svdq_debug_int4_group_accum", "svdq_debug_codec", "svdq_status_string", "svdq_last_error",
     "svdq_launch_count", "svdq_version", "svdq_k1_row_tile",
     "svdq_tp_slice_sizes", "svdq_quantize_act_lowrank_down_kslice", "svdq_tp_assemble_act",
+    "svdq_tp_gather_sizes", "svdq_quantize_act_lowrank_down_kslice_fused", "svdq_tp_reduce_partials",
 ]
 
 
@@ -108,6 +109,10 @@ _sig = {
     "svdq_debug_codec": [_P, _P, _I64, _I32, _P],
     "svdq_tp_slice_sizes": [_I32, _I64, _I64, _I32, _SZ, _SZ, _SZ, _SZ],
     "svdq_quantize_act_lowrank_down_kslice": [_LP, _I64, _I64, _P, _I32, _I64, _I64, _P, _P],
+    "svdq_tp_gather_sizes": [_I32, _I64, _I64, _I32, _I32, _SZ, _SZ, _SZ, _SZ],
+    "svdq_quantize_act_lowrank_down_kslice_fused": [_LP, _I64, _I64, _P, _I32, _I64, _I64, _I32, _I32, C.POINTER(_P),
+                                                    _I32, _P],
+    "svdq_tp_reduce_partials": [_I32, _I64, _I32, _P, _P, _P],
     "svdq_tp_assemble_act": [_I32, _I32, _I64, _I64, _I32, _P, C.c_size_t, C.c_size_t, _P, _P, _P, _P],
 }
 for _name, _args in _sig.items():
@@ -180,6 +185,30 @@ def svdq_quantize_act_lowrank_down_kslice(layer: "QuantizedLinear", k0: int, X, 
                                                       X.stride(0), _ptr(slice_buf), _stream(stream)),
            "svdq_quantize_act_lowrank_down_kslice")
     return slice_buf
+
+
+def svdq_tp_gather_sizes(fmt: str, M: int, K: int, rank: int, P: int):
+    """(xq_off, xs_off, part_off, bytes) of a fused-gather buffer (full K1 outputs + P partial slots)."""
+    o = [C.c_size_t() for _ in range(4)]
+    _check(_lib.svdq_tp_gather_sizes(FMT[fmt], M, K, rank, P, *[C.byref(x) for x in o]), "svdq_tp_gather_sizes")
+    return tuple(x.value for x in o)
+
+
+def svdq_quantize_act_lowrank_down_kslice_fused(layer: "QuantizedLinear", k0: int, X, P: int, p: int, buf_ptrs,
+                                                stream=None):
+    """K1 on input channels [k0, k0 + X.shape[1]) writing its codes / scales at their full-K place
+    and its partial in slot p of every gather buffer in `buf_ptrs` (device addresses, ints)."""
+    M, Kp = X.shape
+    arr = (_P * len(buf_ptrs))(*[int(q) for q in buf_ptrs])
+    _check(_lib.svdq_quantize_act_lowrank_down_kslice_fused(layer.ref, k0, Kp, _ptr(X), DTYPE[DTYPE_OF_TORCH[X.dtype]],
+                                                            M, X.stride(0), P, p, arr, len(buf_ptrs), _stream(stream)),
+           "svdq_quantize_act_lowrank_down_kslice_fused")
+
+
+def svdq_tp_reduce_partials(P: int, M: int, rank: int, parts, xl1, stream=None):
+    """xl1 = bf16(sum of the P fp32 partial slots, in rank order)."""
+    _check(_lib.svdq_tp_reduce_partials(P, M, rank, _ptr(parts), _ptr(xl1), _stream(stream)), "svdq_tp_reduce_partials")
+    return xl1
 
 
 def svdq_tp_assemble_act(fmt: str, P: int, M: int, K: int, rank: int, gathered, xq=None, xs=None, xl1=None,

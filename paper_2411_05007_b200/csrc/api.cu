@@ -267,6 +267,9 @@ svdq_status prepare_k1(const svdq_linear *L, const void *X, int32_t x_dtype, int
   p.xq = xq;
   p.xs = xs;
   p.xl1 = xl1;
+  p.ndst = 1;
+  p.out_k = p.K;
+  p.out_c0 = 0;
   std::memset(&maps->x, 0, sizeof(maps->x));
   std::memset(&maps->l1s, 0, sizeof(maps->l1s));
   std::memset(&maps->lam, 0, sizeof(maps->lam));
@@ -358,17 +361,31 @@ svdq_status svdq_tp_slice_sizes(int32_t fmt, int64_t M, int64_t Kp, int32_t rank
   return SVDQ_OK;
 }
 
-svdq_status svdq_quantize_act_lowrank_down_kslice(const svdq_linear *L, int64_t k0, int64_t Kp, const void *X,
-                                                  int32_t x_dtype, int64_t M, int64_t ldx, uint8_t *slice,
-                                                  void *stream) {
-  svdq_status st = check_linear(L, false);
+svdq_status svdq_tp_gather_sizes(int32_t fmt, int64_t M, int64_t K, int32_t rank, int32_t P, size_t *xq_off,
+                                 size_t *xs_off, size_t *part_off, size_t *bytes) {
+  if (!xq_off || !xs_off || !part_off || !bytes) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null output");
+  if (P < 1) return fail(SVDQ_ERR_INVALID_ARGUMENT, "P must be >= 1");
+  size_t bq, bs, bl;
+  svdq_status st = svdq_act_buffer_sizes(fmt, M, K, rank, &bq, &bs, &bl);
   if (st != SVDQ_OK) return st;
-  size_t oq, os, op, nb;
-  if ((st = svdq_tp_slice_sizes(L->fmt, M, Kp, L->rank, &oq, &os, &op, &nb)) != SVDQ_OK) return st;
-  if (k0 < 0 || k0 % 64 || k0 + Kp > L->K) return fail(SVDQ_ERR_SHAPE, "K-slice [%lld, %lld) outside [0, K)",
-                                                       (long long)k0, (long long)(k0 + Kp));
-  if (!slice) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null slice buffer");
-  if (!aligned16(slice)) return fail(SVDQ_ERR_ALIGNMENT, "slice buffer must be 16-byte aligned");
+  if (fmt == SVDQ_FMT_W8A8) return fail(SVDQ_ERR_UNSUPPORTED, "K-sliced K1: no W8A8 (per-token scales need the whole row)");
+  auto up = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
+  *xq_off = 0;
+  *xs_off = up(bq);
+  *part_off = *xs_off + up(bs);
+  *bytes = *part_off + up(static_cast<size_t>(P) * M * rank * 4);
+  return SVDQ_OK;
+}
+
+namespace {
+// K1 of L restricted to input channels [k0, k0 + Kp): validation, the restricted view, launch.
+svdq_status kslice_launch(const svdq_linear *L, int64_t k0, int64_t Kp, const void *X, int32_t x_dtype, int64_t M,
+                          int64_t ldx, uint8_t *xq, uint8_t *xs, float *part, int64_t out_k, int64_t out_c0,
+                          const int64_t *delta, int ndst, void *stream) {
+  if (k0 < 0 || k0 % 64 || Kp <= 0 || Kp % 64 || k0 + Kp > L->K)
+    return fail(SVDQ_ERR_SHAPE, "K-slice [%lld, %lld) must be 64-aligned inside [0, K)", (long long)k0,
+                (long long)(k0 + Kp));
+  if (L->fmt == SVDQ_FMT_W8A8) return fail(SVDQ_ERR_UNSUPPORTED, "K-sliced K1: no W8A8 (per-token scales)");
   svdq_linear V = *L;                        // the layer restricted to input channels [k0, k0 + Kp)
   V.K = Kp;
   V.lambda_inv = L->lambda_inv + k0;
@@ -377,14 +394,69 @@ svdq_status svdq_quantize_act_lowrank_down_kslice(const svdq_linear *L, int64_t 
   std::memset(&g, 0, sizeof(g));
   g.n = 1;
   const int rt = k1_rows_rt(((M + 127) / 128) * 128, L->rank);
-  float *part = reinterpret_cast<float *>(slice + op);
-  st = prepare_k1(&V, X, x_dtype, M, ldx, slice + oq, slice + os, reinterpret_cast<uint16_t *>(part), &g.pr[0].p,
-                  &g.pr[0], rt, L->K);
+  svdq_status st = prepare_k1(&V, X, x_dtype, M, ldx, xq, xs, reinterpret_cast<uint16_t *>(part), &g.pr[0].p,
+                              &g.pr[0], rt, L->K);
   if (st != SVDQ_OK) return st;
-  g.pr[0].p.xl1 = nullptr;
-  g.pr[0].p.xl1_f32 = L->rank ? part : nullptr;
+  K1Params &p = g.pr[0].p;
+  p.xl1 = nullptr;
+  p.xl1_f32 = L->rank ? part : nullptr;
+  p.out_k = out_k;
+  p.out_c0 = out_c0;
+  p.ndst = ndst;
+  for (int j = 0; j < ndst; ++j) p.dst_delta[j] = delta[j];
   cudaError_t e = launch_k1_rows_group(g, rt, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "K-sliced K1 launch");
+  ++g_launches;
+  return SVDQ_OK;
+}
+}  // namespace
+
+svdq_status svdq_quantize_act_lowrank_down_kslice(const svdq_linear *L, int64_t k0, int64_t Kp, const void *X,
+                                                  int32_t x_dtype, int64_t M, int64_t ldx, uint8_t *slice,
+                                                  void *stream) {
+  svdq_status st = check_linear(L, false);
+  if (st != SVDQ_OK) return st;
+  size_t oq, os, op, nb;
+  if ((st = svdq_tp_slice_sizes(L->fmt, M, Kp, L->rank, &oq, &os, &op, &nb)) != SVDQ_OK) return st;
+  if (!slice) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null slice buffer");
+  if (!aligned16(slice)) return fail(SVDQ_ERR_ALIGNMENT, "slice buffer must be 16-byte aligned");
+  const int64_t zero = 0;
+  return kslice_launch(L, k0, Kp, X, x_dtype, M, ldx, slice + oq, slice + os, reinterpret_cast<float *>(slice + op),
+                       Kp, 0, &zero, 1, stream);
+}
+
+svdq_status svdq_quantize_act_lowrank_down_kslice_fused(const svdq_linear *L, int64_t k0, int64_t Kp, const void *X,
+                                                        int32_t x_dtype, int64_t M, int64_t ldx, int32_t P,
+                                                        int32_t p, uint8_t *const *bufs, int32_t nbuf,
+                                                        void *stream) {
+  svdq_status st = check_linear(L, false);
+  if (st != SVDQ_OK) return st;
+  if (!bufs || nbuf < 1 || nbuf > 8) return fail(SVDQ_ERR_INVALID_ARGUMENT, "nbuf must be 1..8");
+  if (p < 0 || p >= P) return fail(SVDQ_ERR_INVALID_ARGUMENT, "slot %d outside [0, %d)", p, P);
+  for (int j = 0; j < nbuf; ++j) {
+    if (!bufs[j]) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null gather buffer %d", j);
+    if (!aligned16(bufs[j])) return fail(SVDQ_ERR_ALIGNMENT, "gather buffer %d must be 16-byte aligned", j);
+  }
+  size_t oq, os, op, nb;
+  if ((st = svdq_tp_gather_sizes(L->fmt, M, L->K, L->rank, P, &oq, &os, &op, &nb)) != SVDQ_OK) return st;
+  int64_t delta[8];
+  for (int j = 0; j < nbuf; ++j) delta[j] = bufs[j] - bufs[0];
+  uint8_t *b = bufs[0];
+  // codes: column k0 of the [M][K/2] rows (the kernel adds row * K/2); scales: group k0/16 of the
+  // full-K layout (out_c0); partial: slot p
+  return kslice_launch(L, k0, Kp, X, x_dtype, M, ldx, b + oq + k0 / 2, b + os,
+                       reinterpret_cast<float *>(b + op) + static_cast<int64_t>(p) * M * L->rank, L->K, k0 / 16,
+                       delta, nbuf, stream);
+}
+
+svdq_status svdq_tp_reduce_partials(int32_t P, int64_t M, int32_t rank, const float *parts, uint16_t *xl1,
+                                    void *stream) {
+  if (P < 1 || M < 1 || rank < 1 || rank > 128 || rank % 16) return fail(SVDQ_ERR_SHAPE, "bad P / M / rank");
+  if (!parts || !xl1) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null buffer");
+  svdq_status st = check_device();
+  if (st != SVDQ_OK) return st;
+  cudaError_t e = launch_tp_reduce_partials(P, M, rank, parts, xl1, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "TP partial reduction launch");
   ++g_launches;
   return SVDQ_OK;
 }

@@ -58,6 +58,14 @@ struct K1Params {
   uint8_t *xs;
   uint16_t *xl1;
   float *xl1_f32;     // tensor-parallel K-slice: fp32 partial X L1s^T [M][rank] instead of bf16 xl1
+  // fused packed all-gather: every output store is repeated at `ndst` byte
+  // offsets dst_delta[j] from xq / xs / xl1_f32 (destination j = rank j's gather buffer, possibly a
+  // peer's memory mapped over NVLink); ndst = 1, dst_delta[0] = 0 otherwise
+  int ndst;
+  int64_t dst_delta[8];
+  // layout of the outputs: codes row pitch out_k / 2 bytes, scales of the (rows, out_k) layout
+  // starting at 16-column group out_c0 (K-slice inside a full-K buffer); defaults out_k = K, 0
+  int64_t out_k, out_c0;
 };
 cudaError_t launch_k1_int8_rows(const K1Params &p, cudaStream_t s);   // W8A8 per-token INT8 codes
 // Grouped K1: up to kMaxGroup1 problems (same fmt, scale dtype and rank) in one launch; the
@@ -157,6 +165,7 @@ struct TpSliceLayout {
   int64_t xq_off, xs_off, part_off, bytes;   // byte offsets inside one rank's slice
 };
 TpSliceLayout tp_slice_layout(int fmt, int64_t M, int64_t Kp, int rank);
+cudaError_t launch_tp_reduce_partials(int P, int64_t M, int rank, const float *parts, uint16_t *xl1, cudaStream_t s);
 cudaError_t launch_tp_assemble(int fmt, int P, int64_t M, int64_t K, int rank, const uint8_t *gathered,
                                int64_t slice_stride, uint8_t *xq, uint8_t *xs, uint16_t *xl1, cudaStream_t s);
 

@@ -265,9 +265,11 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
     const int64_t row = row0 + m;
     const bool rvalid = row < p.M;
     const float t6 = __fmul_rn(__frcp_rn(p.gs_x), __frcp_rn(6.0f));
-    uint2 *xq_ptr = reinterpret_cast<uint2 *>(p.xq + row * (K / 2) + static_cast<int64_t>(qb) * 32) + q4;
-    uint8_t *sf_ptr = p.xs + sf_offset(row, 0, K) + static_cast<int64_t>(qb) * 512 + q4;
-    uint16_t *s16_ptr = reinterpret_cast<uint16_t *>(p.xs) + row * (K / 64) + qb;
+    // output addressing: the layer's own layout (out_k = K, out_c0 = 0), or -- fused tensor-parallel
+    // gather -- this K-slice's place inside the full-K layout (out_k = full K, out_c0 = k0 / 16)
+    uint2 *xq_ptr = reinterpret_cast<uint2 *>(p.xq + row * (p.out_k / 2) + static_cast<int64_t>(qb) * 32) + q4;
+    uint8_t *sf_ptr = p.xs + sf_offset(row, p.out_c0, p.out_k) + static_cast<int64_t>(qb) * 512 + q4;
+    uint16_t *s16_ptr = reinterpret_cast<uint16_t *>(p.xs) + row * (p.out_k / 64) + p.out_c0 / 4 + qb;
     // L2 prefetch of this lane's future X lines (one 128-B line per staged row, issued by the q4 == 0
     // lane): kPf stages ahead, so the TMA loads find X in L2 instead of paying the DRAM round trip
     // with only S stages in flight.  An L2 prefetch never returns stale data, so the first ones go
@@ -362,8 +364,11 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
         const uint32_t w0 = e2m1x8_pairs(fmul2(xh[0], q2), fmul2(xh[1], q2), fmul2(xh[2], q2), fmul2(xh[3], q2));
         const uint32_t w1 = e2m1x8_pairs(fmul2(xh[4], q2), fmul2(xh[5], q2), fmul2(xh[6], q2), fmul2(xh[7], q2));
         if (active) {
-          if (rvalid) *xq_ptr = make_uint2(w0, w1);
-          *sf_ptr = static_cast<uint8_t>(sf);                   // padding rows (>= M) get 0x00
+          for (int j = 0; j < p.ndst; ++j) {                    // 1, or every rank of a fused gather
+            const int64_t d = p.dst_delta[j];
+            if (rvalid) *reinterpret_cast<uint2 *>(reinterpret_cast<uint8_t *>(xq_ptr) + d) = make_uint2(w0, w1);
+            sf_ptr[d] = static_cast<uint8_t>(sf);               // padding rows (>= M) get 0x00
+          }
         }
       } else {
         amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
@@ -386,8 +391,11 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
           w[c] = word;
         }
         if (rvalid && active) {
-          *xq_ptr = make_uint2(w[0], w[1]);
-          if (q4 == 0) *s16_ptr = sc;
+          for (int j = 0; j < p.ndst; ++j) {
+            const int64_t d = p.dst_delta[j];
+            *reinterpret_cast<uint2 *>(reinterpret_cast<uint8_t *>(xq_ptr) + d) = make_uint2(w[0], w[1]);
+            if (q4 == 0) *reinterpret_cast<uint16_t *>(reinterpret_cast<uint8_t *>(s16_ptr) + d) = sc;
+          }
         }
       }
     }
@@ -434,7 +442,11 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
     }
     const int64_t row = row0 + mm;
     if (row < p.M) {
-      if (p.xl1_f32) *reinterpret_cast<float2 *>(p.xl1_f32 + row * r + col) = make_float2(s0, s1);
+      if (p.xl1_f32) {
+        for (int j = 0; j < p.ndst; ++j)
+          *reinterpret_cast<float2 *>(reinterpret_cast<uint8_t *>(p.xl1_f32 + row * r + col) + p.dst_delta[j]) =
+              make_float2(s0, s1);
+      }
       else *reinterpret_cast<uint32_t *>(p.xl1 + row * r + col) = pack_bf16x2(s0, s1);
     }
   }

@@ -8,6 +8,9 @@
 //   INT4  xs[m][p Kp/64 + j]     = slice_p.scales[m][j]
 //   xl1[m][t] = bf16(sum_p part_p[m][t]) summed in rank order (deterministic on every rank).
 // Groups never straddle slices because Kp % 64 == 0.
+// Fused gather: K1 writes codes / scales straight into every rank's full-K
+// buffers (k1_rows.cu multi-destination stores) and its fp32 partial into slot p; after the
+// cross-rank barrier only the partial reduction below remains.
 #include <cstdint>
 #include <cuda_bf16.h>
 
@@ -56,7 +59,24 @@ __global__ void tp_assemble_kernel(int fmt, int P, int64_t M, int64_t K, int ran
     xl1[i] = __bfloat16_as_ushort(__float2bfloat16_rn(s));
   }
 }
+
+__global__ void tp_reduce_kernel(int P, int64_t n, const float *__restrict__ parts, uint16_t *__restrict__ xl1) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float s = 0.f;
+    for (int p = 0; p < P; ++p) s += parts[p * n + i];   // rank order: deterministic
+    xl1[i] = __bfloat16_as_ushort(__float2bfloat16_rn(s));
+  }
+}
 }  // namespace
+
+cudaError_t launch_tp_reduce_partials(int P, int64_t M, int rank, const float *parts, uint16_t *xl1, cudaStream_t s) {
+  const int64_t n = M * rank;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 4 * device_sm_count()) blocks = 4 * device_sm_count();
+  tp_reduce_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(P, n, parts, xl1);
+  return cudaGetLastError();
+}
 
 TpSliceLayout tp_slice_layout(int fmt, int64_t M, int64_t Kp, int rank) {
   TpSliceLayout L;

@@ -14,6 +14,11 @@ full X.  So rank p of P holds
 Two ways to feed a layer whose input is needed in full:
   Variant 1 (`forward`): X replicated on every rank, K1 runs redundantly, K2 on the N-shard;
       `all_gather_into_tensor` of the bf16 Y shards where a consumer needs the full output.
+  Fused gather (`SymmetricGather`): the same Variant 2, but K1 itself stores
+      its codes / scales at their final full-K place in EVERY rank's gather buffer (torch symmetric
+      memory: peer buffers mapped over NVLink) and its partial in slot p; one device-side barrier,
+      a tiny partial reduction, and K2 reads the buffer -- no collective, no re-layout pass, and
+      the transfer overlaps K1's HBM read.
   Variant 2 (`forward_from_shard`, SURVEY 8(e) "quantize, then gather"): rank p holds only
       X[:, p Kp:(p+1) Kp] (its shard of the previous column-parallel layer's output); it runs K1 on
       that K-slice (svdq_quantize_act_lowrank_down_kslice), ONE all-gather moves the packed slices
@@ -30,7 +35,8 @@ import torch
 import torch.distributed as dist
 
 from .abi import (QuantizedLinear, svdq_act_buffer_sizes, svdq_gemm_w4a4_lowrank_up, svdq_linear_forward,
-                  svdq_quantize_act_lowrank_down_kslice, svdq_tp_assemble_act, svdq_tp_slice_sizes)
+                  svdq_quantize_act_lowrank_down_kslice, svdq_quantize_act_lowrank_down_kslice_fused,
+                  svdq_tp_assemble_act, svdq_tp_gather_sizes, svdq_tp_reduce_partials, svdq_tp_slice_sizes)
 
 
 def _sf_atom_bytes(K: int) -> int:
@@ -195,3 +201,70 @@ class ColumnParallelSVDQLinear:
             t = torch.empty(shape, dtype=dtype, device=device)
             self._bufs[key] = t
         return t
+
+
+class SymmetricGather:
+    """Fused packed all-gather: every rank owns a gather buffer in symmetric memory
+    (torch.distributed._symmetric_memory, peers mapped over NVLink) with one region per layer; a
+    region holds the layer's full K1 outputs (xq, xs) plus P fp32 partial slots
+    (svdq_tp_gather_sizes).  fill(i, ...) runs K1 on this rank's K-slice and stores it, inside the
+    kernel, into region i of EVERY rank's buffer; sync() is the cross-rank device barrier; after it,
+    outputs(i) reduces the partials (rank order) and returns (xq, xs, xl1) for K2."""
+
+    def __init__(self, specs, device, group=None):
+        """specs: [(fmt, M, K, rank)] per layer region."""
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.specs, self.regions, total = list(specs), [], 0
+        for fmt, M, K, r in self.specs:
+            oq, os_, op, nb = svdq_tp_gather_sizes(fmt, M, K, r, self.world)
+            self.regions.append((total, oq, os_, op, nb))
+            total += nb
+        self.buf = self._alloc(total, device)
+        self._xl1 = [torch.empty(max(M * r, 8), dtype=torch.int16, device=device) for _, M, _, r in self.specs]
+
+    def _alloc(self, total, device):
+        import torch.distributed._symmetric_memory as symm_mem
+        buf = symm_mem.empty(total, dtype=torch.uint8, device=device)
+        self.handle = symm_mem.rendezvous(buf, self.group)
+        self.ptrs = [int(p) for p in self.handle.buffer_ptrs]
+        return buf
+
+    def fill(self, i: int, layer: QuantizedLinear, k0: int, x_shard: torch.Tensor, stream=None):
+        base = self.regions[i][0]
+        svdq_quantize_act_lowrank_down_kslice_fused(layer, k0, x_shard, self.world, self.rank,
+                                                    [p + base for p in self.ptrs], stream=stream)
+
+    def sync(self):
+        self.handle.barrier(channel=0)
+
+    def outputs(self, i: int, stream=None):
+        fmt, M, K, r = self.specs[i]
+        base, oq, os_, op, nb = self.regions[i]
+        bq, bs, _ = svdq_act_buffer_sizes(fmt, M, K, r)
+        xq = self.buf[base + oq:base + oq + bq]
+        xs = self.buf[base + os_:base + os_ + bs]
+        if r:
+            parts = self.buf[base + op:base + op + self.world * M * r * 4]
+            svdq_tp_reduce_partials(self.world, M, r, parts, self._xl1[i], stream=stream)
+        return xq, xs, self._xl1[i]
+
+
+class IpcGather(SymmetricGather):
+    """The same buffers from CUDA IPC handles, for ranks sharing one device (the one-GPU
+    multi-process tests: symmetric memory refuses overlapping devices).  sync() is a stream
+    synchronize + host barrier (correct, not fast)."""
+
+    def _alloc(self, total, device):
+        from torch.multiprocessing.reductions import reduce_tensor
+        buf = torch.zeros(total, dtype=torch.uint8, device=device)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, reduce_tensor(buf), group=self.group)
+        self._peers = [buf if j == self.rank else fn(*args) for j, (fn, args) in enumerate(handles)]
+        self.ptrs = [int(t.data_ptr()) for t in self._peers]
+        return buf
+
+    def sync(self):
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)

@@ -91,3 +91,40 @@ def test_variant2_rejects_w8a8_and_bad_slices():
     with pytest.raises(P.SvdqError) as e:
         P.svdq_tp_slice_sizes("w8a8", 64, 384, 16)
     assert e.value.status == 5
+
+
+@pytest.mark.parametrize("fmt", ["nvfp4", "int4"])
+@pytest.mark.parametrize("world,M,K,r", [(4, 200, 3072, 32), (8, 129, 3072, 16), (2, 300, 1152, 0)])
+def test_fused_gather_emulated(fmt, world, M, K, r):
+    """Fused packed all-gather, P ranks emulated on one GPU: rank p's K-sliced K1
+    stores into all P gather buffers (local stand-ins for the symmetric-memory peers); afterwards every
+    buffer's xq / xs equal the unsharded K1's bit for bit and the reduced xl1 equals the all-gather
+    path's (svdq_tp_assemble_act) bit for bit."""
+    need_cuda()
+    import torch
+    import paper_2411_05007_b200 as P
+    from paper_2411_05007_b200 import tp
+    x, w, lam, ops = make_case(fmt, M, K, 256, r, seed=11 + world, cfg=26)
+    dev = torch.device("cuda")
+    full = layer_from_ops(P, ops, dev)
+    X = torch.from_numpy(x).to(dev).to(torch.bfloat16)
+    kp = K // world
+    oq, os_, op, nb = P.svdq_tp_gather_sizes(fmt, M, K, r, world)
+    bufs = [torch.full((nb,), 0xAB, dtype=torch.uint8, device=dev) for _ in range(world)]
+    slices = []
+    for p in range(world):
+        xsh = X[:, p * kp:(p + 1) * kp].contiguous()
+        P.svdq_quantize_act_lowrank_down_kslice_fused(full, p * kp, xsh, world, p, [b.data_ptr() for b in bufs])
+        slices.append(P.svdq_quantize_act_lowrank_down_kslice(full, p * kp, xsh).clone())
+    sq, ss, sl = P.svdq_quantize_act_lowrank_down(full, X)
+    aq, as_, al = P.svdq_tp_assemble_act(fmt, world, M, K, r, torch.cat(slices))
+    torch.cuda.synchronize()
+    bq, bs, _ = P.svdq_act_buffer_sizes(fmt, M, K, r)
+    for b in bufs:
+        assert torch.equal(b[oq:oq + bq], sq), "codes differ from the unsharded K1"
+        assert torch.equal(b[os_:os_ + bs], ss), "scales differ from the unsharded K1"
+        if r:
+            xl1 = torch.empty(M * r, dtype=torch.int16, device=dev)
+            P.svdq_tp_reduce_partials(world, M, r, b[op:op + world * M * r * 4], xl1)
+            torch.cuda.synchronize()
+            assert torch.equal(xl1, al[:M * r]), "xl1 differs from the all-gather path's"

@@ -45,9 +45,21 @@ def _worker(rank, world, port, fmt, q):
         blocks = torch.empty(world * M, y2.shape[1], dtype=y2.dtype, device=dev)
         tp.all_gather(blocks, y2.contiguous())
         y2full = tp.assemble_columns(blocks, world)
+        # fused gather: K1 writes its slice into both ranks' buffers (CUDA IPC here)
+        fused = None
+        try:
+            sg = tp.IpcGather([(fmt, M, K, r)], dev)               # both ranks share cuda:0 here
+            sg.fill(0, layer.local, rank * kp, X[:, rank * kp:(rank + 1) * kp].contiguous())
+            sg.sync()
+            xq, xs, xl1 = sg.outputs(0)
+            y3 = P.svdq_gemm_w4a4_lowrank_up(layer.local, xq, xs, xl1, M)
+            tp.all_gather(blocks, y3.contiguous())
+            fused = tp.assemble_columns(blocks, world).view(torch.int16).cpu().numpy()
+        except Exception as e:  # CUDA IPC unavailable
+            fused = f"unavailable: {type(e).__name__}: {str(e)[:200]}"
         torch.cuda.synchronize()
         if rank == 0:
-            q.put(("ok", y1.view(torch.int16).cpu().numpy(), y2full.view(torch.int16).cpu().numpy()))
+            q.put(("ok", y1.view(torch.int16).cpu().numpy(), (y2full.view(torch.int16).cpu().numpy(), fused)))
     except Exception as e:  # pragma: no cover - surfaced through the queue
         q.put(("err", repr(e), None))
         raise
@@ -70,10 +82,11 @@ def test_tp_two_processes_one_gpu(fmt):
     procs = [ctx.Process(target=_worker, args=(rk, world, port, fmt, q)) for rk in range(world)]
     for p in procs:
         p.start()
-    status, y1, y2 = q.get(timeout=300)
+    status, y1, y23 = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
     assert status == "ok", y1
+    y2, y3 = y23
     # single-process references: the unsharded forward (Variant 1 is bitwise equal to it) and the
     # emulated Variant 2
     dev = torch.device("cuda")
@@ -93,9 +106,13 @@ def test_tp_two_processes_one_gpu(fmt):
         ys.append(P.svdq_gemm_w4a4_lowrank_up(ranks[p].local, xq, xs, xl1, M))
     ref2 = torch.cat(ys, dim=1).view(torch.int16).cpu().numpy()
     np.testing.assert_array_equal(y2, ref2)
+    if isinstance(y3, str):
+        pytest.skip(f"fused symmetric-memory gather: {y3}")
+    np.testing.assert_array_equal(y3, ref2)           # fused gather == collective gather, bitwise
 
 
-def test_bench_tp_mode_two_ranks_gloo():
+@pytest.mark.parametrize("gather", ["nccl", "fused"])
+def test_bench_tp_mode_two_ranks_gloo(gather):
     """bench.py's tensor-parallel arm end to end under torchrun (2 ranks on the one GPU, gloo):
     one JSON line with the strong-scaling TP fields and a positive value."""
     import json
@@ -107,7 +124,7 @@ def test_bench_tp_mode_two_ranks_gloo():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
-           "--gpus", "2", "--backend", "gloo", "--steps", "2", "--warmup", "3", "--no-extras"]
+           "--gpus", "2", "--backend", "gloo", "--steps", "2", "--warmup", "3", "--no-extras", "--tp-gather", gather]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
