@@ -623,15 +623,20 @@ def run_tp(args, rank, world, local_rank, backend):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     layers = flux_block_layers(args.batch)
+    # --tp-emulate P (one GPU): rank 0's share of a P-way TP step -- its shards, K-slices and the
+    # assembly of P slices -- with the gather replaced by a local copy of this rank's slice; the
+    # NVLink transfer is MODELED below (a projection, labelled as such)
+    emulate = args.tp_emulate if world == 1 and args.tp_emulate > 1 else 0
+    shard_world, shard_rank = (emulate, 0) if emulate else (world, rank)
     net = []
     for i, L in enumerate(layers):
         (_, full, b), = build_layers(P, torch, [L], args.fmt, dev, seed_index=i)
-        cp = tp.ColumnParallelSVDQLinear(full, world=world, rank=rank)
+        cp = tp.ColumnParallelSVDQLinear(full, world=shard_world, rank=shard_rank)
         sharded = L.name.endswith(SHARDED_INPUT)
         n = cp.local.N
         e = dict(L=L, cp=cp, sharded=sharded, y=torch.empty(L.M, n, dtype=torch.bfloat16, device=dev))
         if sharded:
-            k0, kp = tp.kslice_bounds(L.K, world, rank)
+            k0, kp = tp.kslice_bounds(L.K, shard_world, shard_rank)
             e["x"] = b["x"][:, k0:k0 + kp].contiguous()
             nb = P.svdq_tp_slice_sizes(args.fmt, L.M, kp, L.r)[3]
             e["slice"] = torch.empty(nb, dtype=torch.uint8, device=dev)
@@ -649,17 +654,20 @@ def run_tp(args, rank, world, local_rank, backend):
     # fused: no collective -- K1 stores each slice into every rank's symmetric-memory buffer
     # (SURVEY 8(f) row 2), then one device-side barrier (CUDA IPC + host barrier for gloo tests)
     gbuf, sgs = {}, {}
-    fused = args.tp_gather == "fused" and world > 1
+    fused = args.tp_gather == "fused" and (world > 1 or emulate)
     for gi, grp in enumerate(groups):
         if grp[0]["sharded"]:
             if fused:
                 specs = [(args.fmt, e["L"].M, e["L"].K, e["L"].r) for e in grp]
-                sgs[gi] = (tp.IpcGather if backend == "gloo" else tp.SymmetricGather)(specs, dev)
+                if emulate:
+                    sgs[gi] = tp.EmulatedGather(specs, dev, world=shard_world)
+                else:
+                    sgs[gi] = (tp.IpcGather if backend == "gloo" else tp.SymmetricGather)(specs, dev)
                 gbuf[gi] = (None, sgs[gi].buf)
             else:
                 tot = sum(e["slice"].numel() for e in grp)
                 gbuf[gi] = (torch.empty(tot, dtype=torch.uint8, device=dev),
-                            torch.empty(world * tot, dtype=torch.uint8, device=dev))
+                            torch.zeros(shard_world * tot, dtype=torch.uint8, device=dev))
     stream = torch.cuda.Stream(device=dev)
     comm_ev = []
 
@@ -677,7 +685,7 @@ def run_tp(args, rank, world, local_rank, backend):
                     e["xq"], e["xs"], e["xl1"] = sgs[gi].outputs(j, stream=st)
             elif grp[0]["sharded"]:
                 send, recv = gbuf[gi]
-                tot = recv.numel() // world
+                tot = recv.numel() // shard_world
                 off = 0
                 for e in grp:
                     nb = e["slice"].numel()
@@ -688,13 +696,13 @@ def run_tp(args, rank, world, local_rank, backend):
                     record[gi][0].record(st)
                 if world > 1:
                     tp.all_gather(recv, send)
-                else:
-                    recv.copy_(send)
+                else:                            # P = 1, or emulation: this rank's slice only
+                    recv[:tot].copy_(send)
                 if record is not None:
                     record[gi][1].record(st)
                 off = 0
                 for e in grp:                    # rank p's slice of this layer at recv[p * tot + off]
-                    P.svdq_tp_assemble_act(args.fmt, world, e["L"].M, e["L"].K, e["L"].r, recv[off:], e["xq"], e["xs"],
+                    P.svdq_tp_assemble_act(args.fmt, shard_world, e["L"].M, e["L"].K, e["L"].r, recv[off:], e["xq"], e["xs"],
                                            e["xl1"], slice_stride=tot, stream=st)
                     off += e["slice"].numel()
             elif len(grp) > 1:
@@ -767,6 +775,23 @@ def run_tp(args, rank, world, local_rank, backend):
     cfg = bench_config(args, world)
     cfg["parallelism"] = f"tp{world} (column-parallel over N; SURVEY 8(e) Variant 2 packed all-gathers)"
     cfg["block_latency_ms"] = round(total_ms / args.steps, 4)
+    projection = None
+    if emulate:
+        # one rank's measured compute + the modeled packed all-gathers (bytes each rank receives at an
+        # assumed all-gather bus bandwidth + a per-collective latency); overlapped = max per gather
+        # bytes each rank receives: (P-1)/P of the packed slices (all-gather) or of the full K1 outputs
+        # written by the peers (fused)
+        recv_bytes = [gbuf[gi][1].numel() * (emulate - 1) / emulate for gi in gbuf]
+        comm_model_ms = sum(b_ / (args.tp_bw_gbs * 1e9) * 1e3 + args.tp_lat_us * 1e-3 for b_ in recv_bytes)
+        step_ms = total_ms / args.steps
+        projection = {"P": emulate, "per_rank_compute_ms": round(step_ms, 4),
+                      "modeled_comm_ms": round(comm_model_ms, 4),
+                      "projected_step_ms_serial": round(step_ms + comm_model_ms, 4),
+                      "projected_tflops_serial": round(flops / ((step_ms + comm_model_ms) / 1e3) / 1e12, 1),
+                      "assumptions": {"allgather_bus_GBps": args.tp_bw_gbs, "per_collective_latency_us": args.tp_lat_us},
+                      "note": "MEASURED: rank 0's kernels of a P-way TP step on one B200 (its N-shards, K-slice K1, "
+                              "assembly of P slices); MODELED: the NVLink all-gathers.  Not a multi-GPU run."}
+        cfg["parallelism"] = f"tp{emulate} emulated on one GPU (rank 0's work; gathers modeled)"
     return {
         "metric": METRIC, "value": round(flops * args.steps / (total_ms / 1e3) / 1e12, 2), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
@@ -785,6 +810,7 @@ def run_tp(args, rank, world, local_rank, backend):
                "note": "value = the full block-pair FLOPs (sum 2MNK over all linears) / max-over-ranks step time "
                        "(strong scaling: the total work is fixed); comm from events around each all-gather in an "
                        "eager replay of the step"},
+        "tp_projection": projection,
         "clocks": clk.summary(),
     }
 
@@ -908,6 +934,10 @@ def main():
     ap.add_argument("--tp-gather", default="nccl", choices=["nccl", "fused"],
                     help="TP packed-slice gather: one all_gather_into_tensor, or K1 storing into every rank's "
                          "symmetric-memory buffer (SURVEY 8(f) row 2)")
+    ap.add_argument("--tp-emulate", type=int, default=0,
+                    help="one GPU, --mode tp: time rank 0's share of a P-way TP step, model the gathers")
+    ap.add_argument("--tp-bw-gbs", type=float, default=750.0, help="modeled all-gather bus bandwidth (emulation)")
+    ap.add_argument("--tp-lat-us", type=float, default=10.0, help="modeled per-collective latency (emulation)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: multi-process tests on one GPU (NCCL refuses two ranks per device)")
     args = ap.parse_args()

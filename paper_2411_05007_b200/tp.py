@@ -211,11 +211,11 @@ class SymmetricGather:
     kernel, into region i of EVERY rank's buffer; sync() is the cross-rank device barrier; after it,
     outputs(i) reduces the partials (rank order) and returns (xq, xs, xl1) for K2."""
 
-    def __init__(self, specs, device, group=None):
+    def __init__(self, specs, device, group=None, world: int | None = None, rank: int | None = None):
         """specs: [(fmt, M, K, rank)] per layer region."""
-        self.group = group if group is not None else dist.group.WORLD
-        self.world = dist.get_world_size(self.group)
-        self.rank = dist.get_rank(self.group)
+        self.group = group if group is not None else (dist.group.WORLD if world is None else None)
+        self.world = world if world is not None else dist.get_world_size(self.group)
+        self.rank = rank if rank is not None else dist.get_rank(self.group)
         self.specs, self.regions, total = list(specs), [], 0
         for fmt, M, K, r in self.specs:
             oq, os_, op, nb = svdq_tp_gather_sizes(fmt, M, K, r, self.world)
@@ -268,3 +268,19 @@ class IpcGather(SymmetricGather):
     def sync(self):
         torch.cuda.current_stream().synchronize()
         dist.barrier(group=self.group)
+
+
+class EmulatedGather(SymmetricGather):
+    """One rank's view of a P-way fused gather on a single GPU (timing emulation): K1 stores only into
+    this rank's own buffer; sync() is a no-op."""
+
+    def __init__(self, specs, device, world: int, rank: int = 0):
+        super().__init__(specs, device, world=world, rank=rank)
+
+    def _alloc(self, total, device):
+        buf = torch.zeros(total, dtype=torch.uint8, device=device)
+        self.ptrs = [int(buf.data_ptr())]
+        return buf
+
+    def sync(self):
+        pass
