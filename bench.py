@@ -42,11 +42,37 @@ def flux_block_layers(batch=1):
     return synth.flux_double_block(batch) + synth.flux_single_block(batch)
 
 
+def config_layers(args):
+    """The step's linears: FLUX.1 block pair (C4, default), a PixArt-Sigma block's linears (C2,
+    fp16, 4096 tokens per image) or an SDXL attention/FF set (C3, fp16, CFG batch 2, rank 32 + LoRA
+    16), token counts scaled by --batch."""
+    import dataclasses
+    if args.config == "flux":
+        return flux_block_layers(args.batch)
+    base = synth.C2 if args.config == "pixart" else synth.C3
+    return [dataclasses.replace(L, M=L.M * args.batch) for L in base]
+
+
+def eff_rank(L):
+    """Rank of the deployed low-rank branch: r, plus the LoRA rank concatenated into it."""
+    return L.r + L.lora
+
+
+WORKLOADS = {
+    "flux": "flux1-dev block linears: 1 double block (img 4096 tok + txt 512 tok: qkv, proj, mlp_up, mlp_down) "
+            "+ 1 single block (4608 tok: linear1, linear2)",
+    "pixart": "pixart-sigma 1024px block linears (4096 tok: qkv, attn_out, cross_q, cross_out, fc1, fc2), fp16",
+    "sdxl": "sdxl 1024px attention/FF linears, CFG batch 2 (8192 tok at 640 ch, 2048 tok at 1280 ch), fp16, "
+            "rank 32 + LoRA 16",
+}
+
+
 def bench_config(args, world):
     """The workload description shared by both arms (svdq and --impl reference)."""
-    return {"workload": "flux1-dev block linears: 1 double block (img 4096 tok + txt 512 tok: "
-                        "qkv, proj, mlp_up, mlp_down) + 1 single block (4608 tok: linear1, linear2)",
-            "batch": args.batch, "hidden": 3072, "mlp": 12288, "rank": 16 if args.fmt == "w8a8" else 32, "format": args.fmt,
+    dims = {"flux": (3072, 12288), "pixart": (1152, 4608), "sdxl": (640, 5120)}[args.config]
+    rank = 16 if args.fmt == "w8a8" else (48 if args.config == "sdxl" else 32)
+    return {"workload": WORKLOADS[args.config], "config": args.config,
+            "batch": args.batch, "hidden": dims[0], "mlp": dims[1], "rank": rank, "format": args.fmt,
             "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
             "l2": "flushed between steps outside the per-step events (512 MiB write, then a 256 MiB read "
                   "so the flush's dirty lines are written back before the step starts)"}
@@ -168,27 +194,33 @@ def build_layers(P, torch, layers, fmt, dev, quality=None, seed_index=None):
         if seed_index is not None:
             i = seed_index
         g = torch.Generator(device="cpu").manual_seed(4000 + i)
+        td = torch.float16 if L.dtype == "fp16" else torch.bfloat16
         w = synth.gen_w(L.K, L.N, synth.rng(4, i, 1))
-        xcal = torch.from_numpy(synth.gen_x(256, L.K, synth.rng(4, i, 2))).to(dev).to(torch.bfloat16)
+        xcal = torch.from_numpy(synth.gen_x(256, L.K, synth.rng(4, i, 2))).to(dev).to(td)
         w_d = torch.from_numpy(w).to(dev)
         # lambda(alpha = 0.5) (App. D) from the library's offline alpha search on a one-point grid
-        _, lam, _ = P.svdq_search_alpha(xcal, w_d, L.r, fmt, [0.5])
-        bias = torch.from_numpy(synth.gen_bias(L.N, synth.rng(4, i, 3))).to(dev).to(torch.bfloat16)
-        layer = P.svdq_quantize_weights(w_d, lam, L.r, fmt, "bf16", 1.0, bias=bias)
-        x = torch.from_numpy(synth.gen_x(L.M, L.K, synth.rng(4, i, 0))).to(dev).to(torch.bfloat16)
+        _, lam, _ = P.svdq_search_alpha(xcal, w_d, L.r, fmt, [0.5], scale_dtype=L.dtype)
+        bias = torch.from_numpy(synth.gen_bias(L.N, synth.rng(4, i, 3))).to(dev).to(td)
+        layer = P.svdq_quantize_weights(w_d, lam, L.r, fmt, L.dtype, 1.0, bias=bias)
+        if L.lora:                                   # LoRA by concatenation into L1 / L2
+            a, b_ = synth.gen_lora(L.K, L.N, L.lora, synth.rng(4, i, 4), synth.rng(4, i, 5))
+            layer = P.svdq_lora_fuse(layer, torch.from_numpy(a).to(dev), torch.from_numpy(b_).to(dev))
+        x = torch.from_numpy(synth.gen_x(L.M, L.K, synth.rng(4, i, 0))).to(dev).to(td)
         if quality is not None:
             # unscored sanity metric: ||XW + b - Y|| / ||XW + b|| on 64 rows, fp64 reference
             rows = torch.arange(0, L.M, max(1, L.M // 64), device=dev)[:64]
             y_s = P.svdq_linear_forward(layer, x[rows].contiguous()).double()
             ref = x[rows].double() @ torch.from_numpy(w).to(dev).double() + bias.double()
+            if L.lora:
+                ref = ref + x[rows].double() @ (torch.from_numpy(a).to(dev).double() @ torch.from_numpy(b_).to(dev).double())
             quality[L.name] = round(float((y_s - ref).norm() / ref.norm()), 5)
-        bq, bs, bl = P.svdq_act_buffer_sizes(fmt, L.M, L.K, L.r)
+        bq, bs, bl = P.svdq_act_buffer_sizes(fmt, L.M, L.K, layer.rank)
         bufs = dict(
             x=x,
             xq=torch.empty(bq, dtype=torch.uint8, device=dev),
             xs=torch.empty(bs, dtype=torch.uint8, device=dev),
             xl1=torch.empty(max(bl // 2, 8), dtype=torch.int16, device=dev),
-            y=torch.empty(L.M, L.N, dtype=torch.bfloat16, device=dev),
+            y=torch.empty(L.M, L.N, dtype=td, device=dev),
         )
         out.append((L, layer, bufs))
         del w, g
@@ -203,15 +235,15 @@ def run_svdq(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    layers = flux_block_layers(args.batch)
+    layers = config_layers(args)
     if args.fmt == "w8a8":                      # the paper's 8-bit setting uses rank 16
         import dataclasses
-        layers = [dataclasses.replace(L, r=16) for L in layers]
+        layers = [dataclasses.replace(L, r=16, lora=0) for L in layers]
     quality = {}
     built = build_layers(P, torch, layers, args.fmt, dev, quality)
     flops = sum(2.0 * L.M * L.N * L.K for L in layers)
     cbytes = {"nvfp4": 0.5625, "int4": 0.53125, "w8a8": 1.0}[args.fmt]
-    k1_bytes = sum(L.M * L.K * (2 + cbytes) + L.M * L.r * 2 for L in layers)
+    k1_bytes = sum(L.M * L.K * (2 + cbytes) + L.M * eff_rank(L) * 2 for L in layers)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     flush_sink = torch.empty((), dtype=torch.int64, device=dev)
     stream = torch.cuda.Stream(device=dev)
@@ -283,7 +315,7 @@ def run_svdq(args, rank, world, local_rank):
         with torch.cuda.graph(g["dag"], stream=stream):
             step_dag(bl, stream)
         g["grouped"] = None
-        if args.fmt == "nvfp4":
+        if args.fmt == "nvfp4" and args.config == "flux":
             with torch.cuda.stream(stream):
                 step_grouped(bl, stream)
             torch.cuda.synchronize()
@@ -378,7 +410,7 @@ def run_svdq(args, rank, world, local_rank):
     # ---------------- low-rank overhead: the same step at rank 0
     lowrank = None
     if rank == 0 and not args.no_extras:
-        layers0 = [synth.Layer(L.name, L.M, L.K, L.N, 0, L.dtype) for L in layers]
+        layers0 = [synth.Layer(L.name, L.M, L.K, L.N, 0, L.dtype, 0) for L in layers]
         built0 = build_layers(P, torch, layers0, args.fmt, dev)
         g0 = capture(built0)
         step0_ms = time_graph(g0["plain"], nrep)
@@ -443,9 +475,10 @@ def run_svdq(args, rank, world, local_rank):
         try:
             lr = []
             for (L, l32, b32), (_, l0, b0) in zip(built, built0):
-                l1 = l32.l1s.view(torch.bfloat16).reshape(L.r, L.K)
-                l2 = l32.l2s.view(torch.bfloat16).reshape(L.N, L.r)
-                lr.append((L, l0, b0, l1, l2, torch.empty(L.M, L.r, dtype=torch.bfloat16, device=dev)))
+                td = b32["x"].dtype
+                l1 = l32.l1s.view(torch.bfloat16).reshape(l32.rank, L.K).to(td)
+                l2 = l32.l2s.view(torch.bfloat16).reshape(L.N, l32.rank).to(td)
+                lr.append((L, l0, b0, l1, l2, torch.empty(L.M, l32.rank, dtype=td, device=dev)))
 
             def unfused_step():
                 for (L, l0, b0, l1, l2, xl1u) in lr:
@@ -544,7 +577,7 @@ def run_svdq(args, rank, world, local_rank):
                           "k2_us": round(float(k2_avg_s[j] * 1e6), 2),
                           "k2_tflops": round(float(k2_flops[j] / k2_avg_s[j] / 1e12), 1),
                           "k1_gbs": round(float((L.M * L.K * (2 + cbytes)
-                                                 + 2 * L.M * L.r) / k1_avg_s[j] / 1e9), 1)}
+                                                 + 2 * L.M * eff_rank(L)) / k1_avg_s[j] / 1e9), 1)}
                  for j, L in enumerate(layers)}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "k2_traffic.json")
@@ -596,10 +629,12 @@ def run_svdq(args, rank, world, local_rank):
                           "step_img_txt_grouped": round(only_ms["grouped"], 4) if only_ms["grouped"] else None,
                           "note": "each kernel's launches replayed back to back as one graph (L2 flushed before)"},
         "gpu_launches": int(launches),
-        "timing": "step captured once as a CUDA graph and replayed per step: the double block's image- and "
-                  "text-stream linears of each kind run as one grouped K1 + one grouped K2 launch (12 launches "
-                  "per step; INT4: two graph branches, 20 launches); per-kernel times from a second, serial "
-                  "graph of single launches with external timing events around each launch",
+        "timing": ("step captured once as a CUDA graph and replayed per step: the double block's image- and "
+                   "text-stream linears of each kind run as one grouped K1 + one grouped K2 launch (12 launches "
+                   "per step; INT4: two graph branches, 20 launches); per-kernel times from a second, serial "
+                   "graph of single launches with external timing events around each launch") if args.config == "flux"
+                  else ("step captured once as a CUDA graph of K1 -> K2 per linear in model order; per-kernel times "
+                        "from a second graph with external timing events around each launch"),
         "clocks": clocks,
     }
 
@@ -891,7 +926,7 @@ def run_reference(args):
     """The reference arm of this tier: the CPU oracle, as it stands, on the same workload.
     Step s = the oracle forward of `--ref-rows` tokens of linear (s mod 10) of the step, so
     every step is a bounded sample and the run ends within a few minutes."""
-    layers = flux_block_layers(args.batch)
+    layers = config_layers(args)
     rows = args.ref_rows
     for w in range(args.warmup):
         oracle_forward_time(layers, 8, args.fmt, idx={w % len(layers)})
@@ -929,6 +964,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=1024)   # ~10-30 s of oracle CPU work (weight prep is ~6 s of it)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the rank-0 overhead / library legs")
+    ap.add_argument("--config", default="flux", choices=["flux", "pixart", "sdxl"],
+                    help="BASELINE config: C4 FLUX.1 block pair (default), C2 PixArt-Sigma block, C3 SDXL + LoRA")
     ap.add_argument("--mode", default="auto", choices=["auto", "tp", "replicas"],
                     help="N > 1: tensor parallel over N (C5, default) or independent replicas")
     ap.add_argument("--tp-gather", default="nccl", choices=["nccl", "fused"],
@@ -976,10 +1013,10 @@ def main():
     out = run_svdq(args, rank, world, local_rank)
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:
-            t, f = oracle_forward_time(flux_block_layers(args.batch), args.cpu_rows, args.fmt)
+            t, f = oracle_forward_time(config_layers(args), args.cpu_rows, args.fmt)
             out["cpu_baseline"] = {"value": round(f / t / 1e12, 6), "unit": UNIT, "cores": oracle_cores(),
                                    "kind": "oracle", "host": host_info(),
-                                   "sample": f"{args.cpu_rows} tokens of each of the step's 10 linears "
+                                   "sample": f"{args.cpu_rows} tokens of each of the step's {len(config_layers(args))} linears "
                                              f"(oracle forward, fp64 NumPy/BLAS; {t:.1f} s of CPU time)"}
         print(json.dumps(out))
     if world > 1:

@@ -21,6 +21,7 @@ __device__ __forceinline__ uint32_t su32(const void *p) { return static_cast<uin
 __global__ void reset_times() { g_t0 = ~0ull; g_t1 = 0; }
 
 __global__ void __launch_bounds__(64, 1) k1x(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap ml,
+                                             const __grid_constant__ CUtensorMap ml3, const uint8_t *l1flat,
                                              int nsteps, int Q, int RT, int depth, int with_l1s, int stage_bytes) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
@@ -46,11 +47,19 @@ __global__ void __launch_bounds__(64, 1) k1x(const __grid_constant__ CUtensorMap
       }
       uint8_t *st = sm + s * stage_bytes;
       asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(tx));
-      if (with_l1s)
+      if (with_l1s == 1)
         for (int q = 0; q < Q; ++q)
           asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
                            su32(st + 16384 + q * 4096)), "l"(&ml), "r"(su32(&full[s])), "r"(((i * Q + q) * 64) % 1024), "r"(0)
                        : "memory");
+      if (with_l1s == 2)         // one contiguous bulk copy of the stage's pre-blocked L1s tiles
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         su32(st + 16384)), "l"(l1flat + ((i * Q) % 16) * 4096), "r"(Q * 4096), "r"(su32(&full[s]))
+                     : "memory");
+      if (with_l1s == 3)         // one 3-D box {64, Q, 32}
+        asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+                         su32(st + 16384)), "l"(&ml3), "r"(su32(&full[s])), "r"(0), "r"((i * Q) % 16), "r"(0)
+                     : "memory");
       asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
                        su32(st)), "l"(&mx), "r"(su32(&full[s])), "r"(0), "r"(i * Q), "r"(row0)
                    : "memory");
@@ -76,7 +85,16 @@ int main() {
   const int64_t Ks[] = {3072, 15360};
   uint16_t *l1s;
   cudaMalloc(&l1s, 32 * 1024 * 2);
-  CUtensorMap ml;
+  uint8_t *l1flat;
+  cudaMalloc(&l1flat, 32 * 4096 * 2);
+  CUtensorMap ml, ml3;
+  {
+    cuuint64_t dims[3] = {64, 16, 32};
+    cuuint64_t str[2] = {128, 2048};
+    cuuint32_t box[3] = {64, 4, 32}, es[3] = {1, 1, 1};
+    enc(&ml3, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, l1s, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   {
     cuuint64_t dims[2] = {1024, 32};
     cuuint64_t str[1] = {2048};
@@ -92,7 +110,7 @@ int main() {
     cudaMalloc(&pool, bytes * NB);
     cudaMemset(pool, 1, bytes * NB);
     struct Cfg { int RT, depth, l1s; };
-    const Cfg cfgs[] = {{32, 6, 0}, {32, 6, 1}, {32, 12, 0}, {32, 8, 0}, {32, 4, 0}, {16, 6, 0}, {64, 6, 0}, {128, 6, 0}};
+    const Cfg cfgs[] = {{32, 6, 0}, {32, 6, 1}, {32, 6, 2}, {32, 6, 3}, {32, 8, 0}, {64, 6, 0}};
     for (const Cfg &c : cfgs) {
       const int Q = 128 / c.RT;
       const int nsteps = static_cast<int>((K / 64 + Q - 1) / Q);
@@ -110,7 +128,7 @@ int main() {
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         reset_times<<<1, 1>>>();
-        k1x<<<grid, 64, stage * c.depth + 1024>>>(mx, ml, nsteps, Q, c.RT, c.depth, c.l1s, stage);
+        k1x<<<grid, 64, stage * c.depth + 1024>>>(mx, ml, ml3, l1flat, nsteps, Q, c.RT, c.depth, c.l1s, stage);
         cudaDeviceSynchronize();
         unsigned long long t0, t1;
         cudaMemcpyFromSymbol(&t0, g_t0, 8);
