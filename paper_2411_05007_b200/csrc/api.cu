@@ -6,6 +6,7 @@
 #include <cudaTypedefs.h>
 #include <cusolverDn.h>
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdio>
@@ -492,9 +493,11 @@ struct K2Prep {
   K2Maps maps;
   CUtensorMap sfa_map, sfb_map;
   bool pair;
+  int bn;                  // pair tile N (192 / 256) when `pair`
 };
 svdq_status prepare_k2(const svdq_linear *L, const uint8_t *xq, const uint8_t *xs, const uint16_t *xl1, int64_t M,
-                       void *Y, int32_t y_dtype, int64_t ldy, bool force_pair, K2Prep *out, void *y_map_base = nullptr) {
+                       void *Y, int32_t y_dtype, int64_t ldy, bool force_pair, K2Prep *out, void *y_map_base = nullptr,
+                       int pair_bn = 0) {
   svdq_status st = check_linear(L, true);
   if (st != SVDQ_OK) return st;
   if (!Y && y_map_base) Y = y_map_base;     // fused launch without a Y store: the map is never used
@@ -530,8 +533,10 @@ svdq_status prepare_k2(const svdq_linear *L, const uint8_t *xq, const uint8_t *x
   std::memset(&maps, 0, sizeof(maps));
   const bool pair = L->fmt == SVDQ_FMT_NVFP4 && (force_pair || use_pair_kernel(M, K));
   out->pair = pair;
-  const int BN = L->fmt == SVDQ_FMT_NVFP4 ? (pair ? kNvfp4PairBN : k2_nvfp4_bn(M, N)) : kInt4BN;
-  const uint32_t b_rows = pair ? kNvfp4PairBN / 2 : static_cast<uint32_t>(BN);   // B rows staged per CTA
+  // pair tile N: the caller's (grouped / fused launches share one) or this problem's own
+  out->bn = pair ? (pair_bn ? pair_bn : k2_pair_bn(N)) : 0;
+  const int BN = L->fmt == SVDQ_FMT_NVFP4 ? (pair ? out->bn : k2_nvfp4_bn(M, N)) : kInt4BN;
+  const uint32_t b_rows = pair ? static_cast<uint32_t>(BN / 2) : static_cast<uint32_t>(BN);   // B rows staged per CTA
   CUtensorMap &sfa_map = out->sfa_map, &sfb_map = out->sfb_map;
   if (L->fmt == SVDQ_FMT_NVFP4) {
     const CUtensorMapDataType ydt = y_dtype == SVDQ_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
@@ -582,7 +587,7 @@ svdq_status svdq_gemm_w4a4_lowrank_up(const svdq_linear *L, const uint8_t *xq, c
   svdq_status st = prepare_k2(L, xq, xs, xl1, M, Y, y_dtype, ldy, false, &k);
   if (st != SVDQ_OK) return st;
   cudaError_t e = L->fmt == SVDQ_FMT_NVFP4
-                      ? (k.pair ? launch_k2_nvfp4_2sm(k.maps, k.sfa_map, k.sfb_map, k.p, static_cast<cudaStream_t>(stream))
+                      ? (k.pair ? launch_k2_nvfp4_2sm(k.maps, k.sfa_map, k.sfb_map, k.p, k.bn, static_cast<cudaStream_t>(stream))
                                 : launch_k2_nvfp4(k.maps, k.p, static_cast<cudaStream_t>(stream)))
                       : launch_k2_int4(k.maps, k.p, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported) return fail(SVDQ_ERR_UNSUPPORTED, "INT4 GEMM not built");
@@ -600,11 +605,16 @@ svdq_status svdq_gemm_w4a4_lowrank_up_grouped(int32_t n, const svdq_linear *cons
   K2PairArgs g;
   std::memset(&g, 0, sizeof(g));
   g.n = n;
+  int bn = 256;                              // one tile shape per launch: 256 only if every N allows it
   for (int i = 0; i < n; ++i) {
     if (!layers[i]) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null layer %d", i);
     if (layers[i]->fmt != SVDQ_FMT_NVFP4) return fail(SVDQ_ERR_UNSUPPORTED, "grouped K2 is NVFP4 only");
+    bn = std::min(bn, k2_pair_bn(layers[i]->N));
+  }
+  g.bn = bn;
+  for (int i = 0; i < n; ++i) {
     K2Prep k;
-    svdq_status st = prepare_k2(layers[i], xq[i], xs[i], xl1[i], M[i], Y[i], y_dtype, ldy[i], true, &k);
+    svdq_status st = prepare_k2(layers[i], xq[i], xs[i], xl1[i], M[i], Y[i], y_dtype, ldy[i], true, &k, nullptr, bn);
     if (st != SVDQ_OK) return st;
     g.pr[i].a = k.maps.a;
     g.pr[i].b = k.maps.b;
@@ -669,7 +679,7 @@ svdq_status prepare_fused(int32_t n, const svdq_linear *const *layers, const uin
     K2Prep k;
     const int slots = g->pr[i].p.nx_slots;
     svdq_status st = prepare_k2(layers[i], xq[i], xs[i], xl1[i], M[i], Y[i], SVDQ_BF16, layers[i]->N, true, &k,
-                                xq_next[i]);
+                                xq_next[i], kNvfp4PairBN);
     if (st != SVDQ_OK) return st;
     g->pr[i].a = k.maps.a;
     g->pr[i].b = k.maps.b;

@@ -129,7 +129,7 @@ int k2_nvfp4_bn(int64_t M, int64_t N);   // N tile the 1-CTA NVFP4 GEMM will use
 // CTA-pair NVFP4 GEMM (256 x 192 tiles, each CTA stages 96 rows of B); SF tensor maps are
 // 3-D uint64 views [tiles128][K/64][64] of the 128x4 scale-factor layout.
 cudaError_t launch_k2_nvfp4_2sm(const K2Maps &maps, const CUtensorMap &sfa, const CUtensorMap &sfb,
-                                const K2Params &p, cudaStream_t s);
+                                const K2Params &p, int bn, cudaStream_t s);
 // Grouped form: up to kMaxGroup independent problems in one persistent launch; CTA pairs
 // walk the concatenation of the problems' tile lists.
 constexpr int kMaxGroup = 4;
@@ -144,7 +144,10 @@ struct K2PairArgs {
   int tile_begin[kMaxGroup + 1];
   int contig;             // set by the launcher: pairs take contiguous tile ranges (fused launches)
   int npairs;             // set by the launcher
+  int bn;                 // pair tile N: 192 or 256 (the B / L2s tensor maps' box rows are bn / 2)
 };
+// Pair tile N for a problem of N output columns (256 when N % 256 == 0)
+int k2_pair_bn(int64_t N);
 cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &args, cudaStream_t s);
 // SM count of the current device (cached per device ordinal; one source for every launcher
 // and for workspace sizing, so the two always agree)
@@ -156,7 +159,7 @@ int k2_pair_count(int64_t tiles);
 int k2_next_slots(int64_t n_tiles_of_problem, int64_t tiles, int npairs);
 // xl1_next[m][j] = bf16(sum over the partial slots of m's 256-row block, in slot order)
 cudaError_t launch_k2_next_reduce(const K2PairArgs &g, int i, uint16_t *xl1_next, cudaStream_t s);
-constexpr int kNvfp4PairBN = 192;
+constexpr int kNvfp4PairBN = 192;   // pair tile N of the fused (layer-boundary) launches; plain launches: k2_pair_bn
 constexpr int kInt4BN = 128;             // N tile of the INT4 GEMM
 cudaError_t launch_k2_int4(const K2Maps &maps, const K2Params &p, cudaStream_t s);
 

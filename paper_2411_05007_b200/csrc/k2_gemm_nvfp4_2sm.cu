@@ -44,13 +44,22 @@ namespace svdq {
 
 namespace {
 
-constexpr int BN = 192;                       // pair tile N
-constexpr int BNH = BN / 2;                   // B rows per CTA
+// Pair tile N: 192 (two TMEM accumulator buffers; any N) or 256 (N % 256 == 0: one accumulator
+// buffer -- TMEM holds 512 columns -- measured as fast as double buffering at N = 192, and the
+// larger tile reads 17 % fewer shared-memory bytes per FLOP and issues 25 % fewer MMAs).
 constexpr int A_BYTES = 128 * 128;            // 16 KB
-constexpr int B_BYTES = BNH * 128;            // 12 KB
 constexpr int SFA_BYTES = 2048;
 constexpr int SFB_BYTES = 4096;               // two 128-row atoms x 4 K-blocks
-constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;   // 34 KB
+template <int kBN>
+struct PC {
+  static constexpr int BN = kBN;
+  static constexpr int BNH = kBN / 2;                       // B rows per CTA
+  static constexpr int B_BYTES = BNH * 128;                 // 12 / 16 KB
+  static constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;   // 34 / 38 KB
+  static constexpr int ACC = kBN == 256 ? 1 : 2;            // accumulator buffers
+  static constexpr int SF_BASE = ACC * kBN;
+};
+constexpr int BN = 192;                       // the fused (layer-boundary) variant's tile N
 #ifndef SVDQ_K2P_STAGES
 #define SVDQ_K2P_STAGES 5
 #endif
@@ -76,24 +85,21 @@ constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;   // 34 KB
 constexpr int kStages = SVDQ_K2P_STAGES;
 constexpr int kEpiBuf = SVDQ_K2P_EPIBUF;      // 2 KB staging buffers per epilogue warp
 constexpr int SF_COLS = 48;
-constexpr int SF_BASE = 2 * BN;
 #ifndef SVDQ_BIGSTORE
 #define SVDQ_BIGSTORE 0
 #endif
-constexpr int EPI_OFF = kStages * STAGE;                 // epilogue staging
 // 16-bit Y with SVDQ_BIGSTORE: three [128 rows x 64 cols] SW128 blocks, one TMA store each;
 // otherwise (and for fp32 Y) 8 warps x kEpiBuf 2 KB chunks
 constexpr int EPI_BYTES = SVDQ_BIGSTORE && 3 * 16384 > 8 * 2048 * kEpiBuf ? 3 * 16384 : 8 * 2048 * kEpiBuf;
-constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
-constexpr int SMEM = BAR_OFF + 256 + BN * 4 + 1024;
 // Shared-memory layout per variant.  Fused launches (layer-boundary fusion) run a 4-stage ring
 // and add the tile's lambda_inv_next [192] fp32, the a tile (3 x [128 rows x 128 B], SW128) and
 // this CTA's half of the L1s_next rows (3 x [r/2 rows x 128 B], SW128) for the X L1s_next^T MMA.
-template <bool kFuse>
+template <bool kFuse, int kBN = 192>
 struct Lay {
+  static constexpr int BN = kBN;
   static constexpr int stages = kFuse ? 3 : kStages;
   static constexpr int epi_w = kFuse ? 12 : SVDQ_K2P_EPIW;  // epilogue warps (2 or 3 per TMEM lane quadrant)
-  static constexpr int epi_off = stages * STAGE;
+  static constexpr int epi_off = stages * PC<kBN>::STAGE;
   static constexpr int bar_off = epi_off + (epi_w != 8 ? epi_w * 2048 * kEpiBuf : EPI_BYTES);
   static constexpr int bias_off = bar_off + 256;
   static constexpr int lamn_off = bias_off + BN * 4;
@@ -103,10 +109,10 @@ struct Lay {
   static constexpr int sfs_off = cs_off + 128 * 96;         // next-layer scale factors, 3 x 512 B
   static constexpr int smem = kFuse ? sfs_off + 3 * 512 + 1024 : bias_off + BN * 4 + 1024;
 };
-constexpr int XL1_COL = SF_BASE + 2 * SF_COLS;   // TMEM columns [480, 512): X L1s_next^T accumulator
+constexpr int XL1_COL = PC<192>::SF_BASE + 2 * SF_COLS;   // TMEM columns [480, 512): X L1s_next^T accumulator
 static_assert(XL1_COL + 32 <= 512, "TMEM budget (fused)");
-static_assert(STAGE % 1024 == 0, "stage alignment");
-static_assert(SF_BASE + 2 * SF_COLS <= 512, "TMEM budget");
+static_assert(PC<192>::STAGE % 1024 == 0 && PC<256>::STAGE % 1024 == 0, "stage alignment");
+static_assert(PC<192>::SF_BASE + 2 * SF_COLS <= 512 && PC<256>::SF_BASE + 2 * SF_COLS <= 512, "TMEM budget");
 
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -141,6 +147,7 @@ struct TileRef {
   int i;
   int64_t m0, n0;
 };
+template <int BN = 192>
 __device__ __forceinline__ TileRef locate(const K2PairArgs &g, int t) {
   int i = 0;
   while (i + 1 < g.n && t >= g.tile_begin[i + 1]) ++i;
@@ -153,13 +160,16 @@ __device__ __forceinline__ TileRef locate(const K2PairArgs &g, int t) {
   return TileRef{i, static_cast<int64_t>(lt % mt) * 256, static_cast<int64_t>(lt / mt) * BN};
 }
 
-template <bool kFuse>
+template <bool kFuse, int kBN>
 __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
     k2_nvfp4_2sm_kernel(const __grid_constant__ K2PairArgs g) {
+  constexpr int BN = kBN, BNH = PC<kBN>::BNH, B_BYTES = PC<kBN>::B_BYTES, STAGE = PC<kBN>::STAGE;
+  constexpr int SF_BASE = PC<kBN>::SF_BASE, ACC = PC<kBN>::ACC;
+  static_assert(!kFuse || kBN == 192, "the fused variant runs 192-wide tiles");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~static_cast<uintptr_t>(1023));
-  using LY = Lay<kFuse>;
+  using LY = Lay<kFuse, kBN>;
   constexpr int kSt = LY::stages;
   constexpr int kEpiW = LY::epi_w, kNWQ = kEpiW / 4, kEpiT = 32 * kEpiW;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + LY::bar_off);
@@ -230,9 +240,9 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
 #endif
       // Weight tiles (B, SFB) of the first tile's first ring do not depend on K1: issue them
       // before the programmatic dependency resolves, so they land while K1 finishes.
-      const int pre = (SVDQ_EXP & 4) || t_first >= t_end ? 0 : min(kSt, nkt_of(locate(g, t_first).i));
+      const int pre = (SVDQ_EXP & 4) || t_first >= t_end ? 0 : min(kSt, nkt_of(locate<kBN>(g, t_first).i));
       if (pre) {
-        const TileRef tr = locate(g, t_first);
+        const TileRef tr = locate<kBN>(g, t_first);
         const K2PairProblem &pr = g.pr[tr.i];
         for (int kt = 0; kt < pre; ++kt) {
           uint8_t *st = smem + kt * STAGE;
@@ -246,7 +256,7 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
       griddep_wait();                                    // xq / xs / xl1 come from K1
       bool first = true;
       for (int t = t_first; t < t_end; t += t_step) {
-        const TileRef tr = locate(g, t);
+        const TileRef tr = locate<kBN>(g, t);
         const K2PairProblem &pr = g.pr[tr.i];
         const int nkt = nkt_of(tr.i);
         const int nslab = nslab_of(tr.i);
@@ -310,7 +320,7 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
       bool xl_prev_first = false;
       uint32_t xa_ph = 0;
       auto issue_xl1 = [&](int tp, bool first) {
-        const int r = g.pr[locate(g, tp).i].p.nx_r;
+        const int r = g.pr[locate<kBN>(g, tp).i].p.nx_r;
         mbar_wait(xa_full, xa_ph);
         xa_ph ^= 1;
         tc_fence_after();
@@ -327,9 +337,10 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
         __syncwarp();
       };
       for (int t = t_first; t < t_end; t += t_step, ++acc_i) {
-        const int b = (SVDQ_EXP & 64) ? 0 : acc_i & 1;            // 64: single accumulator (ablation)
-        const uint32_t acc_ph = (SVDQ_EXP & 64) ? acc_i & 1 : (acc_i >> 1) & 1;
-        const TileRef tr = locate(g, t);
+        const bool single = (SVDQ_EXP & 64) || ACC == 1;          // 64: single accumulator (ablation)
+        const int b = single ? 0 : acc_i & 1;
+        const uint32_t acc_ph = single ? acc_i & 1 : (acc_i >> 1) & 1;
+        const TileRef tr = locate<kBN>(g, t);
         const int64_t n0 = tr.n0;
         const int nkb64 = static_cast<int>(g.pr[tr.i].p.K / 64);
         const int nkt = nkt_of(tr.i);
@@ -416,7 +427,7 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
           if (xl_prev >= 0) issue_xl1(xl_prev, xl_prev_first);
           const K2Params &pt = g.pr[tr.i].p;
           if (pt.fuse && pt.nx_r > 0) {
-            xl_prev_first = t == t_first || locate(g, t - t_step).i != tr.i || locate(g, t - t_step).m0 != tr.m0;
+            xl_prev_first = t == t_first || locate<kBN>(g, t - t_step).i != tr.i || locate<kBN>(g, t - t_step).m0 != tr.m0;
             xl_prev = t;
           } else {
             xl_prev = -1;
@@ -448,9 +459,10 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
 #endif
     griddep_wait();
     for (int t = t_first; t < t_end; t += t_step, ++acc_i) {
-      const int b = (SVDQ_EXP & 64) ? 0 : acc_i & 1;
-      const uint32_t acc_ph = (SVDQ_EXP & 64) ? acc_i & 1 : (acc_i >> 1) & 1;
-      const TileRef tr = locate(g, t);
+      const bool single = (SVDQ_EXP & 64) || ACC == 1;
+      const int b = single ? 0 : acc_i & 1;
+      const uint32_t acc_ph = single ? acc_i & 1 : (acc_i >> 1) & 1;
+      const TileRef tr = locate<kBN>(g, t);
       const K2Params &p = g.pr[tr.i].p;
       const CUtensorMap *tmY = &g.pr[tr.i].y;
       const int64_t m0 = tr.m0 + 128 * crank;
@@ -515,7 +527,7 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
       continue;
 #endif
 #if SVDQ_BIGSTORE
-      if (p.y_dtype != 2) {
+      if (kBN == 192 && p.y_dtype != 2) {
         // drain the 3 column chunks of this warp, release the accumulator, then each 64-column
         // block of the CTA's 128 x 192 tile is assembled by all 8 warps and stored by one TMA op
         const int sub = (warp - 2) >> 2;
@@ -588,7 +600,7 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
             // TMEM once the MMAs of this tile are done, and write them to this pair's slot
             bool flush = t + t_step >= t_end;
             if (!flush) {
-              const TileRef nr = locate(g, t + t_step);
+              const TileRef nr = locate<kBN>(g, t + t_step);
               flush = nr.i != tr.i || nr.m0 != tr.m0;
             }
             if (flush) {
@@ -641,29 +653,46 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
 }  // namespace
 
 cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
-  static_assert(SMEM <= 227 * 1024 && Lay<false>::smem <= 227 * 1024, "smem budget");
+  static_assert(Lay<false, 192>::smem <= 227 * 1024 && Lay<false, 256>::smem <= 227 * 1024, "smem budget");
   static_assert(Lay<true>::smem <= 227 * 1024, "smem budget (fused)");
-  cudaError_t e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       Lay<false>::smem);
-  if (e != cudaSuccess) return e;
-  g.tile_begin[0] = 0;
   bool fuse = false;
-  for (int i = 0; i < g.n; ++i) {
-    g.tile_begin[i + 1] = g.tile_begin[i] + static_cast<int>(((g.pr[i].p.M + 255) / 256) * ((g.pr[i].p.N + BN - 1) / BN));
-    fuse = fuse || g.pr[i].p.fuse;
-  }
+  for (int i = 0; i < g.n; ++i) fuse = fuse || g.pr[i].p.fuse;
+  const int bn = fuse ? 192 : (g.bn == 256 ? 256 : 192);
+  g.bn = bn;
+  g.tile_begin[0] = 0;
+  for (int i = 0; i < g.n; ++i)
+    g.tile_begin[i + 1] = g.tile_begin[i] + static_cast<int>(((g.pr[i].p.M + 255) / 256) * ((g.pr[i].p.N + bn - 1) / bn));
   const int64_t tiles = g.tile_begin[g.n];
   const int64_t pairs = k2_pair_count(tiles);
   static const int force_contig = [] { const char *e = std::getenv("SVDQ_K2_CONTIG"); return e ? std::atoi(e) : 0; }();
   g.contig = (fuse || force_contig) ? 1 : 0;      // SVDQ_K2_CONTIG=1: schedule ablation
   g.npairs = static_cast<int>(pairs);
+  cudaError_t e;
   if (fuse) {
-    e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay<true>::smem);
+    e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<true, 192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Lay<true>::smem);
     if (e != cudaSuccess) return e;
-    return launch_ex(k2_nvfp4_2sm_kernel<true>, dim3(static_cast<unsigned>(2 * pairs)), dim3(448), Lay<true>::smem, s, 2u, g);
+    return launch_ex(k2_nvfp4_2sm_kernel<true, 192>, dim3(static_cast<unsigned>(2 * pairs)), dim3(448),
+                     Lay<true>::smem, s, 2u, g);
   }
-  return launch_ex(k2_nvfp4_2sm_kernel<false>, dim3(static_cast<unsigned>(2 * pairs)), dim3(64 + 32 * SVDQ_K2P_EPIW),
-                   Lay<false>::smem, s, 2u, g);
+  if (bn == 256) {
+    e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Lay<false, 256>::smem);
+    if (e != cudaSuccess) return e;
+    return launch_ex(k2_nvfp4_2sm_kernel<false, 256>, dim3(static_cast<unsigned>(2 * pairs)),
+                     dim3(64 + 32 * SVDQ_K2P_EPIW), Lay<false, 256>::smem, s, 2u, g);
+  }
+  e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<false, 192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           Lay<false, 192>::smem);
+  if (e != cudaSuccess) return e;
+  return launch_ex(k2_nvfp4_2sm_kernel<false, 192>, dim3(static_cast<unsigned>(2 * pairs)),
+                   dim3(64 + 32 * SVDQ_K2P_EPIW), Lay<false, 192>::smem, s, 2u, g);
+}
+
+int k2_pair_bn(int64_t N) {
+  static const int force = [] { const char *e = std::getenv("SVDQ_K2_BN"); return e ? std::atoi(e) : 0; }();
+  if (force == 192) return 192;                 // SVDQ_K2_BN=192: A/B against the 192-wide tile
+  return N % 256 == 0 ? 256 : 192;
 }
 
 int device_sm_count() {
@@ -715,10 +744,11 @@ cudaError_t launch_k2_next_reduce(const K2PairArgs &g, int i, uint16_t *xl1_next
 }
 
 cudaError_t launch_k2_nvfp4_2sm(const K2Maps &maps, const CUtensorMap &sfa, const CUtensorMap &sfb,
-                                const K2Params &p, cudaStream_t s) {
+                                const K2Params &p, int bn, cudaStream_t s) {
   K2PairArgs g;                              // host staging, copied into the launch parameters
   static_assert(sizeof(K2PairArgs) < 30 * 1024, "kernel parameter space");
   g.n = 1;
+  g.bn = bn;
   g.pr[0].a = maps.a;
   g.pr[0].b = maps.b;
   g.pr[0].xl1 = maps.xl1;

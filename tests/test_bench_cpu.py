@@ -24,6 +24,6 @@ def test_reference_arm_json_line():
     sys.path.insert(0, ROOT)
     import bench
     import argparse
-    args = argparse.Namespace(batch=1, fmt="nvfp4")
+    args = argparse.Namespace(batch=1, fmt="nvfp4", config="flux")
     assert d["config"] == bench.bench_config(args, 1)      # same workload description as the GPU arm
     assert d["metric"] == bench.METRIC
