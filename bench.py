@@ -184,6 +184,103 @@ def flux_step_grouped(P, bl, st, ev1=None, ev2=None, launch_groups=None):
                 launch_groups.append([L])
 
 
+def _nbytes(t):
+    return 0 if t is None else t.numel() * t.element_size()
+
+
+def b2b_slope(torch, stream, l2_flush, nrep, launch, copies):
+    """Seconds per launch of `launch(j)` (j = copy index): CUDA events on `stream` around graphs of
+    R and 2R back-to-back launches cycling over the copies, L2 flushed before each replay;
+    (median t_2R - median t_R) / R."""
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    R = max(8, copies)
+    graphs = []
+    for n in (R, 2 * R):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=stream):
+            for j in range(n):
+                launch(j % copies)
+        graphs.append(gr)
+    t = [[], []]
+    for _ in range(nrep):
+        for k, gr in enumerate(graphs):
+            a, b = ev(), ev()
+            with torch.cuda.stream(stream):
+                l2_flush()
+                a.record(stream)
+                gr.replay()
+                b.record(stream)
+            torch.cuda.synchronize()
+            t[k].append(a.elapsed_time(b))
+    return (float(np.median(t[1])) - float(np.median(t[0]))) / R / 1e3
+
+
+def b2b_cold_durations(P, torch, units, stream, l2_flush, nrep, l2_bytes=126 << 20):
+    """Per-launch durations of each unit's K1 and K2 launch, back to back and DRAM-cold.
+
+    A unit is the list of (Layer, QuantizedLinear, buffers) one launch covers (a grouped launch or a
+    single linear).  For each kernel: C copies of everything the launch reads (K1: X; K2: codes,
+    scale factors, L2s, xq / xs / xl1), C chosen so the copies span >= 3x the 126 MB L2, so every
+    launch reads its operands from DRAM as in the flushed step.  Two CUDA graphs of R and 2R
+    launches cycling over the copies are timed with CUDA events on the launch stream (L2 flushed
+    before each replay); duration = (t_2R - t_R) / R, which removes the graph-launch and event
+    overhead of a replay and keeps what the step keeps: launches queued back to back (PDL lets a
+    launch's prologue overlap its predecessor's tail, as between K1 and K2 in the step)."""
+    import math
+
+    def slope(launch, copies):
+        return b2b_slope(torch, stream, l2_flush, nrep, launch, copies)
+
+    out = []
+    for unit in units:
+        grouped = len(unit) > 1
+        # ---- K1: copies of X
+        xin = sum(_nbytes(b["x"]) for (_, _, b) in unit)
+        c1 = int(min(16, max(2, math.ceil(3 * l2_bytes / xin))))
+        xc = [[b["x"].clone() for (_, _, b) in unit] for _ in range(c1)]
+
+        def k1(j):
+            if grouped:
+                P.svdq_quantize_act_lowrank_down_grouped([u[1] for u in unit], xc[j], [u[2]["xq"] for u in unit],
+                                                         [u[2]["xs"] for u in unit], [u[2]["xl1"] for u in unit],
+                                                         stream=stream)
+            else:
+                (L, layer, b), = unit
+                P.svdq_quantize_act_lowrank_down(layer, xc[j][0], b["xq"], b["xs"], b["xl1"], stream=stream)
+        with torch.cuda.stream(stream):
+            k1(0)
+        torch.cuda.synchronize()
+        t1 = slope(k1, c1)
+        del xc
+        # ---- K2: copies of the weights and of K1's outputs
+        win = sum(_nbytes(l.w_codes) + _nbytes(l.w_scales) + _nbytes(l.l2s) + _nbytes(b["xq"]) + _nbytes(b["xs"])
+                  + _nbytes(b["xl1"]) for (_, l, b) in unit)
+        c2 = int(min(16, max(2, math.ceil(3 * l2_bytes / win))))
+        cp = []
+        for _ in range(c2):
+            cp.append([(P.QuantizedLinear(l.fmt, l.K, l.N, l.rank, l.w_codes.clone(), l.w_scales.clone(),
+                                          l.lambda_inv, l.l1s, l.l2s.clone(), l.bias, l.scale_dtype, l.gs_w, l.gs_x),
+                        b["xq"].clone(), b["xs"].clone(), b["xl1"].clone()) for (_, l, b) in unit])
+
+        def k2(j):
+            c = cp[j]
+            if grouped:
+                P.svdq_gemm_w4a4_lowrank_up_grouped([e[0] for e in c], [e[1] for e in c], [e[2] for e in c],
+                                                    [e[3] for e in c], [u[0].M for u in unit],
+                                                    [u[2]["y"] for u in unit], stream=stream)
+            else:
+                (L, _, b), = unit
+                P.svdq_gemm_w4a4_lowrank_up(c[0][0], c[0][1], c[0][2], c[0][3], L.M, Y=b["y"], stream=stream)
+        with torch.cuda.stream(stream):
+            k2(0)
+        torch.cuda.synchronize()
+        t2 = slope(k2, c2)
+        del cp
+        torch.cuda.empty_cache()
+        out.append((t1, t2))
+    return out
+
+
 # ------------------------------------------------------------------ svdq arm
 def build_layers(P, torch, layers, fmt, dev, quality=None, seed_index=None):
     """Synthetic FLUX-shaped layers (DESIGN.md input recipe), weights prepared on the GPU
@@ -403,6 +500,11 @@ def run_svdq(args, rank, world, local_rank):
             r2.append([a.elapsed_time(b) for a, b in g["gk2_ev"]])
         launch_k1_s = np.array(r1).mean(axis=0) / 1e3
         launch_k2_s = np.array(r2).mean(axis=0) / 1e3
+    # back-to-back DRAM-cold durations of the step's own launches (the roofline's denominators)
+    by_name = {L.name: (L, layer, b) for (L, layer, b) in built}
+    units = ([[by_name[L.name] for L in grp] for grp in launch_groups] if g["grouped"] is not None
+             else [[e] for e in built])
+    b2b = b2b_cold_durations(P, torch, units, stream, l2_flush, nrep)
     only_ms = {"k1": time_graph(g["k1"], nrep), "k2": time_graph(g["k2"], nrep),
                "serial": time_graph(g["plain"], nrep), "dag": time_graph(g["dag"], nrep),
                "grouped": time_graph(g["grouped"], nrep) if g["grouped"] is not None else None}
@@ -421,9 +523,16 @@ def run_svdq(args, rank, world, local_rank):
             "def": "[t_step(r=32) - t_step(r=0)] / t_K2-only(r=0), CUDA-graph replays, L2 flushed "
                    "(SURVEY 8(d): [t_K1(r)+t_K2(r)-t_K1(0)-t_K2(0)] / t_K2(0))",
             "step_ms_r32": round(step_r_ms, 4), "step_ms_r0": round(step0_ms, 4),
-            "per_layer": {L.name: round(float((k1_avg_s[j] + k2_avg_s[j] - k1_0[j] - k2_0[j]) / k2_0[j]), 4)
-                          for j, L in enumerate(layers)},
+            "per_layer_isolated": {L.name: round(float((k1_avg_s[j] + k2_avg_s[j] - k1_0[j] - k2_0[j]) / k2_0[j]), 4)
+                                   for j, L in enumerate(layers)},
         }
+        # per launch of the step, from back-to-back DRAM-cold durations (b2b_cold_durations)
+        by0 = {L.name: (L, layer, b) for (L, layer, b) in built0}
+        b2b0 = b2b_cold_durations(P, torch, [[by0[u[0].name] for u in unit] for unit in units], stream, l2_flush, nrep)
+        lowrank["per_launch"] = {"+".join(u[0].name for u in unit): round((t1 + t2 - z1 - z2) / z2, 4)
+                                 for unit, (t1, t2), (z1, z2) in zip(units, b2b, b2b0)}
+        lowrank["per_launch_def"] = ("[t_K1(r) + t_K2(r) - t_K1(0) - t_K2(0)] / t_K2(0) per launch of the step, "
+                                     "back-to-back DRAM-cold durations")
         # ---------------- library context: cuBLASLt NVFP4 GEMM alone on the rank-0 operands
         library = None
         if args.fmt == "nvfp4" and hasattr(torch, "float4_e2m1fn_x2"):
@@ -459,13 +568,27 @@ def run_svdq(args, rank, world, local_rank):
                     rows.append([a.elapsed_time(b) for a, b in lev])
                 lib_s = np.array(rows).mean(axis=0) / 1e3
                 k2f = np.array([2.0 * L.M * L.N * L.K for L in layers])
+                # the same back-to-back DRAM-cold method as K2's roofline durations, per layer
+                import math
+                lib_b2b = []
+                for (fa, fbt, sa, sb, y) in mm:
+                    nb = _nbytes(fa) + _nbytes(fbt) + _nbytes(sa) + _nbytes(sb)
+                    c = int(min(16, max(2, math.ceil(3 * (126 << 20) / nb))))
+                    cps = [(fa.clone(), fbt.t().clone().t(), sa.clone(), sb.clone()) for _ in range(c)]
+                    lib_b2b.append(b2b_slope(torch, stream, l2_flush, nrep,
+                                             lambda j, cps=cps, y=y: torch._scaled_mm(*cps[j], out_dtype=torch.bfloat16),
+                                             c))
+                    del cps
+                lib_b2b = np.array(lib_b2b)
                 library = {
                     "kernel": "cuBLASLt block-scaled NVFP4 GEMM (torch._scaled_mm), plain Q(X)Q(W) only: "
                               "no smoothing, quantization, low-rank branch or bias",
-                    "tflops": round(float(k2f.sum() / lib_s.sum() / 1e12), 1),
-                    "k2_r0_tflops": round(float(k2f.sum() / k2_0.sum() / 1e12), 1),
-                    "per_layer_tflops": {L.name: round(float(k2f[j] / lib_s[j] / 1e12), 1)
+                    "tflops": round(float(k2f.sum() / lib_b2b.sum() / 1e12), 1),
+                    "tflops_def": "per-layer back-to-back DRAM-cold durations (bench.b2b_slope), as K2's roofline",
+                    "per_layer_tflops": {L.name: round(float(k2f[j] / lib_b2b[j] / 1e12), 1)
                                          for j, L in enumerate(layers)},
+                    "tflops_isolated": round(float(k2f.sum() / lib_s.sum() / 1e12), 1),
+                    "k2_r0_tflops_isolated": round(float(k2f.sum() / k2_0.sum() / 1e12), 1),
                 }
             except Exception as e:  # noqa: BLE001  (context only; never part of the product path)
                 library = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
@@ -560,17 +683,22 @@ def run_svdq(args, rank, world, local_rank):
     fp4_sus = ratio * pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     fp4_burst = ratio * pk["bf16_tflops"]
     k2_flops = np.array([2.0 * L.M * L.N * L.K for L in layers])
-    k2_t = launch_k2_s.sum() if launch_k2_s is not None else k2_avg_s.sum()
-    k1_t = launch_k1_s.sum() if launch_k1_s is not None else k1_avg_s.sum()
+    k2_t = float(sum(t2 for _, t2 in b2b))
+    k1_t = float(sum(t1 for t1, _ in b2b))
     k2_achieved = float(k2_flops.sum() / k2_t / 1e12)
     k1_gbs = float(k1_bytes / k1_t / 1e9)
-    per_launch = None
-    if launch_k2_s is not None:
-        per_launch = []
-        for grp, t1, t2 in zip(launch_groups, launch_k1_s, launch_k2_s):
-            fl = sum(2.0 * L.M * L.N * L.K for L in grp)
-            per_launch.append({"layers": [L.name for L in grp], "k1_us": round(float(t1 * 1e6), 2),
-                               "k2_us": round(float(t2 * 1e6), 2), "k2_tflops": round(float(fl / t2 / 1e12), 1)})
+    iso_k2 = launch_k2_s.sum() if launch_k2_s is not None else k2_avg_s.sum()
+    iso_k1 = launch_k1_s.sum() if launch_k1_s is not None else k1_avg_s.sum()
+    per_launch = []
+    iso = (list(zip(launch_k1_s, launch_k2_s)) if launch_k2_s is not None
+           else list(zip(k1_avg_s, k2_avg_s)))
+    for unit, (t1, t2), (i1, i2) in zip(units, b2b, iso):
+        fl = sum(2.0 * u[0].M * u[0].N * u[0].K for u in unit)
+        by = sum(u[0].M * u[0].K * (2 + cbytes) + 2 * u[0].M * eff_rank(u[0]) for u in unit)
+        per_launch.append({"layers": [u[0].name for u in unit], "k1_us": round(t1 * 1e6, 2),
+                           "k2_us": round(t2 * 1e6, 2), "k2_tflops": round(fl / t2 / 1e12, 1),
+                           "k1_gbs": round(by / t1 / 1e9, 1),
+                           "k1_us_isolated": round(float(i1 * 1e6), 2), "k2_us_isolated": round(float(i2 * 1e6), 2)})
     value = world * flops * args.steps / (total_ms / 1e3) / 1e12
     per_layer = {L.name: {"M": L.M, "K": L.K, "N": L.N,
                           "k1_us": round(float(k1_avg_s[j] * 1e6), 2),
@@ -609,11 +737,21 @@ def run_svdq(args, rank, world, local_rank):
                      "frac_vs_clock_peak": round(k2_achieved * 1e12 / (148 * 8192 * ratio * f_sm), 4),
                      "clock_peak_def": f"148 SMs x {int(8192 * ratio)} dense FLOP/clk ({args.fmt}) x median SM clock "
                                        "of the timed region",
-                     "achieved_def": "sum 2*M*N*K over the step's linears / sum of the step's K2 launch durations "
-                                     "(CUDA events around each launch of the step's own launch sequence)"},
+                     "achieved_def": "sum 2*M*N*K over the step's linears / sum of the step's K2 launch durations; "
+                                     "each duration = CUDA events (launch stream) around graphs of R and 2R "
+                                     "back-to-back launches of that launch on DRAM-cold operand copies, "
+                                     "(t_2R - t_R) / R (bench.b2b_cold_durations)",
+                     "achieved_isolated": round(float(k2_flops.sum() / iso_k2 / 1e12), 1),
+                     "isolated_def": "same FLOPs / durations from events around each single launch of the step "
+                                     "sequence (includes each launch's event + launch gap)"},
         "k1": {"bound": "hbm", "achieved": round(k1_gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                "frac": round(k1_gbs / pk["hbm_gbs"], 4),
-               "achieved_def": "sum (2MK + 0.5625MK + 2Mr) / sum of K1 durations"},
+               "achieved_def": "sum (2MK + c MK + 2Mr) / sum of K1 launch durations (back-to-back DRAM-cold, "
+                               "as for K2)",
+               "achieved_isolated": round(float(k1_bytes / iso_k1 / 1e9), 1)},
+        "kernel_sum_ms": {"k1": round(k1_t * 1e3, 4), "k2": round(k2_t * 1e3, 4),
+                          "total": round((k1_t + k2_t) * 1e3, 4),
+                          "note": "sum of the back-to-back per-launch durations; compare with ms_per_step"},
         "lowrank_overhead": lowrank,
         "quality_rel_err_vs_fp64_XW": {"note": "unscored sanity metric: ||XW + b - Y|| / ||XW + b||, 64 rows per "
                                                "linear, synthetic outlier activations (SURVEY 8(d))", **quality},

@@ -84,8 +84,11 @@ struct K1Args {
 // 3-D view {64 cols, K/64 blocks, M rows} with box {64, 128/rt, rt}, L1s box {64, rank}, lambda_inv
 // as [K/32][32] with box {32, 2 * 128/rt}.  bf16 or fp16 X.
 struct K1RowLayout {
-  int rt, q, x_bytes, l1_bytes, stage_bytes, stages;
-  size_t bar_off, smem;
+  int rt, q;
+  int x_bytes;            // X tile bytes of an X stage (fp16 X: + the bf16 low-part tile)
+  int stage_bytes, stages;    // X ring: X tile + the Q blocks' lambda_inv
+  int l1_bytes, wstages;      // L1s ring: the Q blocks' L1s tiles (rank > 0)
+  size_t w_off, bar_off, smem;
 };
 K1RowLayout k1_row_layout(int rt, int rank, bool x16);
 int k1_rows_rt(int64_t rows_total, int rank);            // row tile for `rows_total` padded rows

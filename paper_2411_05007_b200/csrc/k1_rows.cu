@@ -30,20 +30,18 @@
 #include "sm100.cuh"
 
 #ifndef SVDQ_K1REXP
-#define SVDQ_K1REXP 0   // ablation bits: 1 no quantizer math / stores, 2 no MMA, 4 no L1s loads
-#endif
-#ifndef SVDQ_K1R_PF
-#define SVDQ_K1R_PF 0   // 1: quantizer lanes L2-prefetch X S + 2 stages ahead (measured slower)
+#define SVDQ_K1REXP 0   // ablation bits: 1 no quantizer math / stores, 2 no MMA, 4 no L1s loads, 8 no L1s L2 prefetch,
+                        // 16 no code / scale stores, 32 no qinv table lookup
 #endif
 
 #ifdef SVDQ_TRACE
-namespace svdq { __device__ unsigned long long g_k1r_trace[256]; }
+namespace svdq { __device__ unsigned long long g_k1r_trace[512]; }
 extern "C" int svdq_k1r_trace_read(unsigned long long *host) {
-  return cudaMemcpyFromSymbol(host, svdq::g_k1r_trace, sizeof(unsigned long long) * 256) == cudaSuccess ? 0 : 1;
+  return cudaMemcpyFromSymbol(host, svdq::g_k1r_trace, sizeof(unsigned long long) * 512) == cudaSuccess ? 0 : 1;
 }
 __device__ __forceinline__ unsigned long long k1r_gtime() {
   unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
   return t;
 }
 #define RTRACE(slot) \
@@ -56,8 +54,31 @@ namespace svdq {
 
 namespace {
 
+// Waits of the single-thread roles (producers, MMA issuer).  They share the SM sub-partitions'
+// issue slots with quantizer warps, so they wait with the suspend-time hint (the warp is parked
+// until the phase completes) instead of spinning: measured, the quantizer warps that shared a
+// scheduler with a spinning role warp fell ~3 stages behind the others over K = 15360, and the
+// slowest quantizer warp gates every slot release.
+#ifndef SVDQ_K1_SPIN
+#define SVDQ_K1_SPIN 0
+#endif
+__device__ __forceinline__ void role_wait(uint64_t *bar, uint32_t parity) {
+  if (SVDQ_K1_SPIN) mbar_wait_spin(bar, parity);
+  else mbar_wait(bar, parity);
+}
+
 constexpr int kQuantWarps = 16;
-constexpr int kThreads = 32 * (2 + kQuantWarps);
+constexpr int kQ0 = 3;                                 // first quantizer warp (0 X producer, 1 MMA, 2 L1s producer)
+constexpr int kThreads = 32 * (kQ0 + kQuantWarps);
+constexpr int kMaxXStages = 12;
+constexpr int kMaxWStages = 4;
+#ifndef SVDQ_K1_SW
+#define SVDQ_K1_SW 4                                   // L1s ring depth (the tiles come from L2)
+#endif
+static_assert(SVDQ_K1_SW >= 2 && SVDQ_K1_SW <= kMaxWStages, "L1s ring depth");
+#ifndef SVDQ_K1_LAMPRE
+#define SVDQ_K1_LAMPRE 2                               // ring slots whose lambda tile goes out before griddepcontrol.wait
+#endif
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
@@ -115,26 +136,26 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *map, int32_t c0, int32_t c1, int32_t c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
-}
 
 }  // namespace
 
 K1RowLayout k1_row_layout(int rt, int rank, bool x16) {
+  // Two rings: X stages (the DRAM stream: X tile + the Q blocks' lambda_inv) and L1s stages (Q
+  // tiles [r x 64], L2-resident).  Splitting them lets the X ring run deeper than the L1s ring --
+  // the L1s tiles of a stage are as large as its X tile at RT = 32, r = 32, and only the X bytes
+  // need to be in flight long enough to cover the DRAM latency.
   K1RowLayout L;
   L.rt = rt;
   L.q = 128 / rt;
   L.x_bytes = x16 ? 32768 : 16384;                   // fp16 X: + the bf16 low parts (hi stays in place)
-  L.l1_bytes = L.q * rank * 128;
-  L.stage_bytes = (L.x_bytes + L.l1_bytes + L.q * 256 + 1023) / 1024 * 1024;
-  int s = (200 * 1024) / L.stage_bytes;
-  L.stages = s > 8 ? 8 : (s < 2 ? 2 : s);
-  L.bar_off = static_cast<size_t>(L.stages) * L.stage_bytes;
-  L.smem = L.bar_off + 256 + 1024 + 1024;            // barriers, 256-entry qinv table, alignment slack
+  L.stage_bytes = (L.x_bytes + L.q * 256 + 1023) / 1024 * 1024;
+  L.l1_bytes = L.q * rank * 128;                     // multiple of 2 KB (rank % 16 == 0)
+  L.wstages = rank ? SVDQ_K1_SW : 0;
+  const int s = (212 * 1024 - L.wstages * L.l1_bytes) / L.stage_bytes;
+  L.stages = s > kMaxXStages ? kMaxXStages : (s < 2 ? 2 : s);
+  L.w_off = static_cast<size_t>(L.stages) * L.stage_bytes;
+  L.bar_off = L.w_off + static_cast<size_t>(L.wstages) * L.l1_bytes;
+  L.smem = L.bar_off + 512 + 1024 + 1024;            // barriers, 256-entry qinv table, alignment slack
   return L;
 }
 
@@ -150,13 +171,16 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
   const K1Params &p = g.pr[pi].p;
   const CUtensorMap &tmX = g.pr[pi].x, &tmL = g.pr[pi].l1s, &tmLam = g.pr[pi].lam;
   const int r = p.rank;
-  const int RT = Ly.rt, Q = Ly.q, S = Ly.stages;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + Ly.bar_off);
-  uint64_t *empty = full + 8;
-  uint64_t *conv = empty + 8;                                  // fp16 X: hi / lo tiles written
-  uint64_t *dfull = conv + 8;
+  const int RT = Ly.rt, Q = Ly.q, S = Ly.stages, SW = Ly.wstages;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + Ly.bar_off);   // X ring
+  uint64_t *empty = full + kMaxXStages;
+  uint64_t *conv = empty + kMaxXStages;                        // fp16 X: hi / lo tiles written
+  uint64_t *wfull = conv + kMaxXStages;                        // L1s ring
+  uint64_t *wempty = wfull + kMaxWStages;
+  uint64_t *dfull = wempty + kMaxWStages;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dfull + 1);
-  float *qinv_lut = reinterpret_cast<float *>(smem + Ly.bar_off + 256);
+  float *qinv_lut = reinterpret_cast<float *>(smem + Ly.bar_off + 512);
+  uint8_t *wring = smem + Ly.w_off;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -168,23 +192,27 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
   while (tcols < static_cast<uint32_t>(Q * r)) tcols <<= 1;
 
   if (threadIdx.x == 0) RTRACE(0);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kQuantWarps + (r ? 1 : 0));
-      mbar_init(&conv[s], kQuantWarps);
+  if (warp == 0) {                                             // lane s initialises the barriers of slot s
+    if (lane < S) {
+      mbar_init(&full[lane], 1);
+      mbar_init(&empty[lane], kQuantWarps + (r ? 1 : 0));
+      mbar_init(&conv[lane], kQuantWarps);
     }
-    mbar_init(dfull, 1);
+    if (lane < SW) {
+      mbar_init(&wfull[lane], 1);
+      mbar_init(&wempty[lane], 1);
+    }
+    if (lane == 31) mbar_init(dfull, 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmX);
-    if (r) tma_prefetch(&tmL);
     tma_prefetch(&tmLam);
   }
+  if (warp == 2 && lane == 0 && r) tma_prefetch(&tmL);
   if (warp == 1 && r) tmem_alloc_n(tmem_slot, tcols);
-  if (kFmt == 0 && threadIdx.x >= 64 && threadIdx.x < 64 + 256) {
-    const uint32_t code = threadIdx.x - 64;                   // UE4M3 byte; 0x7F.. never produced
+  if (kFmt == 0 && threadIdx.x >= 32 * kQ0 && threadIdx.x < 32 * kQ0 + 256) {
+    const uint32_t code = threadIdx.x - 32 * kQ0;             // UE4M3 byte; 0x7F.. never produced
     const float sfd = e4m3_to_f32(code & 0x7F);
     qinv_lut[code] = sfd == 0.f ? 0.f : __frcp_rn(__fmul_rn(sfd, p.gs_x));
   }
@@ -196,49 +224,73 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
   griddep_launch_dependents();                                 // the next kernel may start its prologue
 
   if (warp == 0) {
-    // -------------------------------------------------------------------- producer
+    // -------------------------------------------------------------------- X producer
     if (elect_one()) {
-      // every box is loaded whole: blocks past K are zero-filled by TMA (and counted), so the
-      // last stage's unused B rows are zeros, never stale smem
-      const uint32_t stage_tx = static_cast<uint32_t>(16384 + ((SVDQ_K1REXP & 4) ? 0 : Q * r * 128) + Q * 256);
-      auto load_weights = [&](int i) {
-        const int s = i % S;
-        uint8_t *st = smem + s * Ly.stage_bytes;
+      // every box is loaded whole: blocks past K / rows past M are zero-filled by TMA (and counted)
+      const uint32_t stage_tx = static_cast<uint32_t>(16384 + Q * 256);
+      // lambda_inv of the nb blocks as [2 nb][32] fp32 rows, 128-B swizzle (conflict-free broadcasts)
+      auto load_lam = [&](int i, int s) {
         mbar_arrive_expect_tx(&full[s], stage_tx);
-        for (int q = 0; q < Q && r && !(SVDQ_K1REXP & 4); ++q)
-          tma_load_2d(st + Ly.x_bytes + q * r * 128, &tmL, &full[s], (i * Q + q) * 64, 0);
-        // lambda_inv of the nb blocks as [2 nb][32] fp32 rows, 128-B swizzle (conflict-free broadcasts)
-        tma_load_2d(st + Ly.x_bytes + Q * r * 128, &tmLam, &full[s], 0, (i * Q) * 2);
+        tma_load_2d(smem + s * Ly.stage_bytes + Ly.x_bytes, &tmLam, &full[s], 0, (i * Q) * 2);
       };
       // Before the programmatic dependency resolves (the previous kernel may still run and may
-      // write X): stage the first ring's L1s / lambda tiles (no kernel of this stream writes them).
-      // X itself is warmed in L2 by the quantizer lanes' prefetches (LSU, not the TMA queue).
-      for (int i = 0; i < nsteps && i < S; ++i) load_weights(i);
+      // write X): the first ring's lambda tiles (no kernel of this stream writes them).
+      const int npre = S < SVDQ_K1_LAMPRE ? S : SVDQ_K1_LAMPRE;   // lambda tiles issued before the wait
+      for (int i = 0; i < nsteps && i < npre; ++i) load_lam(i, i);
       griddep_wait();
+      int s = 0;
+      uint32_t ph = 0;                                          // ring round parity of slot s
       for (int i = 0; i < nsteps; ++i) {
-        const int s = i % S;
         if (i >= S) {
-          mbar_wait_spin(&empty[s], ((i / S) & 1) ^ 1);
-          load_weights(i);
+          role_wait(&empty[s], ph ^ 1);
+          load_lam(i, s);
         }
         if (i < 64) RTRACE(2 + i);
-        // X box {64 cols, Q blocks, RT rows}; blocks past K / rows past M are zero-filled (and
-        // still counted in the transaction bytes)
+        // X box {64 cols, Q blocks, RT rows}
         tma_load_3d(smem + s * Ly.stage_bytes, &tmX, &full[s], 0, i * Q, static_cast<int32_t>(row0));
+        if (i + npre < S && i + npre < nsteps) load_lam(i + npre, i + npre);   // rest of the first ring
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 2) {
+    // -------------------------------------------------------------------- L1s producer
+    // L1s never depends on the previous kernel: the ring fills before griddepcontrol.wait
+    if (r && !(SVDQ_K1REXP & 4) && elect_one()) {
+      // Distributed L2 prefetch of the whole L1s (r x K bf16, <= 1 MB at FLUX shapes): this
+      // problem's CTAs each fetch every ntiles-th [r x 64] box.  All CTAs walk K in near lockstep,
+      // so without it every stage's tiles would be first touched -- and waited for -- behind the X
+      // stream's DRAM queue; with it the L1s ring is fed from L2.
+      if (!(SVDQ_K1REXP & 8)) {
+        const int ntile = g.tile_begin[pi + 1] - g.tile_begin[pi];
+        for (int j = static_cast<int>(blockIdx.x) - g.tile_begin[pi]; j < nkb; j += ntile)
+          tma_prefetch_2d(&tmL, j * 64, 0);
+      }
+      int sw = 0;
+      uint32_t wph = 0;
+      for (int i = 0; i < nsteps; ++i) {
+        if (i >= SW) role_wait(&wempty[sw], wph ^ 1);
+        if (i < 64) RTRACE(200 + i);
+        mbar_arrive_expect_tx(&wfull[sw], static_cast<uint32_t>(Ly.l1_bytes));
+        for (int q = 0; q < Q; ++q)
+          tma_load_2d(wring + sw * Ly.l1_bytes + q * r * 128, &tmL, &wfull[sw], (i * Q + q) * 64, 0);
+        if (++sw == SW) { sw = 0; wph ^= 1; }
       }
     }
   } else if (warp == 1) {
     // -------------------------------------------------------------------- MMA issuer
     if (r) {
       const uint32_t idesc = idesc_bf16(128, static_cast<uint32_t>(Q * r));
+      int s = 0, sw = 0;
+      uint32_t ph = 0, wph = 0;
       for (int i = 0; i < nsteps; ++i) {
-        const int s = i % S;
-        mbar_wait_spin(&full[s], (i / S) & 1);
-        if (kX16) mbar_wait_spin(&conv[s], (i / S) & 1);      // hi / lo bf16 tiles written
+        role_wait(&full[s], ph);
+        if (kX16) role_wait(&conv[s], ph);                      // hi / lo bf16 tiles written
+        if (!(SVDQ_K1REXP & 4)) role_wait(&wfull[sw], wph);
+        if (lane == 0 && i < 64) RTRACE(300 + i);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t xa = smem_u32(smem + s * Ly.stage_bytes);
-          const uint32_t la = xa + Ly.x_bytes;
+          const uint32_t la = smem_u32(wring + sw * Ly.l1_bytes);
 #pragma unroll
           for (int j = 0; j < ((SVDQ_K1REXP & 2) ? 0 : 4); ++j)
             mma_bf16(tmem, sdesc_kmajor_sw128(xa + 32 * j), sdesc_kmajor_sw128(la + 32 * j), idesc,
@@ -249,15 +301,18 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
               mma_bf16(tmem, sdesc_kmajor_sw128(xa + 16384 + 32 * j), sdesc_kmajor_sw128(la + 32 * j), idesc, 1u);
           }
           tc_commit(&empty[s]);
+          tc_commit(&wempty[sw]);
         }
         __syncwarp();
+        if (++s == S) { s = 0; ph ^= 1; }
+        if (++sw == SW) { sw = 0; wph ^= 1; }
       }
       if (elect_one()) tc_commit(dfull);
       __syncwarp();
     }
   } else {
     // -------------------------------------------------------------------- quantizers
-    const int qw = warp - 2;
+    const int qw = warp - kQ0;
     const int R = qw * 8 + (lane >> 2);                         // staged tile row = m * Q + qb
     const int q4 = lane & 3;                                    // 16-element group within the block
     const int m = R / Q;                                        // row within the tile
@@ -267,20 +322,9 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
     const float t6 = __fmul_rn(__frcp_rn(p.gs_x), __frcp_rn(6.0f));
     // output addressing: the layer's own layout (out_k = K, out_c0 = 0), or -- fused tensor-parallel
     // gather -- this K-slice's place inside the full-K layout (out_k = full K, out_c0 = k0 / 16)
-    uint2 *xq_ptr = reinterpret_cast<uint2 *>(p.xq + row * (p.out_k / 2) + static_cast<int64_t>(qb) * 32) + q4;
-    uint8_t *sf_ptr = p.xs + sf_offset(row, p.out_c0, p.out_k) + static_cast<int64_t>(qb) * 512 + q4;
-    uint16_t *s16_ptr = reinterpret_cast<uint16_t *>(p.xs) + row * (p.out_k / 64) + p.out_c0 / 4 + qb;
-    // L2 prefetch of this lane's future X lines (one 128-B line per staged row, issued by the q4 == 0
-    // lane): kPf stages ahead, so the TMA loads find X in L2 instead of paying the DRAM round trip
-    // with only S stages in flight.  An L2 prefetch never returns stale data, so the first ones go
-    // out before the programmatic dependency resolves.
-    const char *xrow = static_cast<const char *>(p.X) + (row < p.M ? row : p.M - 1) * p.ldx * 2 + qb * 128;
-    const int pf_dist = S + 2;
-    auto x_prefetch = [&](int st) {
-      if (SVDQ_K1R_PF && q4 == 0 && st < nsteps && st * Q + qb < nkb)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(xrow + static_cast<int64_t>(st) * Q * 128));
-    };
-    for (int st = 0; st < pf_dist; ++st) x_prefetch(st);
+    uint8_t *const xq_base = p.xq + row * (p.out_k / 2) + static_cast<int64_t>(qb) * 32 + q4 * 8;
+    uint8_t *const sf_base = p.xs + sf_offset(row, p.out_c0, p.out_k) + static_cast<int64_t>(qb) * 512 + q4;
+    uint8_t *const s16_base = p.xs + 2 * (row * (p.out_k / 64) + p.out_c0 / 4 + qb);
     const uint32_t swz = static_cast<uint32_t>(R & 7);
     const uint32_t lut = smem_u32(qinv_lut);
     const uint32_t stage0 = smem_u32(smem);
@@ -289,31 +333,27 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
     uint32_t lam_off[4];
 #pragma unroll
     for (int t = 0; t < 4; ++t)
-      lam_off[t] = static_cast<uint32_t>(jl * 128 + ((((q4 & 1) * 4 + t) ^ (jl & 7)) * 16));
-    const uint32_t lam_base = static_cast<uint32_t>(Ly.x_bytes + Q * r * 128);
-    int s = 0;
-    uint32_t ph = 0;
-    for (int i = 0; i < nsteps; ++i, xq_ptr += Q * 4, sf_ptr += Q * 512, s16_ptr += Q) {
-      x_prefetch(i + pf_dist);
-      mbar_wait(&full[s], ph);
+      lam_off[t] = static_cast<uint32_t>(Ly.x_bytes + jl * 128 + ((((q4 & 1) * 4 + t) ^ (jl & 7)) * 16));
+    const uint32_t x_off[2] = {static_cast<uint32_t>(R * 128) + ((static_cast<uint32_t>(2 * q4) ^ swz) * 16),
+                               static_cast<uint32_t>(R * 128) + ((static_cast<uint32_t>(2 * q4 + 1) ^ swz) * 16)};
+    const int ndst = p.ndst;                                    // 1, or the ranks of a fused gather
+    const int64_t d0 = p.dst_delta[0];
+
+    // Stage i -> x_hat pairs (fl32(x * lambda_inv)) in registers, then the slot is released.
+    int qs = 0;                                                 // ring slot of the next stage
+    uint32_t qph = 0;                                           // and its round parity
+    auto load_stage = [&](int i, uint64_t (&xh)[8]) {
+      const int s = qs;
+      mbar_wait(&full[s], qph);
+      if (++qs == S) { qs = 0; qph ^= 1; }
       if (qw == 0 && lane == 0 && i < 64) RTRACE(110 + i);
-      const bool active = i * Q + qb < nkb;                     // this lane's block exists (last stage)
-      if (kFmt == 2 && !kX16) {                                 // W8A8: the MMA warp alone uses the tile
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        if (++s == S) { s = 0; ph ^= 1; }
-        continue;
-      }
       const uint32_t sbase = stage0 + s * Ly.stage_bytes;
-      const uint32_t xa = sbase + R * 128;
-      const uint32_t la = sbase + lam_base;
-      uint64_t xh[8];                                           // x_hat pairs = fl32(x * lambda_inv)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint64_t l0, l1, l2, l3;
-        lds_v2x64(la + lam_off[2 * c], l0, l1);
-        lds_v2x64(la + lam_off[2 * c + 1], l2, l3);
-        const uint32_t xaddr = xa + ((static_cast<uint32_t>(2 * q4 + c) ^ swz) * 16);
+        lds_v2x64(sbase + lam_off[2 * c], l0, l1);
+        lds_v2x64(sbase + lam_off[2 * c + 1], l2, l3);
+        const uint32_t xaddr = sbase + x_off[c];
         const uint4 v = lds128(xaddr);
         const uint64_t x0 = x2_to_f32x2<kX16>(v.x), x1 = x2_to_f32x2<kX16>(v.y);
         const uint64_t x2 = x2_to_f32x2<kX16>(v.z), x3 = x2_to_f32x2<kX16>(v.w);
@@ -346,28 +386,36 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);                   // tile consumed: values in registers
-      if (++s == S) { s = 0; ph ^= 1; }
-      if constexpr (kFmt == 2) continue;                        // W8A8 (fp16 X): conversion only
-      if (SVDQ_K1REXP & 1) {
-        if (xh[0] == 12345ull) p.xq[0] = 1;                     // keep the loads alive
-        continue;
-      }
+    };
+    // Group absmax -> scale -> codes, stored at stage i's place (App. B recipe, bit-exact).
+    auto quant_store = [&](int i, const uint64_t (&xh)[8], bool st) {
+      const bool active = st && i * Q + qb < nkb;               // this lane's block exists (last stage)
       float am[8];                                              // |x_hat| max as a tree (short chain)
 #pragma unroll
       for (int j = 0; j < 8; ++j) am[j] = fmaxf(fabsf(lo32(xh[j])), fabsf(hi32(xh[j])));
       float amax = fmaxf(fmaxf(fmaxf(am[0], am[1]), fmaxf(am[2], am[3])), fmaxf(fmaxf(am[4], am[5]), fmaxf(am[6], am[7])));
+      const int64_t step = static_cast<int64_t>(i) * Q;         // K blocks before this stage
       if constexpr (kFmt == 0) {
         const uint32_t sf = e4m3_rn_sat(__fmul_rn(amax, t6));
         float qinv;
-        asm("ld.shared.f32 %0, [%1];" : "=f"(qinv) : "r"(lut + sf * 4));
+        if (SVDQ_K1REXP & 32) qinv = __uint_as_float(0x3C000000u + (sf << 20));   // ablation: no LUT
+        else asm("ld.shared.f32 %0, [%1];" : "=f"(qinv) : "r"(lut + sf * 4));
         const uint64_t q2 = pack64(__float_as_uint(qinv), __float_as_uint(qinv));
         const uint32_t w0 = e2m1x8_pairs(fmul2(xh[0], q2), fmul2(xh[1], q2), fmul2(xh[2], q2), fmul2(xh[3], q2));
         const uint32_t w1 = e2m1x8_pairs(fmul2(xh[4], q2), fmul2(xh[5], q2), fmul2(xh[6], q2), fmul2(xh[7], q2));
+        if (SVDQ_K1REXP & 16) {                                 // ablation: no global stores
+          if ((w0 ^ w1 ^ sf) == 0x12345u) p.xq[0] = 1;
+          return;
+        }
         if (active) {
-          for (int j = 0; j < p.ndst; ++j) {                    // 1, or every rank of a fused gather
+          uint8_t *xq = xq_base + step * 32;
+          uint8_t *sfp = sf_base + step * 512;
+          if (rvalid) *reinterpret_cast<uint2 *>(xq + d0) = make_uint2(w0, w1);
+          sfp[d0] = static_cast<uint8_t>(sf);                   // padding rows (>= M) get 0x00
+          for (int j = 1; j < ndst; ++j) {                      // the other ranks of a fused gather
             const int64_t d = p.dst_delta[j];
-            if (rvalid) *reinterpret_cast<uint2 *>(reinterpret_cast<uint8_t *>(xq_ptr) + d) = make_uint2(w0, w1);
-            sf_ptr[d] = static_cast<uint8_t>(sf);               // padding rows (>= M) get 0x00
+            if (rvalid) *reinterpret_cast<uint2 *>(xq + d) = make_uint2(w0, w1);
+            sfp[d] = static_cast<uint8_t>(sf);
           }
         }
       } else {
@@ -391,40 +439,67 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
           w[c] = word;
         }
         if (rvalid && active) {
-          for (int j = 0; j < p.ndst; ++j) {
+          uint8_t *xq = xq_base + step * 32;
+          uint8_t *s16 = s16_base + step * 2;
+          for (int j = 0; j < ndst; ++j) {
             const int64_t d = p.dst_delta[j];
-            *reinterpret_cast<uint2 *>(reinterpret_cast<uint8_t *>(xq_ptr) + d) = make_uint2(w[0], w[1]);
-            if (q4 == 0) *reinterpret_cast<uint16_t *>(reinterpret_cast<uint8_t *>(s16_ptr) + d) = sc;
+            *reinterpret_cast<uint2 *>(xq + d) = make_uint2(w[0], w[1]);
+            if (q4 == 0) *reinterpret_cast<uint16_t *>(s16 + d) = sc;
           }
         }
+      }
+    };
+
+    if (kFmt == 2 && !kX16) {                                   // W8A8: the MMA warp alone uses the tile
+      for (int i = 0; i < nsteps; ++i) {
+        const int s = qs;
+        mbar_wait(&full[s], qph);
+        if (++qs == S) { qs = 0; qph ^= 1; }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+    } else {
+      for (int i = 0; i < nsteps; ++i) {
+        uint64_t xh[8];
+        load_stage(i, xh);
+        if (kFmt == 2) continue;                                // W8A8 (fp16 X): conversion only
+        if (SVDQ_K1REXP & 1) {
+          if (xh[0] == 12345ull) p.xq[0] = 1;                   // keep the loads alive
+          continue;
+        }
+        quant_store(i, xh, true);
+        if (lane == 0 && i == nsteps / 2) RTRACE(420 + qw);
       }
     }
   }
 
-  if (threadIdx.x == 64) RTRACE(100);                          // quantizer 0 done
+  if (threadIdx.x == 32 * kQ0) RTRACE(100);                    // quantizer 0 done
+  if (warp >= kQ0 && lane == 0) RTRACE(400 + warp - kQ0);
   if (r == 0) return;
   // ---------------------------------------------------------------------- xl1 = sum_q diag blocks
   __syncthreads();                                             // every stage consumed: ring reusable
   float *red = reinterpret_cast<float *>(smem);                // [Q][RT][r + 4] fp32 (<= 68 KB)
   const int rs = r + 4;                                        // padded row stride: fewer bank conflicts
-  if (warp >= 2 && warp < 6) {
+  if (warp >= kQ0) {
+    // the 16 quantizer warps drain TMEM in parallel: 4 per lane quadrant, 16-column chunks
+    // c = qq, qq + 4, ...; a lane keeps the chunks of its own row's diagonal block
     const int qd = warp & 3;                                   // TMEM lane quadrant of this warp
+    const int qq = (warp - kQ0) >> 2;                          // 0..3 within the quadrant
     const int d = 32 * qd + lane;                              // D row = m * Q + q
     const int q = d % Q, mm = d / Q;
-    mbar_wait_spin(dfull, 0);
+    mbar_wait(dfull, 0);
     tc_fence_after();
-    for (int qq = 0; qq < Q; ++qq) {
-      for (int c = 0; c < r; c += 16) {
-        uint32_t v[16];
-        tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(32 * qd) << 16) + qq * r + c, v);
-        tmem_ld_wait();
-        if (qq == q) {                                         // the diagonal block of this lane's row
-          float *dst = red + (q * RT + mm) * rs + c;
+    for (int c = qq; c < Q * r / 16; c += 4) {
+      uint32_t v[16];
+      tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(32 * qd) << 16) + 16 * c, v);
+      tmem_ld_wait();
+      const int blk = 16 * c / r;
+      if (blk == q) {                                          // the diagonal block of this lane's row
+        float *dst = red + (q * RT + mm) * rs + (16 * c - blk * r);
 #pragma unroll
-          for (int j = 0; j < 16; j += 4)
-            *reinterpret_cast<float4 *>(dst + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
-                                                               __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-        }
+        for (int j = 0; j < 16; j += 4)
+          *reinterpret_cast<float4 *>(dst + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                                             __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
       }
     }
   }
@@ -450,7 +525,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
       else *reinterpret_cast<uint32_t *>(p.xl1 + row * r + col) = pack_bf16x2(s0, s1);
     }
   }
-  if (threadIdx.x == 64) RTRACE(101);
+  if (threadIdx.x == 32 * kQ0) RTRACE(101);
 }
 
 template <int kFmt, bool kScaleBf16, bool kX16>

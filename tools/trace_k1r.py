@@ -19,11 +19,16 @@ if os.environ.get("COLD", "0") == "1":
     flush.zero_(); flush[: 256 << 20].view(torch.int64).sum()
 P.svdq_quantize_act_lowrank_down(layer, x)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * 256)()
+buf = (ctypes.c_ulonglong * 512)()
 P.abi.lib().svdq_k1r_trace_read(buf)
 t = np.array(buf[:], dtype=np.int64)
 rel = lambda i: (t[i] - t[0]) / 1000.0
 print("cold" if os.environ.get("COLD") == "1" else "warm", f"M={M} K={K}: setup done {rel(1):.2f} us")
 print("stage issue times:", " ".join(f"{rel(2 + i):.2f}" for i in range(64) if t[2 + i] > 0 and t[2 + i] >= t[0]))
 print("stage seen by quantizer warp 0:", " ".join(f"{rel(110 + i):.2f}" for i in range(64) if t[110 + i] >= t[0]))
+print("L1s issue times:", " ".join(f"{rel(200 + i):.2f}" for i in range(64) if t[200 + i] >= t[0]))
+print("MMA passes waits:", " ".join(f"{rel(300 + i):.2f}" for i in range(64) if t[300 + i] >= t[0]))
+print("quantizer warps at stage nsteps/2:", " ".join(f"{rel(420 + i):.2f}" for i in range(16)))
+print("quantizer warps done:", " ".join(f"{rel(400 + i):.2f}" for i in range(16)))
+print(f"all quantizers done (tail sync) {rel(102):.2f}")
 print(f"quantizer 0 done {rel(100):.2f}  xl1 stored {rel(101):.2f}")
