@@ -536,7 +536,8 @@ svdq_status prepare_k2(const svdq_linear *L, const uint8_t *xq, const uint8_t *x
   // pair tile N: the caller's (grouped / fused launches share one) or this problem's own
   out->bn = pair ? (pair_bn ? pair_bn : k2_pair_bn(N)) : 0;
   const int BN = L->fmt == SVDQ_FMT_NVFP4 ? (pair ? out->bn : k2_nvfp4_bn(M, N)) : kInt4BN;
-  const uint32_t b_rows = pair ? static_cast<uint32_t>(BN / 2) : static_cast<uint32_t>(BN);   // B rows staged per CTA
+  // rows per B-side TMA box: the CTA's BN / 2 rows in one box, or three 64-row boxes at BN = 384
+  const uint32_t b_rows = pair ? static_cast<uint32_t>(BN == 384 ? 64 : BN / 2) : static_cast<uint32_t>(BN);
   CUtensorMap &sfa_map = out->sfa_map, &sfb_map = out->sfb_map;
   if (L->fmt == SVDQ_FMT_NVFP4) {
     const CUtensorMapDataType ydt = y_dtype == SVDQ_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
@@ -557,7 +558,7 @@ svdq_status prepare_k2(const svdq_linear *L, const uint8_t *xq, const uint8_t *x
     if ((st = make_map(&maps.b, L->w_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, N, K / 2, 128, b_rows)) != SVDQ_OK) return st;
     if (pair) {
       if ((st = make_sf_map(&sfa_map, xs, M, K, 1)) != SVDQ_OK) return st;
-      if ((st = make_sf_map(&sfb_map, L->w_scales, N, K, 2)) != SVDQ_OK) return st;
+      if ((st = make_sf_map(&sfb_map, L->w_scales, N, K, BN == 384 ? 3 : 2)) != SVDQ_OK) return st;
     }
   } else if (L->fmt == SVDQ_FMT_W8A8) {
     // int8 tiles [rows x 128 B], 128-B swizzle: straight into the kind::i8 operand ring
@@ -605,11 +606,17 @@ svdq_status svdq_gemm_w4a4_lowrank_up_grouped(int32_t n, const svdq_linear *cons
   K2PairArgs g;
   std::memset(&g, 0, sizeof(g));
   g.n = n;
-  int bn = 256;                              // one tile shape per launch: 256 only if every N allows it
+  int cap = 384;                             // one tile shape per launch: the widest every N allows
   for (int i = 0; i < n; ++i) {
     if (!layers[i]) return fail(SVDQ_ERR_INVALID_ARGUMENT, "null layer %d", i);
     if (layers[i]->fmt != SVDQ_FMT_NVFP4) return fail(SVDQ_ERR_UNSUPPORTED, "grouped K2 is NVFP4 only");
-    bn = std::min(bn, k2_pair_bn(layers[i]->N));
+    cap = std::min(cap, k2_pair_bn(layers[i]->N));
+  }
+  int bn = 192;
+  for (const int c : {384, 256}) {
+    bool ok = c <= cap;
+    for (int i = 0; i < n && ok; ++i) ok = layers[i]->N % c == 0;
+    if (ok) { bn = c; break; }
   }
   g.bn = bn;
   for (int i = 0; i < n; ++i) {

@@ -44,20 +44,27 @@ namespace svdq {
 
 namespace {
 
-// Pair tile N: 192 (two TMEM accumulator buffers; any N) or 256 (N % 256 == 0: one accumulator
-// buffer -- TMEM holds 512 columns -- measured as fast as double buffering at N = 192, and the
-// larger tile reads 17 % fewer shared-memory bytes per FLOP and issues 25 % fewer MMAs).
+// Pair tile N: 192 (two TMEM accumulator buffers; any N), 256 (N % 256 == 0; the default when it
+// divides N) or 384 (opt-in, SVDQ_K2_BN=384): one accumulator buffer -- TMEM holds 512 columns:
+// 384 accumulator + 2 x 64 scale-factor columns.  The 384 tile reads 16 % fewer operand bytes per
+// FLOP (per CTA and K step of 256: 48 KB for 25.2 MFLOP vs 38 KB for 16.8 MFLOP), for the case
+// that the L2 -> SM stream binds (ncu: 12.5 TB/s on FLUX linear1 at 256); measured, it does not
+// (see k2_pair_bn).  At 384 each CTA stages 192 B rows as [its 128 rows of the N = 256 MMA | its
+// 64 rows of the N = 128 MMA] (three 64-row TMA boxes); the scale-factor rows are three atoms.
 constexpr int A_BYTES = 128 * 128;            // 16 KB
 constexpr int SFA_BYTES = 2048;
-constexpr int SFB_BYTES = 4096;               // two 128-row atoms x 4 K-blocks
 template <int kBN>
 struct PC {
   static constexpr int BN = kBN;
   static constexpr int BNH = kBN / 2;                       // B rows per CTA
-  static constexpr int B_BYTES = BNH * 128;                 // 12 / 16 KB
-  static constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;   // 34 / 38 KB
-  static constexpr int ACC = kBN == 256 ? 1 : 2;            // accumulator buffers
+  static constexpr int NATOM = kBN == 384 ? 3 : 2;          // 128-row SFB atoms staged per stage
+  static constexpr int B_BYTES = BNH * 128;                 // 12 / 16 / 24 KB
+  static constexpr int SFB_BYTES = NATOM * 2048;            // atoms x 4 K-blocks x 512 B
+  static constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;   // 34 / 38 / 48 KB
+  static constexpr int ACC = kBN == 192 ? 2 : 1;            // accumulator buffers
+  static constexpr int SF_COLS = 16 + 16 * NATOM;           // TMEM columns per SF slot (SFA + SFB, 4 K-blocks)
   static constexpr int SF_BASE = ACC * kBN;
+  static constexpr int BLOAD = kBN == 384 ? 64 : BNH;       // rows per B / L2s TMA box
 };
 constexpr int BN = 192;                       // the fused (layer-boundary) variant's tile N
 #ifndef SVDQ_K2P_STAGES
@@ -84,7 +91,9 @@ constexpr int BN = 192;                       // the fused (layer-boundary) vari
 #endif
 constexpr int kStages = SVDQ_K2P_STAGES;
 constexpr int kEpiBuf = SVDQ_K2P_EPIBUF;      // 2 KB staging buffers per epilogue warp
-constexpr int SF_COLS = 48;
+#ifndef SVDQ_K2P384_STAGES
+#define SVDQ_K2P384_STAGES 4                  // 384-wide tile: 4 x 48 KB stages, 16 epilogue warps x 1 buffer
+#endif
 #ifndef SVDQ_BIGSTORE
 #define SVDQ_BIGSTORE 0
 #endif
@@ -97,22 +106,27 @@ constexpr int EPI_BYTES = SVDQ_BIGSTORE && 3 * 16384 > 8 * 2048 * kEpiBuf ? 3 * 
 template <bool kFuse, int kBN = 192>
 struct Lay {
   static constexpr int BN = kBN;
-  static constexpr int stages = kFuse ? 3 : kStages;
-  static constexpr int epi_w = kFuse ? 12 : SVDQ_K2P_EPIW;  // epilogue warps (2 or 3 per TMEM lane quadrant)
+  static constexpr int stages = kFuse ? 3 : (kBN == 384 ? SVDQ_K2P384_STAGES : kStages);
+  // epilogue warps per CTA (2-4 per TMEM lane quadrant); at 384 columns 4 (3 x 32 columns per warp:
+  // the 96-register drain fits the 112 registers 576 threads allow)
+  static constexpr int epi_w = kFuse ? 12 : (kBN == 384 ? 16 : SVDQ_K2P_EPIW);
+  static constexpr int epibuf = kBN == 384 ? 1 : kEpiBuf;   // 2 KB staging buffers per epilogue warp
+  static constexpr int threads = 64 + 32 * epi_w;
   static constexpr int epi_off = stages * PC<kBN>::STAGE;
-  static constexpr int bar_off = epi_off + (epi_w != 8 ? epi_w * 2048 * kEpiBuf : EPI_BYTES);
+  static constexpr int bar_off = epi_off + (epi_w != 8 ? epi_w * 2048 * epibuf : EPI_BYTES);
   static constexpr int bias_off = bar_off + 256;
   static constexpr int lamn_off = bias_off + BN * 4;
-  static constexpr int at_off = (lamn_off + BN * 4 + 1023) / 1024 * 1024;
-  static constexpr int bt_off = at_off + 3 * 16384;
-  static constexpr int cs_off = bt_off + 3 * 2048;         // next-layer code tile [128 x 96 B]
+  static constexpr int at_off = (lamn_off + BN * 4 + 1023) / 1024 * 1024;   // a tile: 3 x 16 KB
+  static constexpr int bt_off = at_off + 3 * 16384;         // L1s_next half: 3 x 2 KB (r <= 32)
+  static constexpr int cs_off = bt_off + 3 * 2048;          // next-layer codes, [128 rows x 96 B]
   static constexpr int sfs_off = cs_off + 128 * 96;         // next-layer scale factors, 3 x 512 B
   static constexpr int smem = kFuse ? sfs_off + 3 * 512 + 1024 : bias_off + BN * 4 + 1024;
 };
-constexpr int XL1_COL = PC<192>::SF_BASE + 2 * SF_COLS;   // TMEM columns [480, 512): X L1s_next^T accumulator
+constexpr int XL1_COL = PC<192>::SF_BASE + 2 * PC<192>::SF_COLS;   // TMEM columns [480, 512): X L1s_next^T accumulator
 static_assert(XL1_COL + 32 <= 512, "TMEM budget (fused)");
-static_assert(PC<192>::STAGE % 1024 == 0 && PC<256>::STAGE % 1024 == 0, "stage alignment");
-static_assert(PC<192>::SF_BASE + 2 * SF_COLS <= 512 && PC<256>::SF_BASE + 2 * SF_COLS <= 512, "TMEM budget");
+static_assert(PC<192>::STAGE % 1024 == 0 && PC<256>::STAGE % 1024 == 0 && PC<384>::STAGE % 1024 == 0, "stage alignment");
+static_assert(PC<192>::SF_BASE + 2 * PC<192>::SF_COLS <= 512 && PC<256>::SF_BASE + 2 * PC<256>::SF_COLS <= 512 &&
+              PC<384>::SF_BASE + 2 * PC<384>::SF_COLS <= 512, "TMEM budget");
 
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -161,10 +175,12 @@ __device__ __forceinline__ TileRef locate(const K2PairArgs &g, int t) {
 }
 
 template <bool kFuse, int kBN>
-__global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
+__global__ void __launch_bounds__(Lay<kFuse, kBN>::threads, 1)
     k2_nvfp4_2sm_kernel(const __grid_constant__ K2PairArgs g) {
   constexpr int BN = kBN, BNH = PC<kBN>::BNH, B_BYTES = PC<kBN>::B_BYTES, STAGE = PC<kBN>::STAGE;
-  constexpr int SF_BASE = PC<kBN>::SF_BASE, ACC = PC<kBN>::ACC;
+  constexpr int SF_BASE = PC<kBN>::SF_BASE, ACC = PC<kBN>::ACC, SF_COLS = PC<kBN>::SF_COLS;
+  constexpr int NATOM = PC<kBN>::NATOM, SFB_BYTES = PC<kBN>::SFB_BYTES;
+  (void)SFB_BYTES;
   static_assert(!kFuse || kBN == 192, "the fused variant runs 192-wide tiles");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -240,6 +256,17 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
 #endif
       // Weight tiles (B, SFB) of the first tile's first ring do not depend on K1: issue them
       // before the programmatic dependency resolves, so they land while K1 finishes.
+      // this CTA's B-side rows of the pair tile at n0 (B codes or, for the low-rank slab, L2s): one box
+      // of BN/2 rows, or at 384 three 64-row boxes [n0 + 128 c, +128) and [n0 + 256 + 64 c, +64)
+      auto load_bside = [&](uint8_t *dst, const CUtensorMap *map, uint32_t fb, int32_t kc, int64_t n0) {
+        if constexpr (kBN == 384) {
+          tma_load_2d_cg2(dst, map, fb, kc, static_cast<int32_t>(n0 + 128 * crank));
+          tma_load_2d_cg2(dst + 64 * 128, map, fb, kc, static_cast<int32_t>(n0 + 128 * crank + 64));
+          tma_load_2d_cg2(dst + 128 * 128, map, fb, kc, static_cast<int32_t>(n0 + 256 + 64 * crank));
+        } else {
+          tma_load_2d_cg2(dst, map, fb, kc, static_cast<int32_t>(n0 + BNH * crank));
+        }
+      };
       const int pre = (SVDQ_EXP & 4) || t_first >= t_end ? 0 : min(kSt, nkt_of(locate<kBN>(g, t_first).i));
       if (pre) {
         const TileRef tr = locate<kBN>(g, t_first);
@@ -248,7 +275,7 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
           uint8_t *st = smem + kt * STAGE;
           const uint32_t fb = full0 + kt * 8;
           if (crank == 0) mbar_arrive_expect_tx(&full[kt], 2 * STAGE);
-          tma_load_2d_cg2(st + A_BYTES, &pr.b, fb, kt * 128, static_cast<int32_t>(tr.n0 + BNH * crank));
+          load_bside(st + A_BYTES, &pr.b, fb, kt * 128, tr.n0);
           tma_load_3d_cg2(st + A_BYTES + B_BYTES + SFA_BYTES, &pr.sfb, fb, 0, kt * 4,
                           static_cast<int32_t>(tr.n0 / 128));
         }
@@ -263,7 +290,6 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
         const int64_t m0 = tr.m0;
         const int64_t n0 = tr.n0;
         const int32_t ma = static_cast<int32_t>(m0 + 128 * crank);
-        const int32_t nb = static_cast<int32_t>(n0 + BNH * crank);
         for (int kt = 0; kt < nkt; ++kt) {
           uint8_t *st = smem + s * STAGE;
           const uint32_t fb = full0 + s * 8;
@@ -281,7 +307,7 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
 #endif
           if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE);
           tma_load_2d_cg2(st, &pr.a, fb, kt * 128, ma);
-          tma_load_2d_cg2(st + A_BYTES, &pr.b, fb, kt * 128, nb);
+          load_bside(st + A_BYTES, &pr.b, fb, kt * 128, n0);
           tma_load_3d_cg2(st + A_BYTES + B_BYTES, &pr.sfa, fb, 0, kt * 4, static_cast<int32_t>(m0 / 128 + crank));
           tma_load_3d_cg2(st + A_BYTES + B_BYTES + SFA_BYTES, &pr.sfb, fb, 0, kt * 4,
                           static_cast<int32_t>(n0 / 128));
@@ -294,7 +320,7 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
           const uint32_t fb = full0 + s * 8;
           if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
           tma_load_2d_cg2(st, &pr.xl1, fb, j * 64, ma);
-          tma_load_2d_cg2(st + A_BYTES, &pr.l2, fb, j * 64, nb);
+          load_bside(st + A_BYTES, &pr.l2, fb, j * 64, n0);
           if (++s == kSt) { s = 0; ph ^= 1; }
         }
       }
@@ -305,8 +331,13 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader)
     if (crank == 0) {
-      constexpr uint32_t idesc_q = idesc_nvfp4(256, BN);
-      constexpr uint32_t idesc_h = idesc_bf16(256, BN);
+      // 384: an N = 256 MMA into columns [0, 256) and an N = 128 MMA into [256, 384) per K block
+      constexpr uint32_t NM1 = kBN == 384 ? 256 : BN;
+      constexpr uint32_t idesc_q = idesc_nvfp4(256, NM1);
+      constexpr uint32_t idesc_h = idesc_bf16(256, NM1);
+      constexpr uint32_t idesc_q2 = idesc_nvfp4(256, 128);
+      constexpr uint32_t idesc_h2 = idesc_bf16(256, 128);
+      constexpr uint32_t B2_OFF = 128 * 128;                 // smem offset of the second MMA's B rows
       int s = 0;
       uint32_t ph = 0;
       int acc_i = 0;
@@ -366,38 +397,33 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
             // descriptors: +16 B in smem = +1 in the start-address field (no carry: smem < 256 KB)
             const uint64_t sfa_d = sdesc_cp_32x128b(sfa_addr), sfb_d = sdesc_cp_32x128b(sfb_addr);
             const uint64_t a_d = sdesc_kmajor_sw128(a_addr), b_d = sdesc_kmajor_sw128(b_addr);
+            const uint64_t b2_d = sdesc_kmajor_sw128(b_addr + B2_OFF);
+            // SFB atoms of K block i at columns sfb_col + 4 NATOM i + 4 a; the smem atom a at + 2 KB a
+            auto sf_copy = [&](int i) {
+#if (SVDQ_EXP & 3) < 2
+              tmem_cp_32x128b_warpx4_cg2(sfa_col + 4 * i, sfa_d + 32 * i);
+#endif
+#if (SVDQ_EXP & 3) < 1
+#pragma unroll
+              for (int a = 0; a < NATOM; ++a)
+                tmem_cp_32x128b_warpx4_cg2(sfb_col + 4 * NATOM * i + 4 * a, sfb_d + 128 * a + 32 * i);
+#endif
+            };
+            auto mma_kb = [&](int i) {
+              mma_nvfp4_cg2(d_tmem, a_d + 2 * i, b_d + 2 * i, idesc_q, sfa_col + 4 * i,
+                            sfb_col + 4 * NATOM * i + sfb_off, (kt | i) != 0);
+              if constexpr (kBN == 384)
+                mma_nvfp4_cg2(d_tmem + 256, a_d + 2 * i, b2_d + 2 * i, idesc_q2, sfa_col + 4 * i,
+                              sfb_col + 4 * NATOM * i + 8, (kt | i) != 0);
+            };
             if (nsub == 4) {
-            #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-#if (SVDQ_EXP & 3) < 2
-                tmem_cp_32x128b_warpx4_cg2(sfa_col + 4 * i, sfa_d + 32 * i);
-#endif
-#if (SVDQ_EXP & 3) < 1
-                tmem_cp_32x128b_warpx4_cg2(sfb_col + 8 * i, sfb_d + 32 * i);
-#endif
-#if (SVDQ_EXP & 3) < 1
-                tmem_cp_32x128b_warpx4_cg2(sfb_col + 8 * i + 4, sfb_d + 128 + 32 * i);
-#endif
-              }
-            #pragma unroll
-              for (int i = 0; i < 4; ++i)
-                mma_nvfp4_cg2(d_tmem, a_d + 2 * i, b_d + 2 * i, idesc_q, sfa_col + 4 * i, sfb_col + 8 * i + sfb_off,
-                      (kt | i) != 0);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) sf_copy(i);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) mma_kb(i);
             } else {
-              for (int i = 0; i < nsub; ++i) {
-#if (SVDQ_EXP & 3) < 2
-                tmem_cp_32x128b_warpx4_cg2(sfa_col + 4 * i, sfa_d + 32 * i);
-#endif
-#if (SVDQ_EXP & 3) < 1
-                tmem_cp_32x128b_warpx4_cg2(sfb_col + 8 * i, sfb_d + 32 * i);
-#endif
-#if (SVDQ_EXP & 3) < 1
-                tmem_cp_32x128b_warpx4_cg2(sfb_col + 8 * i + 4, sfb_d + 128 + 32 * i);
-#endif
-              }
-              for (int i = 0; i < nsub; ++i)
-                mma_nvfp4_cg2(d_tmem, a_d + 2 * i, b_d + 2 * i, idesc_q, sfa_col + 4 * i, sfb_col + 8 * i + sfb_off,
-                      (kt | i) != 0);
+              for (int i = 0; i < nsub; ++i) sf_copy(i);
+              for (int i = 0; i < nsub; ++i) mma_kb(i);
             }
             tc_commit_cg2_mc(&empty[s], 0x3);
           }
@@ -413,9 +439,13 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
             const uint32_t a_addr = smem_u32(st);
             const uint32_t b_addr = smem_u32(st + A_BYTES);
             const int nk16 = min(4, (rank - j * 64) / 16);
-            for (int i = 0; i < nk16; ++i)
+            for (int i = 0; i < nk16; ++i) {
               mma_bf16_cg2(d_tmem, sdesc_kmajor_sw128(a_addr + 32 * i), sdesc_kmajor_sw128(b_addr + 32 * i),
                            idesc_h, (nkt > 0 || j > 0 || i > 0) ? 1u : 0u);
+              if constexpr (kBN == 384)
+                mma_bf16_cg2(d_tmem + 256, sdesc_kmajor_sw128(a_addr + 32 * i),
+                             sdesc_kmajor_sw128(b_addr + B2_OFF + 32 * i), idesc_h2, (nkt > 0 || j > 0 || i > 0) ? 1u : 0u);
+            }
             tc_commit_cg2_mc(&empty[s], 0x3);
           }
           __syncwarp();
@@ -568,10 +598,10 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
 #endif
       if constexpr (kFuse) {
         if (p.fuse) {
-          epilogue_tile_next<BN, kNWQ, kEpiBuf>(
+          epilogue_tile_next<BN, kNWQ, LY::epibuf>(
               tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.Y ? tmY : nullptr,
               static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
-              smem + LY::epi_off + (warp - 2) * 2048 * kEpiBuf, ebuf, lane,
+              smem + LY::epi_off + (warp - 2) * 2048 * LY::epibuf, ebuf, lane,
               [&]() {
                 tc_fence_before();
                 __syncwarp();
@@ -627,9 +657,9 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
           continue;
         }
       }
-      epilogue_tile<BN, kNWQ, kEpiBuf>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
+      epilogue_tile<BN, kNWQ, LY::epibuf>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
                            tmY, static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
-                           smem + LY::epi_off + (warp - 2) * 2048 * kEpiBuf, ebuf, lane, [&]() {
+                           smem + LY::epi_off + (warp - 2) * 2048 * LY::epibuf, ebuf, lane, [&]() {
                           tc_fence_before();
                           __syncwarp();
                           if (lane == 0) K2_ACC_RELEASE(acc_empty0 + b * 8);
@@ -652,12 +682,25 @@ __global__ void __launch_bounds__(kFuse ? 448 : 64 + 32 * SVDQ_K2P_EPIW, 1)
 
 }  // namespace
 
+namespace {
+template <int kBN>
+cudaError_t launch_plain(const K2PairArgs &g, int64_t pairs, cudaStream_t s) {
+  using LY = Lay<false, kBN>;
+  cudaError_t e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<false, kBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       LY::smem);
+  if (e != cudaSuccess) return e;
+  return launch_ex(k2_nvfp4_2sm_kernel<false, kBN>, dim3(static_cast<unsigned>(2 * pairs)), dim3(LY::threads),
+                   LY::smem, s, 2u, g);
+}
+}  // namespace
+
 cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
-  static_assert(Lay<false, 192>::smem <= 227 * 1024 && Lay<false, 256>::smem <= 227 * 1024, "smem budget");
+  static_assert(Lay<false, 192>::smem <= 227 * 1024 && Lay<false, 256>::smem <= 227 * 1024 &&
+                Lay<false, 384>::smem <= 227 * 1024, "smem budget");
   static_assert(Lay<true>::smem <= 227 * 1024, "smem budget (fused)");
   bool fuse = false;
   for (int i = 0; i < g.n; ++i) fuse = fuse || g.pr[i].p.fuse;
-  const int bn = fuse ? 192 : (g.bn == 256 ? 256 : 192);
+  const int bn = fuse ? 192 : (g.bn == 384 || g.bn == 256 ? g.bn : 192);
   g.bn = bn;
   g.tile_begin[0] = 0;
   for (int i = 0; i < g.n; ++i)
@@ -667,32 +710,28 @@ cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
   static const int force_contig = [] { const char *e = std::getenv("SVDQ_K2_CONTIG"); return e ? std::atoi(e) : 0; }();
   g.contig = (fuse || force_contig) ? 1 : 0;      // SVDQ_K2_CONTIG=1: schedule ablation
   g.npairs = static_cast<int>(pairs);
-  cudaError_t e;
   if (fuse) {
-    e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<true, 192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Lay<true>::smem);
+    cudaError_t e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<true, 192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Lay<true>::smem);
     if (e != cudaSuccess) return e;
-    return launch_ex(k2_nvfp4_2sm_kernel<true, 192>, dim3(static_cast<unsigned>(2 * pairs)), dim3(448),
+    return launch_ex(k2_nvfp4_2sm_kernel<true, 192>, dim3(static_cast<unsigned>(2 * pairs)), dim3(Lay<true>::threads),
                      Lay<true>::smem, s, 2u, g);
   }
-  if (bn == 256) {
-    e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Lay<false, 256>::smem);
-    if (e != cudaSuccess) return e;
-    return launch_ex(k2_nvfp4_2sm_kernel<false, 256>, dim3(static_cast<unsigned>(2 * pairs)),
-                     dim3(64 + 32 * SVDQ_K2P_EPIW), Lay<false, 256>::smem, s, 2u, g);
-  }
-  e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<false, 192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           Lay<false, 192>::smem);
-  if (e != cudaSuccess) return e;
-  return launch_ex(k2_nvfp4_2sm_kernel<false, 192>, dim3(static_cast<unsigned>(2 * pairs)),
-                   dim3(64 + 32 * SVDQ_K2P_EPIW), Lay<false, 192>::smem, s, 2u, g);
+  if (bn == 384) return launch_plain<384>(g, pairs, s);
+  if (bn == 256) return launch_plain<256>(g, pairs, s);
+  return launch_plain<192>(g, pairs, s);
 }
 
 int k2_pair_bn(int64_t N) {
-  static const int force = [] { const char *e = std::getenv("SVDQ_K2_BN"); return e ? std::atoi(e) : 0; }();
-  if (force == 192) return 192;                 // SVDQ_K2_BN=192: A/B against the 192-wide tile
-  return N % 256 == 0 ? 256 : 192;
+  // 256 when it divides N.  The 384-wide tile is built and correct but measured slower on every FLUX
+  // shape (linear1 143 vs 121 us, linear2 78 vs 72 us): its mainloop + TMEM drain alone matches the
+  // 256 tile (94.5 vs 95.5 us, SVDQ_EXP=32) -- the operand stream is not the limit -- while its
+  // epilogue (16 warps x 1 staging buffer, 384 columns behind one accumulator) is not hidden.
+  // SVDQ_K2_BN=384 opts in; SVDQ_K2_BN=192 caps at 192 (A/B).
+  static const int cap = [] { const char *e = std::getenv("SVDQ_K2_BN"); return e ? std::atoi(e) : 256; }();
+  if (cap >= 384 && N % 384 == 0) return 384;
+  if (cap >= 256 && N % 256 == 0) return 256;
+  return 192;
 }
 
 int device_sm_count() {

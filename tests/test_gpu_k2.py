@@ -156,3 +156,26 @@ def test_k2_grouped_equals_single(shapes):
         torch.cuda.synchronize()
         assert torch.equal(Ys[i], single), f"problem {i} differs from its single launch"
         assert rel_fro(Ys[i].float().cpu().numpy(), refs[i]) <= 1e-3
+
+
+# ---- the opt-in 384-wide CTA-pair tile (SVDQ_K2_BN=384: the launcher reads it once per process)
+_BN384_CASES = [(1000, 1536, 768, 32, "bf16"), (300, 6144, 384, 0, "bf16"), (513, 3072, 1152, 48, "fp32")]
+
+
+@pytest.mark.parametrize("M,K,N,r,out", _BN384_CASES)
+def test_k2_bn384_cases(M, K, N, r, out):
+    import os
+    if os.environ.get("SVDQ_RUN_BN384") != "1":
+        pytest.skip("runs in the subprocess of test_k2_bn384_opt_in")
+    run_k2("nvfp4", M, K, N, r, out=out, seed=M)
+
+
+def test_k2_bn384_opt_in():
+    import os, subprocess, sys
+    need_cuda()
+    env = dict(os.environ, SVDQ_K2_BN="384", SVDQ_K2_PAIR="1", SVDQ_RUN_BN384="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        f"{__file__}::test_k2_bn384_cases"], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert f"{len(_BN384_CASES)} passed" in r.stdout, r.stdout[-500:]
