@@ -531,19 +531,22 @@ svdq_status prepare_k2(const svdq_linear *L, const uint8_t *xq, const uint8_t *x
   p.w8 = L->fmt == SVDQ_FMT_W8A8;
   K2Maps &maps = out->maps;
   std::memset(&maps, 0, sizeof(maps));
-  const bool pair = L->fmt == SVDQ_FMT_NVFP4 && (force_pair || use_pair_kernel(M, K));
+  // CTA-pair kernel: NVFP4, and W8A8 (its kind::i8 mode, 192-wide tiles)
+  const bool pair = (L->fmt == SVDQ_FMT_NVFP4 || L->fmt == SVDQ_FMT_W8A8) && (force_pair || use_pair_kernel(M, K));
   out->pair = pair;
   // pair tile N: the caller's (grouped / fused launches share one) or this problem's own
-  out->bn = pair ? (pair_bn ? pair_bn : k2_pair_bn(N)) : 0;
-  const int BN = L->fmt == SVDQ_FMT_NVFP4 ? (pair ? out->bn : k2_nvfp4_bn(M, N)) : kInt4BN;
+  out->bn = !pair ? 0 : L->fmt == SVDQ_FMT_W8A8 ? 192 : (pair_bn ? pair_bn : k2_pair_bn(N));
+  const int BN = pair ? out->bn : L->fmt == SVDQ_FMT_NVFP4 ? k2_nvfp4_bn(M, N) : kInt4BN;
+  std::memset(&out->sfa_map, 0, sizeof(out->sfa_map));
+  std::memset(&out->sfb_map, 0, sizeof(out->sfb_map));
   // rows per B-side TMA box: the CTA's BN / 2 rows in one box, or three 64-row boxes at BN = 384
   const uint32_t b_rows = pair ? static_cast<uint32_t>(BN == 384 ? 64 : BN / 2) : static_cast<uint32_t>(BN);
   CUtensorMap &sfa_map = out->sfa_map, &sfb_map = out->sfb_map;
+  const CUtensorMapDataType ydt = y_dtype == SVDQ_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                  : y_dtype == SVDQ_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const int64_t ysz = y_dtype == SVDQ_FP32 ? 4 : 2;
   if (L->fmt == SVDQ_FMT_NVFP4) {
-    const CUtensorMapDataType ydt = y_dtype == SVDQ_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
-                                    : y_dtype == SVDQ_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
-                                                           : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    const int64_t ysz = y_dtype == SVDQ_FP32 ? 4 : 2;
 #ifndef SVDQ_BIGSTORE
 #define SVDQ_BIGSTORE 0
 #endif
@@ -563,7 +566,10 @@ svdq_status prepare_k2(const svdq_linear *L, const uint8_t *xq, const uint8_t *x
   } else if (L->fmt == SVDQ_FMT_W8A8) {
     // int8 tiles [rows x 128 B], 128-B swizzle: straight into the kind::i8 operand ring
     if ((st = make_map(&maps.a, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, M, K, 128, 128)) != SVDQ_OK) return st;
-    if ((st = make_map(&maps.b, L->w_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, BN)) != SVDQ_OK) return st;
+    if ((st = make_map(&maps.b, L->w_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, b_rows)) != SVDQ_OK) return st;
+    if (pair && (st = make_map(&maps.y, Y, ydt, N, M, ldy * ysz, static_cast<uint32_t>(64 / ysz), 32,
+                               CU_TENSOR_MAP_SWIZZLE_64B)) != SVDQ_OK)
+      return st;
   } else {
     // packed int4 tiles [rows x 64 B] (two K groups), dense (no swizzle): unpacked in smem
     if ((st = make_map(&maps.a, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, K / 2, M, K / 2, 64, 128,
@@ -587,10 +593,9 @@ svdq_status svdq_gemm_w4a4_lowrank_up(const svdq_linear *L, const uint8_t *xq, c
   K2Prep k;
   svdq_status st = prepare_k2(L, xq, xs, xl1, M, Y, y_dtype, ldy, false, &k);
   if (st != SVDQ_OK) return st;
-  cudaError_t e = L->fmt == SVDQ_FMT_NVFP4
-                      ? (k.pair ? launch_k2_nvfp4_2sm(k.maps, k.sfa_map, k.sfb_map, k.p, k.bn, static_cast<cudaStream_t>(stream))
-                                : launch_k2_nvfp4(k.maps, k.p, static_cast<cudaStream_t>(stream)))
-                      : launch_k2_int4(k.maps, k.p, static_cast<cudaStream_t>(stream));
+  cudaError_t e = k.pair ? launch_k2_nvfp4_2sm(k.maps, k.sfa_map, k.sfb_map, k.p, k.bn, static_cast<cudaStream_t>(stream))
+                  : L->fmt == SVDQ_FMT_NVFP4 ? launch_k2_nvfp4(k.maps, k.p, static_cast<cudaStream_t>(stream))
+                                             : launch_k2_int4(k.maps, k.p, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported) return fail(SVDQ_ERR_UNSUPPORTED, "INT4 GEMM not built");
   if (e != cudaSuccess) return cuda_fail(e, "K2 launch");
   ++g_launches;

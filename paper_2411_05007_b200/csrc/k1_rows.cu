@@ -7,18 +7,21 @@
 //
 //   stage i = Q = 128 / RT consecutive 64-wide K blocks of the CTA's RT rows, staged by ONE 3-D TMA
 //             box {64 cols, Q blocks, RT rows} (128-B swizzle) as a [128 rows x 128 B] K-major tile
-//             whose row m * Q + q holds block q of row m;
-//   warp 0    TMA producer (X box, Q L1s tiles [r x 64], lambda_inv of the Q blocks);
+//             whose row m * Q + q holds block q of row m; X stages and L1s stages live in two rings;
+//   warp 0    X producer (X box + lambda_inv of the Q blocks; X ring, up to 12 deep);
 //   warp 1    TMEM allocator + MMA issuer: D[128 x Q*r] += A[128 x 64] . B[Q*r x 64]^T with
 //             B row q' * r + t = L1s[t, block q'] (tcgen05.mma kind::f16, fp32 in TMEM).  The
 //             diagonal entries D[m Q + q, q r + t] accumulate sum_k X[m, k] L1s[t, k] over the k of
 //             block q of every stage; the off-diagonal products are discarded (the MMA is ~1/3 of
 //             the HBM time, so the Q-fold extra tensor work is free);
-//   warps 2..17  quantizers, one 16-element NVFP4 group (a quarter of an INT4 group) per lane per
+//   warp 2    L1s producer (Q tiles [r x 64] per stage; L1s ring, 4 deep, fed from L2 after a
+//             distributed L2 prefetch of the whole L1s);
+//   warps 3..18  quantizers, one 16-element NVFP4 group (a quarter of an INT4 group) per lane per
 //             stage: x_hat = fl32(x * lambda_inv), App. B recipe bit-exact, codes + scales stored.
 //             fp16 X: they also split the tile into bf16 hi (in place) + lo parts, X = hi + lo
 //             exactly, and the MMA warp issues hi . L1s^T + lo . L1s^T (kind::f16 takes one type).
-//   tail      xl1[m, t] = bf16(sum_q D[m Q + q, q r + t]) in fixed q order (deterministic).
+//   tail      xl1[m, t] = bf16(sum_q D[m Q + q, q r + t]) in a fixed q order (deterministic), by
+//             warp shuffles straight out of TMEM.
 // X rows >= M are zero-filled by TMA, so the NVFP4 padding rows of the 128x4 scale layout get 0x00.
 #include <cstdint>
 #include <cstdlib>
@@ -54,11 +57,9 @@ namespace svdq {
 
 namespace {
 
-// Waits of the single-thread roles (producers, MMA issuer).  They share the SM sub-partitions'
-// issue slots with quantizer warps, so they wait with the suspend-time hint (the warp is parked
-// until the phase completes) instead of spinning: measured, the quantizer warps that shared a
-// scheduler with a spinning role warp fell ~3 stages behind the others over K = 15360, and the
-// slowest quantizer warp gates every slot release.
+// Waits of the single-thread roles (producers, MMA issuer): with the suspend-time hint, so a waiting
+// role warp does not take issue slots from the quantizer warps of its sub-partition (measured
+// neutral against spinning, SVDQ_K1_SPIN=1, on the FLUX shapes).
 #ifndef SVDQ_K1_SPIN
 #define SVDQ_K1_SPIN 0
 #endif
@@ -252,6 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
+    __syncwarp();                                        // reconverge before the block-wide barrier
   } else if (warp == 2) {
     // -------------------------------------------------------------------- L1s producer
     // L1s never depends on the previous kernel: the ring fills before griddepcontrol.wait
@@ -276,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
         if (++sw == SW) { sw = 0; wph ^= 1; }
       }
     }
+    __syncwarp();                                        // reconverge before the block-wide barrier
   } else if (warp == 1) {
     // -------------------------------------------------------------------- MMA issuer
     if (r) {
@@ -477,54 +480,64 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
   if (warp >= kQ0 && lane == 0) RTRACE(400 + warp - kQ0);
   if (r == 0) return;
   // ---------------------------------------------------------------------- xl1 = sum_q diag blocks
-  __syncthreads();                                             // every stage consumed: ring reusable
-  float *red = reinterpret_cast<float *>(smem);                // [Q][RT][r + 4] fp32 (<= 68 KB)
-  const int rs = r + 4;                                        // padded row stride: fewer bank conflicts
+  // No shared-memory round trip: a warp's 32 TMEM lanes are rows d = m Q + q of whole m (32 % Q == 0).
+  // The 16 quantizer warps split xl1's r columns into 8-column chunks (4 warps per lane quadrant,
+  // chunks qq, qq + 4, ...); for a chunk a warp loads it from every block q' (all loads, then one
+  // wait), each lane keeps the one of its own q (the diagonal), a butterfly over the Q lanes of a row
+  // sums them in a fixed order ((q0 + q1) + (q2 + q3) at Q = 4: deterministic), and lane q = 0 of
+  // the row stores the 8 columns.  The barrier first: the ring is no longer read by anyone.
+  __syncthreads();
+  if (threadIdx.x == 32 * kQ0) RTRACE(102);
   if (warp >= kQ0) {
-    // the 16 quantizer warps drain TMEM in parallel: 4 per lane quadrant, 16-column chunks
-    // c = qq, qq + 4, ...; a lane keeps the chunks of its own row's diagonal block
     const int qd = warp & 3;                                   // TMEM lane quadrant of this warp
     const int qq = (warp - kQ0) >> 2;                          // 0..3 within the quadrant
     const int d = 32 * qd + lane;                              // D row = m * Q + q
     const int q = d % Q, mm = d / Q;
-    mbar_wait(dfull, 0);
-    tc_fence_after();
-    for (int c = qq; c < Q * r / 16; c += 4) {
-      uint32_t v[16];
-      tmem_ld_32x32b_x16(tmem + (static_cast<uint32_t>(32 * qd) << 16) + 16 * c, v);
-      tmem_ld_wait();
-      const int blk = 16 * c / r;
-      if (blk == q) {                                          // the diagonal block of this lane's row
-        float *dst = red + (q * RT + mm) * rs + (16 * c - blk * r);
-#pragma unroll
-        for (int j = 0; j < 16; j += 4)
-          *reinterpret_cast<float4 *>(dst + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
-                                                             __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc_n(tmem, tcols);
-  for (int idx = threadIdx.x; idx < RT * (r / 2); idx += kThreads) {
-    const int mm = idx / (r / 2);
-    const int col = 2 * (idx % (r / 2));
-    float s0 = 0.f, s1 = 0.f;
-    for (int q = 0; q < Q; ++q) {                              // fixed block order: deterministic
-      const float2 v = *reinterpret_cast<const float2 *>(red + (q * RT + mm) * rs + col);
-      s0 += v.x;
-      s1 += v.y;
-    }
     const int64_t row = row0 + mm;
-    if (row < p.M) {
-      if (p.xl1_f32) {
-        for (int j = 0; j < p.ndst; ++j)
-          *reinterpret_cast<float2 *>(reinterpret_cast<uint8_t *>(p.xl1_f32 + row * r + col) + p.dst_delta[j]) =
-              make_float2(s0, s1);
+    const int nc8 = r / 8;
+    if (qq < nc8) {
+      mbar_wait(dfull, 0);
+      tc_fence_after();
+    }
+    if (threadIdx.x == 32 * kQ0) RTRACE(103);
+    for (int c8 = qq; c8 < nc8; c8 += 4) {
+      float val[8];
+      for (int q0 = 0; q0 < Q; q0 += 4) {
+        uint32_t v[4][8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (q0 + u < Q) tmem_ld_32x32b_x8(tmem + (static_cast<uint32_t>(32 * qd) << 16) + (q0 + u) * r + 8 * c8, v[u]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (q0 + u == q) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) val[j] = __uint_as_float(v[u][j]);
+          }
       }
-      else *reinterpret_cast<uint32_t *>(p.xl1 + row * r + col) = pack_bf16x2(s0, s1);
+      for (int off = 1; off < Q; off <<= 1) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) val[j] += __shfl_xor_sync(0xffffffffu, val[j], off);
+      }
+      if (q == 0 && row < p.M) {
+        const int64_t c = row * r + 8 * c8;
+        if (p.xl1_f32) {
+          for (int j = 0; j < p.ndst; ++j) {
+            float4 *dst = reinterpret_cast<float4 *>(reinterpret_cast<uint8_t *>(p.xl1_f32 + c) + p.dst_delta[j]);
+            dst[0] = make_float4(val[0], val[1], val[2], val[3]);
+            dst[1] = make_float4(val[4], val[5], val[6], val[7]);
+          }
+        } else {
+          *reinterpret_cast<uint4 *>(p.xl1 + c) = make_uint4(pack_bf16x2(val[0], val[1]), pack_bf16x2(val[2], val[3]),
+                                                             pack_bf16x2(val[4], val[5]), pack_bf16x2(val[6], val[7]));
+        }
+      }
     }
   }
+  if (threadIdx.x == 32 * kQ0) RTRACE(104);
+  tc_fence_before();
+  __syncthreads();                                             // every tcgen05.ld is done
+  if (warp == 1) tmem_dealloc_n(tmem, tcols);
   if (threadIdx.x == 32 * kQ0) RTRACE(101);
 }
 

@@ -91,6 +91,67 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tmem_acc_lane, const floa
   }
 }
 
+// W8A8 (the paper's 8-bit setting) epilogue of the CTA-pair kernel: the exact int32
+// accumulator of X_q W_q^T in TMEM columns [0, NCOLS) and the fp32 low-rank accumulator in
+// [lr_col, lr_col + NCOLS) of this warp's lanes:
+//   Y[m,n] = out_rn(fma(fl32(f32(acc[m,n]) * sx[m]), sw[n], lr[m,n]) + bias[n])
+// -- the 1-CTA kernel's formula, operation for operation (readings W2 / W3).  |acc| may exceed
+// 2^24 over a whole K: the int -> fp32 conversion rounds to nearest.  Block by block: the
+// accumulator is released after the last block's loads; staging / TMA stores as epilogue_tile.
+template <int NCOLS, int NWQ, int NBUF = 2, typename Release>
+__device__ __forceinline__ void epilogue_tile_w8(uint32_t tmem_acc_lane, uint32_t lr_col, bool has_lr,
+                                                 const float *bias_s, const float *sw_s, float sx, int y_dtype,
+                                                 const CUtensorMap *tmY, int32_t row0, int32_t col0, int sub,
+                                                 uint8_t *stage, int &buf, int lane, Release release) {
+  constexpr int NB = NCOLS / (32 * NWQ);
+  static_assert(NCOLS % (32 * NWQ) == 0, "column split");
+  const uint32_t sw = static_cast<uint32_t>((lane >> 1) & 3);
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const int cb = sub + i * NWQ;
+    uint32_t ra[32], rl[32];
+    tmem_ld_32x32b_x32(tmem_acc_lane + cb * 32, ra);
+    if (has_lr) tmem_ld_32x32b_x32(tmem_acc_lane + lr_col + cb * 32, rl);
+    tmem_ld_wait();
+    if (i == NB - 1) release();
+    const float *bs = bias_s + cb * 32;
+    const float *ws = sw_s + cb * 32;
+    float v[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      const float t = __fmul_rn(__int2float_rn(static_cast<int>(ra[e])), sx);
+      v[e] = __fadd_rn(__fmaf_rn(t, ws[e], has_lr ? __uint_as_float(rl[e]) : 0.f), bs[e]);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (y_dtype != 2 && h == 1) break;                  // 16-bit: one 64-B chunk per block
+      uint8_t *sb = stage + (NBUF == 2 ? buf * 2048 : 0);
+      if (lane == 0) bulk_wait_group_read<NBUF - 1>();   // the store that last used sb has read it
+      __syncwarp();
+      uint8_t *rowp = sb + lane * 64;
+      if (y_dtype == 2) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          *reinterpret_cast<float4 *>(rowp + ((c ^ sw) * 16)) =
+              make_float4(v[16 * h + 4 * c], v[16 * h + 4 * c + 1], v[16 * h + 4 * c + 2], v[16 * h + 4 * c + 3]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          *reinterpret_cast<uint4 *>(rowp + ((c ^ sw) * 16)) =
+              make_uint4(pack2(v[8 * c], v[8 * c + 1], y_dtype), pack2(v[8 * c + 2], v[8 * c + 3], y_dtype),
+                         pack2(v[8 * c + 4], v[8 * c + 5], y_dtype), pack2(v[8 * c + 6], v[8 * c + 7], y_dtype));
+      }
+      fence_proxy_async();                                 // generic smem writes -> TMA (async proxy)
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmY, sb, col0 + cb * 32 + h * 16, row0);
+        bulk_commit_group();
+      }
+      buf ^= 1;
+    }
+  }
+}
+
 // Direct variant: no shared-memory staging and no TMA store.  Lane l of the warp owns row
 // row0 + l; each 32-column block becomes 64 contiguous bytes of that row (four 16-byte
 // st.global, or eight for fp32), so every store fills whole 32-byte sectors.  Rows >= M and

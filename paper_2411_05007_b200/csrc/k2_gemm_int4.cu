@@ -273,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    __syncwarp();                                        // reconverge before the block-wide barrier
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc_i = idesc_s8(BM, BN);

@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(320, 1)
       if (blockIdx.x < 148) { g_k2_trace[blockIdx.x][0] = t_prod_wait; g_k2_trace[blockIdx.x][1] = clock64() - t_start; }
 #endif
     }
+    __syncwarp();                                        // reconverge before the block-wide barrier
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc_q = idesc_nvfp4(128, BN);

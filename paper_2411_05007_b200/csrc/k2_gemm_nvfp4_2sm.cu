@@ -53,17 +53,20 @@ namespace {
 // 64 rows of the N = 128 MMA] (three 64-row TMA boxes); the scale-factor rows are three atoms.
 constexpr int A_BYTES = 128 * 128;            // 16 KB
 constexpr int SFA_BYTES = 2048;
-template <int kBN>
+template <int kBN, bool kW8 = false>
 struct PC {
   static constexpr int BN = kBN;
   static constexpr int BNH = kBN / 2;                       // B rows per CTA
-  static constexpr int NATOM = kBN == 384 ? 3 : 2;          // 128-row SFB atoms staged per stage
+  static constexpr int NATOM = kW8 ? 0 : (kBN == 384 ? 3 : 2);   // 128-row SFB atoms staged per stage
   static constexpr int B_BYTES = BNH * 128;                 // 12 / 16 / 24 KB
   static constexpr int SFB_BYTES = NATOM * 2048;            // atoms x 4 K-blocks x 512 B
-  static constexpr int STAGE = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;   // 34 / 38 / 48 KB
-  static constexpr int ACC = kBN == 192 ? 2 : 1;            // accumulator buffers
-  static constexpr int SF_COLS = 16 + 16 * NATOM;           // TMEM columns per SF slot (SFA + SFB, 4 K-blocks)
+  static constexpr int STAGE = A_BYTES + B_BYTES + (kW8 ? 0 : SFA_BYTES + SFB_BYTES);   // 34 / 38 / 48; W8A8 28 KB
+  static constexpr int ACC = kBN == 192 && !kW8 ? 2 : 1;    // accumulator buffers
+  static constexpr int SF_COLS = kW8 ? 0 : 16 + 16 * NATOM; // TMEM columns per SF slot (SFA + SFB, 4 K-blocks)
   static constexpr int SF_BASE = ACC * kBN;
+  // W8A8: the int32 accumulator of X_q W_q^T in [0, BN) and the fp32 low-rank accumulator in
+  // [BN, 2 BN) (an int32 and an fp32 product cannot share one accumulator)
+  static constexpr int LR_COL = kW8 ? kBN : 0;
   static constexpr int BLOAD = kBN == 384 ? 64 : BNH;       // rows per B / L2s TMA box
 };
 constexpr int BN = 192;                       // the fused (layer-boundary) variant's tile N
@@ -103,16 +106,16 @@ constexpr int EPI_BYTES = SVDQ_BIGSTORE && 3 * 16384 > 8 * 2048 * kEpiBuf ? 3 * 
 // Shared-memory layout per variant.  Fused launches (layer-boundary fusion) run a 4-stage ring
 // and add the tile's lambda_inv_next [192] fp32, the a tile (3 x [128 rows x 128 B], SW128) and
 // this CTA's half of the L1s_next rows (3 x [r/2 rows x 128 B], SW128) for the X L1s_next^T MMA.
-template <bool kFuse, int kBN = 192>
+template <bool kFuse, int kBN = 192, bool kW8 = false>
 struct Lay {
   static constexpr int BN = kBN;
-  static constexpr int stages = kFuse ? 3 : (kBN == 384 ? SVDQ_K2P384_STAGES : kStages);
+  static constexpr int stages = kFuse ? 3 : (kBN == 384 ? SVDQ_K2P384_STAGES : (kW8 ? 6 : kStages));
   // epilogue warps per CTA (2-4 per TMEM lane quadrant); at 384 columns 4 (3 x 32 columns per warp:
   // the 96-register drain fits the 112 registers 576 threads allow)
   static constexpr int epi_w = kFuse ? 12 : (kBN == 384 ? 16 : SVDQ_K2P_EPIW);
   static constexpr int epibuf = kBN == 384 ? 1 : kEpiBuf;   // 2 KB staging buffers per epilogue warp
   static constexpr int threads = 64 + 32 * epi_w;
-  static constexpr int epi_off = stages * PC<kBN>::STAGE;
+  static constexpr int epi_off = stages * PC<kBN, kW8>::STAGE;
   static constexpr int bar_off = epi_off + (epi_w != 8 ? epi_w * 2048 * epibuf : EPI_BYTES);
   static constexpr int bias_off = bar_off + 256;
   static constexpr int lamn_off = bias_off + BN * 4;
@@ -120,11 +123,13 @@ struct Lay {
   static constexpr int bt_off = at_off + 3 * 16384;         // L1s_next half: 3 x 2 KB (r <= 32)
   static constexpr int cs_off = bt_off + 3 * 2048;          // next-layer codes, [128 rows x 96 B]
   static constexpr int sfs_off = cs_off + 128 * 96;         // next-layer scale factors, 3 x 512 B
-  static constexpr int smem = kFuse ? sfs_off + 3 * 512 + 1024 : bias_off + BN * 4 + 1024;
+  static constexpr int sw_off = bias_off + BN * 4;          // W8A8: the tile's per-channel weight scales
+  static constexpr int smem = kFuse ? sfs_off + 3 * 512 + 1024 : bias_off + (kW8 ? 2 : 1) * BN * 4 + 1024;
 };
 constexpr int XL1_COL = PC<192>::SF_BASE + 2 * PC<192>::SF_COLS;   // TMEM columns [480, 512): X L1s_next^T accumulator
 static_assert(XL1_COL + 32 <= 512, "TMEM budget (fused)");
-static_assert(PC<192>::STAGE % 1024 == 0 && PC<256>::STAGE % 1024 == 0 && PC<384>::STAGE % 1024 == 0, "stage alignment");
+static_assert(PC<192>::STAGE % 1024 == 0 && PC<256>::STAGE % 1024 == 0 && PC<384>::STAGE % 1024 == 0 &&
+              PC<192, true>::STAGE % 1024 == 0, "stage alignment");
 static_assert(PC<192>::SF_BASE + 2 * PC<192>::SF_COLS <= 512 && PC<256>::SF_BASE + 2 * PC<256>::SF_COLS <= 512 &&
               PC<384>::SF_BASE + 2 * PC<384>::SF_COLS <= 512, "TMEM budget");
 
@@ -174,18 +179,22 @@ __device__ __forceinline__ TileRef locate(const K2PairArgs &g, int t) {
   return TileRef{i, static_cast<int64_t>(lt % mt) * 256, static_cast<int64_t>(lt / mt) * BN};
 }
 
-template <bool kFuse, int kBN>
-__global__ void __launch_bounds__(Lay<kFuse, kBN>::threads, 1)
+// kW8: the paper's 8-bit setting (SVDQ_FMT_W8A8) on the same CTA-pair skeleton:
+// kind::i8 over the whole K into an exact int32 accumulator, the low-rank slab into a separate fp32
+// accumulator, scales applied once per tile in the epilogue (epilogue_tile_w8).
+template <bool kFuse, int kBN, bool kW8 = false>
+__global__ void __launch_bounds__(Lay<kFuse, kBN, kW8>::threads, 1)
     k2_nvfp4_2sm_kernel(const __grid_constant__ K2PairArgs g) {
-  constexpr int BN = kBN, BNH = PC<kBN>::BNH, B_BYTES = PC<kBN>::B_BYTES, STAGE = PC<kBN>::STAGE;
-  constexpr int SF_BASE = PC<kBN>::SF_BASE, ACC = PC<kBN>::ACC, SF_COLS = PC<kBN>::SF_COLS;
-  constexpr int NATOM = PC<kBN>::NATOM, SFB_BYTES = PC<kBN>::SFB_BYTES;
-  (void)SFB_BYTES;
+  using PCK = PC<kBN, kW8>;
+  constexpr int BN = kBN, BNH = PCK::BNH, B_BYTES = PCK::B_BYTES, STAGE = PCK::STAGE;
+  constexpr int SF_BASE = PCK::SF_BASE, ACC = PCK::ACC, SF_COLS = PCK::SF_COLS;
+  constexpr int NATOM = PCK::NATOM, LR_COL = PCK::LR_COL;
   static_assert(!kFuse || kBN == 192, "the fused variant runs 192-wide tiles");
+  static_assert(!kW8 || (kBN == 192 && !kFuse), "W8A8 runs plain 192-wide tiles");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~static_cast<uintptr_t>(1023));
-  using LY = Lay<kFuse, kBN>;
+  using LY = Lay<kFuse, kBN, kW8>;
   constexpr int kSt = LY::stages;
   constexpr int kEpiW = LY::epi_w, kNWQ = kEpiW / 4, kEpiT = 32 * kEpiW;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + LY::bar_off);
@@ -208,7 +217,8 @@ __global__ void __launch_bounds__(Lay<kFuse, kBN>::threads, 1)
   const int t_first = g.contig ? static_cast<int>(static_cast<int64_t>(pair) * tiles / npairs) : pair;
   const int t_end = g.contig ? static_cast<int>(static_cast<int64_t>(pair + 1) * tiles / npairs) : tiles;
   const int t_step = g.contig ? 1 : npairs;
-  auto nkt_of = [&](int i) { return static_cast<int>((g.pr[i].p.K / 64 + 3) / 4); };
+  // K steps per tile: 128-byte rows of packed codes = 256 FP4 or 128 int8 elements
+  auto nkt_of = [&](int i) { return static_cast<int>(kW8 ? (g.pr[i].p.K + 127) / 128 : (g.pr[i].p.K / 64 + 3) / 4); };
   auto nslab_of = [&](int i) { return (g.pr[i].p.rank + 63) / 64; };
 
   if (threadIdx.x == 0) {
@@ -230,8 +240,10 @@ __global__ void __launch_bounds__(Lay<kFuse, kBN>::threads, 1)
     for (int i = 0; i < g.n; ++i) {
       tma_prefetch(&g.pr[i].a);
       tma_prefetch(&g.pr[i].b);
-      tma_prefetch(&g.pr[i].sfa);
-      tma_prefetch(&g.pr[i].sfb);
+      if (!kW8) {
+        tma_prefetch(&g.pr[i].sfa);
+        tma_prefetch(&g.pr[i].sfb);
+      }
       if (nslab_of(i)) {
         tma_prefetch(&g.pr[i].xl1);
         tma_prefetch(&g.pr[i].l2);
@@ -276,8 +288,9 @@ __global__ void __launch_bounds__(Lay<kFuse, kBN>::threads, 1)
           const uint32_t fb = full0 + kt * 8;
           if (crank == 0) mbar_arrive_expect_tx(&full[kt], 2 * STAGE);
           load_bside(st + A_BYTES, &pr.b, fb, kt * 128, tr.n0);
-          tma_load_3d_cg2(st + A_BYTES + B_BYTES + SFA_BYTES, &pr.sfb, fb, 0, kt * 4,
-                          static_cast<int32_t>(tr.n0 / 128));
+          if (!kW8)
+            tma_load_3d_cg2(st + A_BYTES + B_BYTES + SFA_BYTES, &pr.sfb, fb, 0, kt * 4,
+                            static_cast<int32_t>(tr.n0 / 128));
         }
       }
       griddep_wait();                                    // xq / xs / xl1 come from K1
@@ -295,7 +308,8 @@ __global__ void __launch_bounds__(Lay<kFuse, kBN>::threads, 1)
           const uint32_t fb = full0 + s * 8;
           if (first && kt < pre) {                         // B / SFB already in flight
             tma_load_2d_cg2(st, &pr.a, fb, kt * 128, ma);
-            tma_load_3d_cg2(st + A_BYTES + B_BYTES, &pr.sfa, fb, 0, kt * 4, static_cast<int32_t>(m0 / 128 + crank));
+            if (!kW8)
+              tma_load_3d_cg2(st + A_BYTES + B_BYTES, &pr.sfa, fb, 0, kt * 4, static_cast<int32_t>(m0 / 128 + crank));
             if (++s == kSt) { s = 0; ph ^= 1; }
             continue;
           }
@@ -308,9 +322,11 @@ __global__ void __launch_bounds__(Lay<kFuse, kBN>::threads, 1)
           if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE);
           tma_load_2d_cg2(st, &pr.a, fb, kt * 128, ma);
           load_bside(st + A_BYTES, &pr.b, fb, kt * 128, n0);
-          tma_load_3d_cg2(st + A_BYTES + B_BYTES, &pr.sfa, fb, 0, kt * 4, static_cast<int32_t>(m0 / 128 + crank));
-          tma_load_3d_cg2(st + A_BYTES + B_BYTES + SFA_BYTES, &pr.sfb, fb, 0, kt * 4,
-                          static_cast<int32_t>(n0 / 128));
+          if (!kW8) {
+            tma_load_3d_cg2(st + A_BYTES + B_BYTES, &pr.sfa, fb, 0, kt * 4, static_cast<int32_t>(m0 / 128 + crank));
+            tma_load_3d_cg2(st + A_BYTES + B_BYTES + SFA_BYTES, &pr.sfb, fb, 0, kt * 4,
+                            static_cast<int32_t>(n0 / 128));
+          }
           if (++s == kSt) { s = 0; ph ^= 1; }
         }
         first = false;
@@ -328,6 +344,7 @@ __global__ void __launch_bounds__(Lay<kFuse, kBN>::threads, 1)
       if (crank == 0 && pair < 148) g_k2p_trace[pair][6] = t_pwait;
 #endif
     }
+    __syncwarp();                                        // reconverge before the block-wide barrier
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader)
     if (crank == 0) {
@@ -416,7 +433,11 @@ __global__ void __launch_bounds__(Lay<kFuse, kBN>::threads, 1)
                 mma_nvfp4_cg2(d_tmem + 256, a_d + 2 * i, b2_d + 2 * i, idesc_q2, sfa_col + 4 * i,
                               sfb_col + 4 * NATOM * i + 8, (kt | i) != 0);
             };
-            if (nsub == 4) {
+            if constexpr (kW8) {                     // 128 int8 of K per stage: 4 x K32
+#pragma unroll
+              for (int h = 0; h < 4; ++h)
+                mma_s8_cg2(d_tmem, a_d + 2 * h, b_d + 2 * h, idesc_s8(256, BN), (kt | h) != 0);
+            } else if (nsub == 4) {
 #pragma unroll
               for (int i = 0; i < 4; ++i) sf_copy(i);
 #pragma unroll
@@ -440,8 +461,10 @@ __global__ void __launch_bounds__(Lay<kFuse, kBN>::threads, 1)
             const uint32_t b_addr = smem_u32(st + A_BYTES);
             const int nk16 = min(4, (rank - j * 64) / 16);
             for (int i = 0; i < nk16; ++i) {
-              mma_bf16_cg2(d_tmem, sdesc_kmajor_sw128(a_addr + 32 * i), sdesc_kmajor_sw128(b_addr + 32 * i),
-                           idesc_h, (nkt > 0 || j > 0 || i > 0) ? 1u : 0u);
+              // NVFP4: into the same accumulator (after the K loop); W8A8: its own fp32 accumulator
+              const uint32_t acc_in = ((!kW8 && nkt > 0) || j > 0 || i > 0) ? 1u : 0u;
+              mma_bf16_cg2(d_tmem + LR_COL, sdesc_kmajor_sw128(a_addr + 32 * i), sdesc_kmajor_sw128(b_addr + 32 * i),
+                           idesc_h, acc_in);
               if constexpr (kBN == 384)
                 mma_bf16_cg2(d_tmem + 256, sdesc_kmajor_sw128(a_addr + 32 * i),
                              sdesc_kmajor_sw128(b_addr + B2_OFF + 32 * i), idesc_h2, (nkt > 0 || j > 0 || i > 0) ? 1u : 0u);
@@ -501,6 +524,10 @@ __global__ void __launch_bounds__(Lay<kFuse, kBN>::threads, 1)
       named_bar(1, kEpiT);
       for (int c = et; c < BN; c += kEpiT)
         bias_s[c] = (p.bias && n0 + c < p.N) ? load_bias(p.bias, p.bias_dtype, n0 + c) : 0.f;
+      if constexpr (kW8) {                               // per-channel weight scales of the tile
+        float *sw_s = reinterpret_cast<float *>(smem + LY::sw_off);
+        for (int c = et; c < BN; c += kEpiT) sw_s[c] = n0 + c < p.N ? reinterpret_cast<const float *>(p.sfb)[n0 + c] : 0.f;
+      }
       const bool fx = kFuse && p.fuse && p.nx_r > 0;   // this tile feeds the X L1s_next^T MMA
       if constexpr (kFuse) {
         if (p.fuse) {
@@ -657,6 +684,20 @@ __global__ void __launch_bounds__(Lay<kFuse, kBN>::threads, 1)
           continue;
         }
       }
+      if constexpr (kW8) {
+        const int64_t grow = m0 + quad * 32 + lane;       // per-token activation scale of this lane's row
+        const float sx = grow < p.M ? reinterpret_cast<const float *>(p.sfa)[grow] : 0.f;
+        epilogue_tile_w8<BN, kNWQ, LY::epibuf>(tmem + (static_cast<uint32_t>(quad * 32) << 16), LR_COL, p.rank > 0,
+                                               bias_s, reinterpret_cast<const float *>(smem + LY::sw_off), sx,
+                                               p.y_dtype, tmY, static_cast<int32_t>(m0 + quad * 32),
+                                               static_cast<int32_t>(n0), (warp - 2) >> 2,
+                                               smem + LY::epi_off + (warp - 2) * 2048 * LY::epibuf, ebuf, lane, [&]() {
+                                                 tc_fence_before();
+                                                 __syncwarp();
+                                                 if (lane == 0) K2_ACC_RELEASE(acc_empty0);
+                                               });
+        continue;
+      }
       epilogue_tile<BN, kNWQ, LY::epibuf>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
                            tmY, static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
                            smem + LY::epi_off + (warp - 2) * 2048 * LY::epibuf, ebuf, lane, [&]() {
@@ -683,13 +724,13 @@ __global__ void __launch_bounds__(Lay<kFuse, kBN>::threads, 1)
 }  // namespace
 
 namespace {
-template <int kBN>
+template <int kBN, bool kW8 = false>
 cudaError_t launch_plain(const K2PairArgs &g, int64_t pairs, cudaStream_t s) {
-  using LY = Lay<false, kBN>;
-  cudaError_t e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<false, kBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       LY::smem);
+  using LY = Lay<false, kBN, kW8>;
+  cudaError_t e = cudaFuncSetAttribute(k2_nvfp4_2sm_kernel<false, kBN, kW8>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, LY::smem);
   if (e != cudaSuccess) return e;
-  return launch_ex(k2_nvfp4_2sm_kernel<false, kBN>, dim3(static_cast<unsigned>(2 * pairs)), dim3(LY::threads),
+  return launch_ex(k2_nvfp4_2sm_kernel<false, kBN, kW8>, dim3(static_cast<unsigned>(2 * pairs)), dim3(LY::threads),
                    LY::smem, s, 2u, g);
 }
 }  // namespace
@@ -698,9 +739,13 @@ cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
   static_assert(Lay<false, 192>::smem <= 227 * 1024 && Lay<false, 256>::smem <= 227 * 1024 &&
                 Lay<false, 384>::smem <= 227 * 1024, "smem budget");
   static_assert(Lay<true>::smem <= 227 * 1024, "smem budget (fused)");
-  bool fuse = false;
-  for (int i = 0; i < g.n; ++i) fuse = fuse || g.pr[i].p.fuse;
-  const int bn = fuse ? 192 : (g.bn == 384 || g.bn == 256 ? g.bn : 192);
+  static_assert(Lay<false, 192, true>::smem <= 227 * 1024, "smem budget (W8A8)");
+  bool fuse = false, w8 = false;
+  for (int i = 0; i < g.n; ++i) {
+    fuse = fuse || g.pr[i].p.fuse;
+    w8 = w8 || g.pr[i].p.w8;
+  }
+  const int bn = fuse || w8 ? 192 : (g.bn == 384 || g.bn == 256 ? g.bn : 192);
   g.bn = bn;
   g.tile_begin[0] = 0;
   for (int i = 0; i < g.n; ++i)
@@ -717,6 +762,7 @@ cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
     return launch_ex(k2_nvfp4_2sm_kernel<true, 192>, dim3(static_cast<unsigned>(2 * pairs)), dim3(Lay<true>::threads),
                      Lay<true>::smem, s, 2u, g);
   }
+  if (w8) return launch_plain<192, true>(g, pairs, s);
   if (bn == 384) return launch_plain<384>(g, pairs, s);
   if (bn == 256) return launch_plain<256>(g, pairs, s);
   return launch_plain<192>(g, pairs, s);

@@ -105,3 +105,16 @@ def test_w8a8_config_layer_sampled(name):
     np.testing.assert_array_equal(xq.cpu().numpy().reshape(M, K)[rows], qa.codes.astype(np.int8).view(np.uint8))
     y_ref = S.round_output(S.gemm_reference(qa, ops), dt)
     assert rel_fro(Y.float().cpu().numpy()[rows], y_ref) <= 1e-3
+
+
+def test_w8a8_pair_kernel_forced():
+    """The CTA-pair kind::i8 K2 (256 x 192 tiles, separate fp32 low-rank accumulator) on the
+    parity cases above, forced for every M > 128 (SVDQ_K2_PAIR=1 is read once per process)."""
+    import os, subprocess, sys
+    need_cuda()
+    env = dict(os.environ, SVDQ_K2_PAIR="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        f"{__file__}::test_w8a8_k1_k2_parity"], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "8 passed" in r.stdout, r.stdout[-500:]

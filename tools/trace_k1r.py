@@ -30,5 +30,5 @@ print("L1s issue times:", " ".join(f"{rel(200 + i):.2f}" for i in range(64) if t
 print("MMA passes waits:", " ".join(f"{rel(300 + i):.2f}" for i in range(64) if t[300 + i] >= t[0]))
 print("quantizer warps at stage nsteps/2:", " ".join(f"{rel(420 + i):.2f}" for i in range(16)))
 print("quantizer warps done:", " ".join(f"{rel(400 + i):.2f}" for i in range(16)))
-print(f"all quantizers done (tail sync) {rel(102):.2f}")
+print(f"tail: sync1 {rel(102):.2f}  dfull {rel(103):.2f}  drained {rel(104):.2f}  sync2 {rel(105):.2f}  stored {rel(101):.2f}")
 print(f"quantizer 0 done {rel(100):.2f}  xl1 stored {rel(101):.2f}")
