@@ -91,6 +91,101 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tmem_acc_lane, const floa
   }
 }
 
+// epilogue_tile for wide tiles (4 column blocks per warp, e.g. 384 columns over 3 warps per lane
+// quadrant) within a 128-register budget: the first two blocks are loaded, scaled and packed to
+// 16-bit pairs (16 registers each) before the last two are loaded; the accumulator is released
+// after the last load, then all four blocks are staged and stored.  fp32 Y: block by block.
+template <int NCOLS, int NWQ, int NBUF, typename Release>
+__device__ __forceinline__ void epilogue_tile_wide(uint32_t tmem_acc_lane, const float *bias_s, float alpha, int y_dtype,
+                                                   const CUtensorMap *tmY, int32_t row0, int32_t col0, int sub,
+                                                   uint8_t *stage, int &buf, int lane, Release release) {
+  constexpr int NB = NCOLS / (32 * NWQ);
+  static_assert(NCOLS % (32 * NWQ) == 0 && NB == 4, "four column blocks per warp");
+  const uint32_t sw = static_cast<uint32_t>((lane >> 1) & 3);
+  auto stage_store = [&](int cb, int h, auto &&write_row) {
+    uint8_t *sb = stage + (NBUF == 2 ? buf * 2048 : 0);
+    if (lane == 0) bulk_wait_group_read<NBUF - 1>();     // the store that last used sb has read it
+    __syncwarp();
+    write_row(sb + lane * 64);
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmY, sb, col0 + cb * 32 + h * 16, row0);
+      bulk_commit_group();
+    }
+    buf ^= 1;
+  };
+  if (y_dtype == 2) {
+#pragma unroll 1
+    for (int i = 0; i < NB; ++i) {
+      const int cb = sub + i * NWQ;
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem_acc_lane + cb * 32, r);
+      tmem_ld_wait();
+      if (i == NB - 1) release();
+      const float *bs = bias_s + cb * 32;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        stage_store(cb, h, [&](uint8_t *rowp) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int j = 16 * h + 4 * c;
+            *reinterpret_cast<float4 *>(rowp + ((c ^ sw) * 16)) =
+                make_float4(__fadd_rn(__fmul_rn(alpha, __uint_as_float(r[j + 0])), bs[j + 0]),
+                            __fadd_rn(__fmul_rn(alpha, __uint_as_float(r[j + 1])), bs[j + 1]),
+                            __fadd_rn(__fmul_rn(alpha, __uint_as_float(r[j + 2])), bs[j + 2]),
+                            __fadd_rn(__fmul_rn(alpha, __uint_as_float(r[j + 3])), bs[j + 3]));
+          }
+        });
+    }
+    return;
+  }
+  uint32_t pk[2][16];
+  {
+    uint32_t r[2][32];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) tmem_ld_32x32b_x32(tmem_acc_lane + (sub + i * NWQ) * 32, r[i]);
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float *bs = bias_s + (sub + i * NWQ) * 32;
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        pk[i][e] = pack2(__fadd_rn(__fmul_rn(alpha, __uint_as_float(r[i][2 * e])), bs[2 * e]),
+                         __fadd_rn(__fmul_rn(alpha, __uint_as_float(r[i][2 * e + 1])), bs[2 * e + 1]), y_dtype);
+    }
+  }
+  uint32_t r2[2][32];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) tmem_ld_32x32b_x32(tmem_acc_lane + (sub + (2 + i) * NWQ) * 32, r2[i]);
+  tmem_ld_wait();
+  release();
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+    stage_store(sub + i * NWQ, 0, [&](uint8_t *rowp) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4 *>(rowp + ((c ^ sw) * 16)) =
+            make_uint4(pk[i][4 * c], pk[i][4 * c + 1], pk[i][4 * c + 2], pk[i][4 * c + 3]);
+    });
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int cb = sub + (2 + i) * NWQ;
+    const float *bs = bias_s + cb * 32;
+    stage_store(cb, 0, [&](uint8_t *rowp) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = __fadd_rn(__fmul_rn(alpha, __uint_as_float(r2[i][8 * c + e])), bs[8 * c + e]);
+        *reinterpret_cast<uint4 *>(rowp + ((c ^ sw) * 16)) =
+            make_uint4(pack2(o[0], o[1], y_dtype), pack2(o[2], o[3], y_dtype), pack2(o[4], o[5], y_dtype),
+                       pack2(o[6], o[7], y_dtype));
+      }
+    });
+  }
+}
+
 // W8A8 (the paper's 8-bit setting) epilogue of the CTA-pair kernel: the exact int32
 // accumulator of X_q W_q^T in TMEM columns [0, NCOLS) and the fp32 low-rank accumulator in
 // [lr_col, lr_col + NCOLS) of this warp's lanes:

@@ -95,7 +95,7 @@ constexpr int BN = 192;                       // the fused (layer-boundary) vari
 constexpr int kStages = SVDQ_K2P_STAGES;
 constexpr int kEpiBuf = SVDQ_K2P_EPIBUF;      // 2 KB staging buffers per epilogue warp
 #ifndef SVDQ_K2P384_STAGES
-#define SVDQ_K2P384_STAGES 4                  // 384-wide tile: 4 x 48 KB stages, 16 epilogue warps x 1 buffer
+#define SVDQ_K2P384_STAGES 4                  // 384-wide tile: 4 x 48 KB stages, 12 epilogue warps x 1 buffer
 #endif
 #ifndef SVDQ_BIGSTORE
 #define SVDQ_BIGSTORE 0
@@ -110,9 +110,9 @@ template <bool kFuse, int kBN = 192, bool kW8 = false>
 struct Lay {
   static constexpr int BN = kBN;
   static constexpr int stages = kFuse ? 3 : (kBN == 384 ? SVDQ_K2P384_STAGES : (kW8 ? 6 : kStages));
-  // epilogue warps per CTA (2-4 per TMEM lane quadrant); at 384 columns 4 (3 x 32 columns per warp:
-  // the 96-register drain fits the 112 registers 576 threads allow)
-  static constexpr int epi_w = kFuse ? 12 : (kBN == 384 ? 16 : SVDQ_K2P_EPIW);
+  // epilogue warps per CTA (2 or 3 per TMEM lane quadrant); 384 columns: 3 (4 x 32 columns per warp,
+  // drained by epilogue_tile_wide within the 128 registers 448 threads allow)
+  static constexpr int epi_w = kFuse || kBN == 384 ? 12 : SVDQ_K2P_EPIW;
   static constexpr int epibuf = kBN == 384 ? 1 : kEpiBuf;   // 2 KB staging buffers per epilogue warp
   static constexpr int threads = 64 + 32 * epi_w;
   static constexpr int epi_off = stages * PC<kBN, kW8>::STAGE;
@@ -698,6 +698,17 @@ __global__ void __launch_bounds__(Lay<kFuse, kBN, kW8>::threads, 1)
                                                });
         continue;
       }
+      if constexpr (kBN == 384) {
+        epilogue_tile_wide<BN, kNWQ, LY::epibuf>(tmem + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha,
+                                                 p.y_dtype, tmY, static_cast<int32_t>(m0 + quad * 32),
+                                                 static_cast<int32_t>(n0), (warp - 2) >> 2,
+                                                 smem + LY::epi_off + (warp - 2) * 2048 * LY::epibuf, ebuf, lane, [&]() {
+                                                   tc_fence_before();
+                                                   __syncwarp();
+                                                   if (lane == 0) K2_ACC_RELEASE(acc_empty0);
+                                                 });
+        continue;
+      }
       epilogue_tile<BN, kNWQ, LY::epibuf>(tmem + b * BN + (static_cast<uint32_t>(quad * 32) << 16), bias_s, p.alpha, p.y_dtype,
                            tmY, static_cast<int32_t>(m0 + quad * 32), static_cast<int32_t>(n0), (warp - 2) >> 2,
                            smem + LY::epi_off + (warp - 2) * 2048 * LY::epibuf, ebuf, lane, [&]() {
@@ -769,11 +780,11 @@ cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
 }
 
 int k2_pair_bn(int64_t N) {
-  // 256 when it divides N.  The 384-wide tile is built and correct but measured slower on every FLUX
-  // shape (linear1 143 vs 121 us, linear2 78 vs 72 us): its mainloop + TMEM drain alone matches the
-  // 256 tile (94.5 vs 95.5 us, SVDQ_EXP=32) -- the operand stream is not the limit -- while its
-  // epilogue (16 warps x 1 staging buffer, 384 columns behind one accumulator) is not hidden.
-  // SVDQ_K2_BN=384 opts in; SVDQ_K2_BN=192 caps at 192 (A/B).
+  // 256 when it divides N.  The 384-wide tile is built and correct but measured no faster on the
+  // FLUX shapes (linear1 126 vs 123 us, qkv 53 vs 49 us with 6 vs 8 waves, linear2 74.3 vs 73.5 us):
+  // its 16 % fewer operand bytes per FLOP are offset by the 4- instead of 5-deep ring and the
+  // longer single-accumulator drain (clock64 trace: MMA waits on operands 22 % of the time at both
+  // widths).  SVDQ_K2_BN=384 opts in; SVDQ_K2_BN=192 caps at 192 (A/B).
   static const int cap = [] { const char *e = std::getenv("SVDQ_K2_BN"); return e ? std::atoi(e) : 256; }();
   if (cap >= 384 && N % 384 == 0) return 384;
   if (cap >= 256 && N % 256 == 0) return 256;
