@@ -35,20 +35,30 @@ for r in rows[2:]:
             d[k] = float(v)
     launches.append(d)
 layers = synth.flux_double_block(1) + synth.flux_single_block(1)
+by = {L.name: L for L in layers}
+# the step's launch groups (bench.flux_step_grouped): img + txt of each double-block kind, then the single block
+groups = [[by[f"double_{s_}_{k}"] for s_ in ("img", "txt")] for k in ("qkv", "proj", "mlp_up", "mlp_down")]
+groups += [[by["single_linear1"]], [by["single_linear2"]]]
 k2 = [d for d in launches if "k2_" in d["Kernel Name"]]
 k1 = [d for d in launches if "k1_" in d["Kernel Name"]]
+if len(k2) == len(layers):                       # serial form (one launch per linear)
+    groups = [[L] for L in layers]
 alg = []
-for L, d in zip(layers, k2):
-    alg_bytes = 0.5625 * (L.M + L.N) * L.K + 2 * (L.M + L.N) * L.r + 2 * L.N + 2 * L.M * L.N
-    d["layer"] = L.name
+for grp, d, d1 in zip(groups, k2, k1):
+    alg_bytes = sum(0.5625 * (L.M + L.N) * L.K + 2 * (L.M + L.N) * L.r + 2 * L.N + 2 * L.M * L.N for L in grp)
+    k1_bytes = sum(L.M * L.K * 2.5625 + 2 * L.M * L.r for L in grp)
+    d["layer"] = "+".join(L.name for L in grp)
     d["algorithmic_min_bytes"] = alg_bytes
-    d["algorithmic_flops"] = 2.0 * L.M * L.N * L.K
+    d["algorithmic_flops"] = sum(2.0 * L.M * L.N * L.K for L in grp)
     d["tflops_under_ncu"] = d["algorithmic_flops"] / (d["gpu__time_duration.sum"] * 1e-6) / 1e12
+    d1["layer"] = d["layer"]
+    d1["algorithmic_bytes"] = k1_bytes
+    d1["tbs_under_ncu"] = k1_bytes / (d1["gpu__time_duration.sum"] * 1e-6) / 1e12
     alg.append(alg_bytes)
 traffic = [d["dram__bytes_read_bytes"] + d["dram__bytes_write_bytes"] for d in k2]
 summary = {
     "source": os.path.basename(rep),
-    "note": "ncu --set full --clock-control none; one bench step (20 launches, CUDA-graph replay). "
+    "note": "ncu --set full --clock-control none; one grouped bench step (tools/step_once.py: 6 K1 + 6 K2 launches). "
             "Per-launch times are cold-cache and serialised: compare shares, not absolutes.",
     "k2_traffic_bytes_per_launch_mean": sum(traffic) / max(1, len(traffic)),
     "k2_algorithmic_min_bytes_per_launch_mean": sum(alg) / max(1, len(alg)),
@@ -60,9 +70,12 @@ json.dump(summary, open(os.path.join(outdir, "ncu_full_summary.json"), "w"), ind
 json.dump({"bytes_per_launch": round(summary["k2_traffic_bytes_per_launch_mean"]),
            "algorithmic_min_bytes_per_launch": round(summary["k2_algorithmic_min_bytes_per_launch_mean"]),
            "source": f"{outdir}/ncu_full_summary.json",
-           "definition": "mean over the step's 10 K2 launches of dram__bytes_read.sum + dram__bytes_write.sum"},
+           "definition": "mean over the step's K2 launches of dram__bytes_read.sum + dram__bytes_write.sum"},
           open(os.path.join(os.path.dirname(outdir.rstrip('/')), "k2_traffic.json"), "w"), indent=1)
 print(json.dumps({k: v for k, v in summary.items() if k != "launches"}, indent=1))
 for d in k2:
-    print(f"{d['layer']:22s} {d['gpu__time_duration.sum']:8.1f} us  tensor {d.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active', 0):5.1f}%  "
+    print(f"K2 {d["layer"]:40s} {d['gpu__time_duration.sum']:8.1f} us  tensor {d.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active', 0):5.1f}%  "
           f"dram {(d['dram__bytes_read_bytes'] + d['dram__bytes_write_bytes'])/1e6:7.1f} MB  alg {d['algorithmic_min_bytes']/1e6:7.1f} MB")
+for d in k1:
+    print(f"K1 {d.get('layer', '?'):40s} {d['gpu__time_duration.sum']:8.1f} us  dram {(d['dram__bytes_read_bytes'] + d['dram__bytes_write_bytes'])/1e6:7.1f} MB  "
+          f"alg {d.get('algorithmic_bytes', 0)/1e6:7.1f} MB  {d.get('tbs_under_ncu', 0):.2f} TB/s")
