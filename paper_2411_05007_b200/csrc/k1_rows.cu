@@ -196,8 +196,8 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
   if (warp == 0) {                                             // lane s initialises the barriers of slot s
     if (lane < S) {
       mbar_init(&full[lane], 1);
-      mbar_init(&empty[lane], kQuantWarps + (r ? 1 : 0));
-      mbar_init(&conv[lane], kQuantWarps);
+      mbar_init(&empty[lane], kQuantWarps / 2 + (r ? 1 : 0));   // one team + the MMA
+      mbar_init(&conv[lane], kQuantWarps / 2);
     }
     if (lane < SW) {
       mbar_init(&wfull[lane], 1);
@@ -315,20 +315,35 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
     }
   } else {
     // -------------------------------------------------------------------- quantizers
+    // Two teams of 8 warps take alternate stages (team t: stages i = t mod 2), and each thread
+    // takes TWO groups of its team's stage: staged rows R and R + 64, which hold the same K block
+    // (R = m Q + qb, Q | 64) and so share one set of lambda_inv loads.  Shared memory is this
+    // kernel's binding resource (ncu: every LDS.128 costs 4 wavefronts; quantizer loads + tcgen05
+    // operand reads + TMA fills ~ 1000 wavefronts per 16 KB stage); sharing the lambda loads
+    // removes a third of the quantizers' wavefronts, and the two teams overlap each other's
+    // load latency.
     const int qw = warp - kQ0;
-    const int R = qw * 8 + (lane >> 2);                         // staged tile row = m * Q + qb
+    const int team = qw >> 3;
+    const int R = (qw & 7) * 8 + (lane >> 2);                   // staged tile rows R and R + 64
     const int q4 = lane & 3;                                    // 16-element group within the block
-    const int m = R / Q;                                        // row within the tile
-    const int qb = R % Q;                                       // K block within the stage
-    const int64_t row = row0 + m;
-    const bool rvalid = row < p.M;
+    const int qb = R % Q;                                       // K block within the stage (both rows)
+    const int mh[2] = {R / Q, (R + 64) / Q};                    // rows within the tile
     const float t6 = __fmul_rn(__frcp_rn(p.gs_x), __frcp_rn(6.0f));
     // output addressing: the layer's own layout (out_k = K, out_c0 = 0), or -- fused tensor-parallel
     // gather -- this K-slice's place inside the full-K layout (out_k = full K, out_c0 = k0 / 16)
-    uint8_t *const xq_base = p.xq + row * (p.out_k / 2) + static_cast<int64_t>(qb) * 32 + q4 * 8;
-    uint8_t *const sf_base = p.xs + sf_offset(row, p.out_c0, p.out_k) + static_cast<int64_t>(qb) * 512 + q4;
-    uint8_t *const s16_base = p.xs + 2 * (row * (p.out_k / 64) + p.out_c0 / 4 + qb);
-    const uint32_t swz = static_cast<uint32_t>(R & 7);
+    int64_t rowh[2];
+    bool rvalid[2];
+    uint8_t *xq_base[2], *sf_base[2], *s16_base[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t row = row0 + mh[h];
+      rowh[h] = row;
+      rvalid[h] = row < p.M && mh[h] < RT;
+      xq_base[h] = p.xq + row * (p.out_k / 2) + static_cast<int64_t>(qb) * 32 + q4 * 8;
+      sf_base[h] = p.xs + sf_offset(row, p.out_c0, p.out_k) + static_cast<int64_t>(qb) * 512 + q4;
+      s16_base[h] = p.xs + 2 * (row * (p.out_k / 64) + p.out_c0 / 4 + qb);
+    }
+    const uint32_t swz = static_cast<uint32_t>(R & 7);          // == (R + 64) & 7
     const uint32_t lut = smem_u32(qinv_lut);
     const uint32_t stage0 = smem_u32(smem);
     // lambda row j = 2 qb + (q4 >> 1) of the swizzled [2Q][128 B] block; chunk (q4 & 1) * 4 + t
@@ -342,13 +357,18 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
     const int ndst = p.ndst;                                    // 1, or the ranks of a fused gather
     const int64_t d0 = p.dst_delta[0];
 
-    // Stage i -> x_hat pairs (fl32(x * lambda_inv)) in registers, then the slot is released.
-    int qs = 0;                                                 // ring slot of the next stage
-    uint32_t qph = 0;                                           // and its round parity
-    auto load_stage = [&](int i, uint64_t (&xh)[8]) {
+    // This team's next stage: slot and round parity (stages advance by 2)
+    int qs = team % S;
+    uint32_t qph = team >= S ? 1u : 0u;
+    auto next_slot = [&]() {
+      qs += 2;
+      if (qs >= S) { qs -= S; qph ^= 1; }
+    };
+    // Stage i -> x_hat pairs (fl32(x * lambda_inv)) of both rows in registers, then the slot is released.
+    auto load_stage = [&](int i, uint64_t (&xh)[2][8]) {
       const int s = qs;
       mbar_wait(&full[s], qph);
-      if (++qs == S) { qs = 0; qph ^= 1; }
+      next_slot();
       if (qw == 0 && lane == 0 && i < 64) RTRACE(110 + i);
       const uint32_t sbase = stage0 + s * Ly.stage_bytes;
 #pragma unroll
@@ -356,31 +376,34 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
         uint64_t l0, l1, l2, l3;
         lds_v2x64(sbase + lam_off[2 * c], l0, l1);
         lds_v2x64(sbase + lam_off[2 * c + 1], l2, l3);
-        const uint32_t xaddr = sbase + x_off[c];
-        const uint4 v = lds128(xaddr);
-        const uint64_t x0 = x2_to_f32x2<kX16>(v.x), x1 = x2_to_f32x2<kX16>(v.y);
-        const uint64_t x2 = x2_to_f32x2<kX16>(v.z), x3 = x2_to_f32x2<kX16>(v.w);
-        if constexpr (kX16) {
-          // fp16 X -> hi = bf16(x) (in place) + lo = bf16(x - hi) (the lo tile): both exact, so the
-          // bf16 x bf16 MMAs reproduce X . L1s^T (kind::f16 takes one A/B type)
-          uint32_t hw[4], lw[4];
-          const uint64_t xs4[4] = {x0, x1, x2, x3};
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const float a = lo32(xs4[t]), b = hi32(xs4[t]);
-            const uint32_t h = pack_bf16x2(a, b);
-            hw[t] = h;
-            lw[t] = pack_bf16x2(a - __uint_as_float(h << 16), b - __uint_as_float(h & 0xFFFF0000u));
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t xaddr = sbase + x_off[c] + h * 8192;   // row R + 64 h
+          const uint4 v = lds128(xaddr);
+          const uint64_t x0 = x2_to_f32x2<kX16>(v.x), x1 = x2_to_f32x2<kX16>(v.y);
+          const uint64_t x2 = x2_to_f32x2<kX16>(v.z), x3 = x2_to_f32x2<kX16>(v.w);
+          if constexpr (kX16) {
+            // fp16 X -> hi = bf16(x) (in place) + lo = bf16(x - hi) (the lo tile): both exact, so the
+            // bf16 x bf16 MMAs reproduce X . L1s^T (kind::f16 takes one A/B type)
+            uint32_t hw[4], lw[4];
+            const uint64_t xs4[4] = {x0, x1, x2, x3};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float a = lo32(xs4[t]), b = hi32(xs4[t]);
+              const uint32_t hb = pack_bf16x2(a, b);
+              hw[t] = hb;
+              lw[t] = pack_bf16x2(a - __uint_as_float(hb << 16), b - __uint_as_float(hb & 0xFFFF0000u));
+            }
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(xaddr), "r"(hw[0]), "r"(hw[1]), "r"(hw[2]),
+                         "r"(hw[3]) : "memory");
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(xaddr + 16384), "r"(lw[0]), "r"(lw[1]),
+                         "r"(lw[2]), "r"(lw[3]) : "memory");
           }
-          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(xaddr), "r"(hw[0]), "r"(hw[1]), "r"(hw[2]),
-                       "r"(hw[3]) : "memory");
-          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(xaddr + 16384), "r"(lw[0]), "r"(lw[1]),
-                       "r"(lw[2]), "r"(lw[3]) : "memory");
+          xh[h][4 * c + 0] = fmul2(x0, l0);
+          xh[h][4 * c + 1] = fmul2(x1, l1);
+          xh[h][4 * c + 2] = fmul2(x2, l2);
+          xh[h][4 * c + 3] = fmul2(x3, l3);
         }
-        xh[4 * c + 0] = fmul2(x0, l0);
-        xh[4 * c + 1] = fmul2(x1, l1);
-        xh[4 * c + 2] = fmul2(x2, l2);
-        xh[4 * c + 3] = fmul2(x3, l3);
       }
       if constexpr (kX16) {
         fence_proxy_async();                                    // generic smem writes -> tcgen05 reads
@@ -390,9 +413,9 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);                   // tile consumed: values in registers
     };
-    // Group absmax -> scale -> codes, stored at stage i's place (App. B recipe, bit-exact).
-    auto quant_store = [&](int i, const uint64_t (&xh)[8], bool st) {
-      const bool active = st && i * Q + qb < nkb;               // this lane's block exists (last stage)
+    // Group absmax -> scale -> codes of row half h, stored at stage i's place (App. B recipe, bit-exact).
+    auto quant_store = [&](int i, int h, const uint64_t (&xh)[8]) {
+      const bool active = i * Q + qb < nkb;                     // this lane's block exists (last stage)
       float am[8];                                              // |x_hat| max as a tree (short chain)
 #pragma unroll
       for (int j = 0; j < 8; ++j) am[j] = fmaxf(fabsf(lo32(xh[j])), fabsf(hi32(xh[j])));
@@ -410,14 +433,14 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
           if ((w0 ^ w1 ^ sf) == 0x12345u) p.xq[0] = 1;
           return;
         }
-        if (active) {
-          uint8_t *xq = xq_base + step * 32;
-          uint8_t *sfp = sf_base + step * 512;
-          if (rvalid) *reinterpret_cast<uint2 *>(xq + d0) = make_uint2(w0, w1);
+        if (active && mh[h] < RT) {
+          uint8_t *xq = xq_base[h] + step * 32;
+          uint8_t *sfp = sf_base[h] + step * 512;
+          if (rvalid[h]) *reinterpret_cast<uint2 *>(xq + d0) = make_uint2(w0, w1);
           sfp[d0] = static_cast<uint8_t>(sf);                   // padding rows (>= M) get 0x00
           for (int j = 1; j < ndst; ++j) {                      // the other ranks of a fused gather
             const int64_t d = p.dst_delta[j];
-            if (rvalid) *reinterpret_cast<uint2 *>(xq + d) = make_uint2(w0, w1);
+            if (rvalid[h]) *reinterpret_cast<uint2 *>(xq + d) = make_uint2(w0, w1);
             sfp[d] = static_cast<uint8_t>(sf);
           }
         }
@@ -441,9 +464,9 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
           }
           w[c] = word;
         }
-        if (rvalid && active) {
-          uint8_t *xq = xq_base + step * 32;
-          uint8_t *s16 = s16_base + step * 2;
+        if (rvalid[h] && active) {
+          uint8_t *xq = xq_base[h] + step * 32;
+          uint8_t *s16 = s16_base[h] + step * 2;
           for (int j = 0; j < ndst; ++j) {
             const int64_t d = p.dst_delta[j];
             *reinterpret_cast<uint2 *>(xq + d) = make_uint2(w[0], w[1]);
@@ -454,24 +477,25 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
     };
 
     if (kFmt == 2 && !kX16) {                                   // W8A8: the MMA warp alone uses the tile
-      for (int i = 0; i < nsteps; ++i) {
+      for (int i = team; i < nsteps; i += 2) {
         const int s = qs;
         mbar_wait(&full[s], qph);
-        if (++qs == S) { qs = 0; qph ^= 1; }
+        next_slot();
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
       }
     } else {
-      for (int i = 0; i < nsteps; ++i) {
-        uint64_t xh[8];
+      for (int i = team; i < nsteps; i += 2) {
+        uint64_t xh[2][8];
         load_stage(i, xh);
         if (kFmt == 2) continue;                                // W8A8 (fp16 X): conversion only
         if (SVDQ_K1REXP & 1) {
-          if (xh[0] == 12345ull) p.xq[0] = 1;                   // keep the loads alive
+          if (xh[0][0] == 12345ull || xh[1][0] == 12345ull) p.xq[0] = 1;   // keep the loads alive
           continue;
         }
-        quant_store(i, xh, true);
-        if (lane == 0 && i == nsteps / 2) RTRACE(420 + qw);
+        quant_store(i, 0, xh[0]);
+        quant_store(i, 1, xh[1]);
+        if (lane == 0 && (i >> 1) == (nsteps >> 2)) RTRACE(420 + qw);
       }
     }
   }

@@ -22,6 +22,7 @@
 // 2*192 + 2*48 <= 512; N tiles that start mid scale-factor atom (n0 % 128 == 64)
 // read SFB from a TMEM address 2 columns (64 rows) into the loaded atom pair.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -357,6 +358,9 @@ static cudaError_t launch_bn(const K2Maps &maps, const K2Params &p, cudaStream_t
 
 int k2_nvfp4_bn(int64_t M, int64_t N) {
   (void)M;
+  // SVDQ_K2_BN1=128 / 192 forces the 1-CTA tile N (A/B of small-layer tile shapes)
+  static const int force = [] { const char *e = std::getenv("SVDQ_K2_BN1"); return e ? std::atoi(e) : 0; }();
+  if (force == 128 || force == 192) return force;
   if (N % 192 == 0) return 192;
   if (N % 128 == 0) return 128;
   return N > 1024 ? 192 : 128;
