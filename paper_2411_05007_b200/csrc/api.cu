@@ -154,18 +154,45 @@ svdq_status make_sf_map(CUtensorMap *map, const void *base, int64_t rows, int64_
   return SVDQ_OK;
 }
 
-// CTA-pair kernel unless the problem is small (measured on B200 with the 8-warp TMA-store
-// epilogue: pairs are 12-13 % faster at K = 12288 / 15360 and equal or 1 % faster at
-// K = 3072, M >= 4096; the 1-CTA kernel is 3 % faster at M = 512, K = 3072).
-// SVDQ_K2_PAIR=0 / 1 forces one kernel (testing / comparison).
-bool use_pair_kernel(int64_t M, int64_t K) {
+// W8A8: the CTA-pair kernel unless the problem is small.  SVDQ_K2_PAIR=0 / 1 forces one kernel
+// (testing / comparison).
+int pair_mode() {
   static int mode = -1;
   if (mode < 0) {
     const char *e = getenv("SVDQ_K2_PAIR");
     mode = e ? atoi(e) : 2;
   }
-  if (M <= 128 || mode == 0) return false;
-  return mode == 1 || K >= 6144 || M >= 1024;
+  return mode;
+}
+bool use_pair_kernel(int64_t M, int64_t K) {
+  if (M <= 128 || pair_mode() == 0) return false;
+  return pair_mode() == 1 || K >= 6144 || M >= 1024;
+}
+
+// NVFP4 tile plan of one (non-grouped) K2 launch: the CTA-pair kernel (256 x 256 / 256 x 192 tiles,
+// 74 pairs) or the 1-CTA kernel (128 x 192 / 128 x 128, 148 SMs), whichever leaves the least
+// per-SM work in its last wave -- cost = waves x (tile columns per SM), the 1-CTA kernel weighted
+// 1.1 (its SMs each stage all of B: measured 3-15 % slower per tile on C2 / C3 shapes).  Chooses
+// the pair kernel on every FLUX layer with M >= 4096 and the 1-CTA 128-wide tile on e.g. PixArt's
+// 4096 x 1152 x 1152 (tools/k2_shape_sweep.py).
+struct K2Plan {
+  bool pair;
+  int bn;
+};
+K2Plan plan_nvfp4(int64_t M, int64_t N) {
+  const int64_t sms = svdq::device_sm_count();
+  auto waves = [](int64_t tiles, int64_t units) { return (tiles + units - 1) / units; };
+  K2Plan best{true, svdq::k2_pair_bn(N)};
+  double cbest = 1e30;
+  for (int bn : {svdq::k2_pair_bn(N), 192}) {
+    const double c = static_cast<double>(waves(((M + 255) / 256) * ((N + bn - 1) / bn), sms / 2) * bn);
+    if (c < cbest) { cbest = c; best = K2Plan{true, bn}; }
+  }
+  if (pair_mode() == 1) return best;
+  const int bn1 = svdq::k2_nvfp4_bn(M, N);
+  const double c1 = 1.1 * static_cast<double>(waves(((M + 127) / 128) * ((N + bn1 - 1) / bn1), sms) * bn1);
+  if (M <= 128 || pair_mode() == 0 || c1 < cbest) return K2Plan{false, bn1};
+  return best;
 }
 
 }  // namespace
@@ -532,10 +559,12 @@ svdq_status prepare_k2(const svdq_linear *L, const uint8_t *xq, const uint8_t *x
   K2Maps &maps = out->maps;
   std::memset(&maps, 0, sizeof(maps));
   // CTA-pair kernel: NVFP4, and W8A8 (its kind::i8 mode, 192-wide tiles)
-  const bool pair = (L->fmt == SVDQ_FMT_NVFP4 || L->fmt == SVDQ_FMT_W8A8) && (force_pair || use_pair_kernel(M, K));
+  const K2Plan plan = L->fmt == SVDQ_FMT_NVFP4 && !force_pair ? plan_nvfp4(M, N) : K2Plan{true, 0};
+  const bool pair = L->fmt == SVDQ_FMT_NVFP4 ? (force_pair || plan.pair)
+                                             : (L->fmt == SVDQ_FMT_W8A8 && (force_pair || use_pair_kernel(M, K)));
   out->pair = pair;
-  // pair tile N: the caller's (grouped / fused launches share one) or this problem's own
-  out->bn = !pair ? 0 : L->fmt == SVDQ_FMT_W8A8 ? 192 : (pair_bn ? pair_bn : k2_pair_bn(N));
+  // pair tile N: the caller's (grouped / fused launches share one) or this problem's own plan
+  out->bn = !pair ? 0 : L->fmt == SVDQ_FMT_W8A8 ? 192 : (pair_bn ? pair_bn : (plan.bn ? plan.bn : k2_pair_bn(N)));
   const int BN = pair ? out->bn : L->fmt == SVDQ_FMT_NVFP4 ? k2_nvfp4_bn(M, N) : kInt4BN;
   std::memset(&out->sfa_map, 0, sizeof(out->sfa_map));
   std::memset(&out->sfb_map, 0, sizeof(out->sfb_map));

@@ -357,13 +357,15 @@ static cudaError_t launch_bn(const K2Maps &maps, const K2Params &p, cudaStream_t
 }
 
 int k2_nvfp4_bn(int64_t M, int64_t N) {
-  (void)M;
   // SVDQ_K2_BN1=128 / 192 forces the 1-CTA tile N (A/B of small-layer tile shapes)
   static const int force = [] { const char *e = std::getenv("SVDQ_K2_BN1"); return e ? std::atoi(e) : 0; }();
   if (force == 128 || force == 192) return force;
-  if (N % 192 == 0) return 192;
-  if (N % 128 == 0) return 128;
-  return N > 1024 ? 192 : 128;
+  // the tile N with the least per-SM work in the last wave: waves x BN (ties -> 192); on the small
+  // layers of C2 / C3 the 128-wide tile often fills one more SM wave (PixArt 4096 x 1152 x 1152:
+  // 7.8 vs 8.7 us, tools/k2_shape_sweep.py)
+  const int64_t sms = device_sm_count(), mt = (M + 127) / 128;
+  const int64_t w128 = (mt * ((N + 127) / 128) + sms - 1) / sms, w192 = (mt * ((N + 191) / 192) + sms - 1) / sms;
+  return w192 * 192 <= w128 * 128 ? 192 : 128;
 }
 
 cudaError_t launch_k2_nvfp4(const K2Maps &maps, const K2Params &p, cudaStream_t s) {

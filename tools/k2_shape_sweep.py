@@ -10,7 +10,8 @@ import paper_2411_05007_b200 as P  # noqa: E402
 SHAPES = [(4096, 1152, 3456), (4096, 1152, 1152), (4096, 1152, 4608), (4096, 4608, 1152),
           (8192, 640, 1920), (8192, 640, 640), (8192, 640, 5120), (8192, 2560, 640),
           (2048, 1280, 3840), (2048, 1280, 1280), (2048, 1280, 10240), (2048, 5120, 1280),
-          (512, 3072, 3072), (512, 3072, 9216)]
+          (512, 3072, 3072), (512, 3072, 9216), (512, 12288, 3072), (512, 3072, 12288),
+          (4096, 3072, 3072), (4608, 15360, 3072)]
 tag = sys.argv[1] if len(sys.argv) > 1 else "default"
 dev = torch.device("cuda")
 st = torch.cuda.Stream()
