@@ -37,7 +37,14 @@
 #ifndef SVDQ_I4_SLEEP_NS
 #define SVDQ_I4_SLEEP_NS 64
 #endif
+#ifndef SVDQ_I4_WAITMODE
+#define SVDQ_I4_WAITMODE 0       // 0: test_wait + nanosleep back-off; 1: try_wait with the suspend-time hint
+#endif
+#if SVDQ_I4_WAITMODE == 1
+#define SVDQ_I4_WAIT(bar, par) mbar_wait((bar), (par))
+#else
 #define SVDQ_I4_WAIT(bar, par) mbar_wait_sleep((bar), (par), SVDQ_I4_SLEEP_NS)
+#endif
 #ifndef SVDQ_I4EXP
 #define SVDQ_I4EXP 0   // ablation bits: 1 no scale fetch, 2 no promotion math, 4 no unpack, 8 no MMA
 #endif
