@@ -77,6 +77,9 @@ constexpr int kMaxWStages = 4;
 #define SVDQ_K1_SW 4                                   // L1s ring depth (the tiles come from L2)
 #endif
 static_assert(SVDQ_K1_SW >= 2 && SVDQ_K1_SW <= kMaxWStages, "L1s ring depth");
+#ifndef SVDQ_K1_XPRE
+#define SVDQ_K1_XPRE 12                                // X boxes prefetched to L2 before griddepcontrol.wait
+#endif
 #ifndef SVDQ_K1_LAMPRE
 #define SVDQ_K1_LAMPRE 2                               // ring slots whose lambda tile goes out before griddepcontrol.wait
 #endif
@@ -136,6 +139,14 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
       "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+
+// L2 prefetch of a 3-D box (no smem destination, no completion tracking)
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *map, int32_t c0, int32_t c1, int32_t c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
 }
 
 }  // namespace
@@ -238,6 +249,11 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
       // write X): the first ring's lambda tiles (no kernel of this stream writes them).
       const int npre = S < SVDQ_K1_LAMPRE ? S : SVDQ_K1_LAMPRE;   // lambda tiles issued before the wait
       for (int i = 0; i < nsteps && i < npre; ++i) load_lam(i, i);
+      // ... and an L2 prefetch of the first ring's X boxes: it overlaps the cold first access
+      // (~1.6 us) with the previous kernel's tail.  Safe while that kernel may still write X:
+      // L2 is the coherence point and the TMA loads below are issued after the wait.
+      for (int i = 0; i < nsteps && i < (SVDQ_K1_XPRE < S ? SVDQ_K1_XPRE : S); ++i)
+        tma_prefetch_3d(&tmX, 0, i * Q, static_cast<int32_t>(row0));
       griddep_wait();
       int s = 0;
       uint32_t ph = 0;                                          // ring round parity of slot s
