@@ -63,6 +63,15 @@ namespace {
 #ifndef SVDQ_K1_SPIN
 #define SVDQ_K1_SPIN 0
 #endif
+// Waits of the quantizer warps (stage full, the tail's dfull): SVDQ_K1_QSPIN=1 spins instead of
+// suspending (A/B of the wake-up latency on small launches).
+#ifndef SVDQ_K1_QSPIN
+#define SVDQ_K1_QSPIN 0
+#endif
+__device__ __forceinline__ void q_wait(uint64_t *bar, uint32_t parity) {
+  if (SVDQ_K1_QSPIN) mbar_wait_spin(bar, parity);
+  else mbar_wait(bar, parity);
+}
 __device__ __forceinline__ void role_wait(uint64_t *bar, uint32_t parity) {
   if (SVDQ_K1_SPIN) mbar_wait_spin(bar, parity);
   else mbar_wait(bar, parity);
@@ -383,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
     // Stage i -> x_hat pairs (fl32(x * lambda_inv)) of both rows in registers, then the slot is released.
     auto load_stage = [&](int i, uint64_t (&xh)[2][8]) {
       const int s = qs;
-      mbar_wait(&full[s], qph);
+      q_wait(&full[s], qph);
       next_slot();
       if (qw == 0 && lane == 0 && i < 64) RTRACE(110 + i);
       const uint32_t sbase = stage0 + s * Ly.stage_bytes;
@@ -536,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
     const int64_t row = row0 + mm;
     const int nc8 = r / 8;
     if (qq < nc8) {
-      mbar_wait(dfull, 0);
+      q_wait(dfull, 0);
       tc_fence_after();
     }
     if (threadIdx.x == 32 * kQ0) RTRACE(103);

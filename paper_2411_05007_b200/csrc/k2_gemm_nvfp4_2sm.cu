@@ -252,6 +252,10 @@ __global__ void __launch_bounds__(Lay<kFuse, kBN, kW8>::threads, 1)
   }
   if (warp == 1) tmem_alloc_cg2(tmem_slot, 512);
   tc_fence_before();
+  // CTA barrier before the cluster barrier: orders the allocator's write of tmem_slot before the
+  // other warps' reads in a form compute-sanitizer's racecheck models (it flagged the
+  // tcgen05.alloc write against the reads below when only barrier.cluster separated them)
+  __syncthreads();
   cluster_sync();                                        // barriers of both CTAs initialised
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
