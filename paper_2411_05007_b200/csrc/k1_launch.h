@@ -114,6 +114,7 @@ struct K2Params {
   // next layer's K1 on its own bf16 output -- NVFP4 codes / scale factors of
   // act(Y) * lambda_inv_next and partial X L1s_next^T sums (reduced by launch_k2_next_reduce).
   int fuse;               // 1: on (this problem's tiles are walked n-fastest)
+  int band;               // CTA-pair K2: 256-row tiles per L2 band (0 = the whole M, m-fastest order)
   int nx_act;             // 0 identity, 1 GELU (tanh form)
   int nx_r;               // next layer's rank: 0, 16 or 32
   float nx_gs;            // next layer's gs_x

@@ -176,7 +176,15 @@ __device__ __forceinline__ TileRef locate(const K2PairArgs &g, int t) {
     return TileRef{i, static_cast<int64_t>(lt / nt) * 256, static_cast<int64_t>(lt % nt) * BN};
   }
   const int mt = static_cast<int>((g.pr[i].p.M + 255) / 256);
-  return TileRef{i, static_cast<int64_t>(lt % mt) * 256, static_cast<int64_t>(lt / mt) * BN};
+  const int band = g.pr[i].p.band;
+  if (band <= 0 || band >= mt)                     // m-fastest over the whole M
+    return TileRef{i, static_cast<int64_t>(lt % mt) * 256, static_cast<int64_t>(lt / mt) * BN};
+  // L2 bands: all N tiles of `band` row tiles (m-fastest inside the band), then the next band,
+  // so the band's A rows stay L2-resident while every weight tile streams past them once
+  const int nt = static_cast<int>((g.pr[i].p.N + BN - 1) / BN);
+  const int b = lt / (band * nt), in = lt - b * band * nt;
+  const int rows = min(band, mt - b * band);
+  return TileRef{i, static_cast<int64_t>(b * band + in % rows) * 256, static_cast<int64_t>(in / rows) * BN};
 }
 
 // kW8: the paper's 8-bit setting (SVDQ_FMT_W8A8) on the same CTA-pair skeleton:
@@ -767,6 +775,25 @@ cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
     g.tile_begin[i + 1] = g.tile_begin[i] + static_cast<int>(((g.pr[i].p.M + 255) / 256) * ((g.pr[i].p.N + bn - 1) / bn));
   const int64_t tiles = g.tile_begin[g.n];
   const int64_t pairs = k2_pair_count(tiles);
+  // L2 banding (large M): the m-fastest order re-streams the whole of A for every weight column
+  // tile; once A (M x K codes + scales) outgrows the L2 budget -- FLUX batch >= 4 -- its rows come
+  // from DRAM again for each of the N / BN columns.  Band size: as many 256-row tiles as fit
+  // SVDQ_K2_BAND_MB (default 48 MB) of A, balanced over the bands.  At batch 1 every FLUX problem
+  // fits one band, so the order is unchanged there.
+  static const double band_mb = [] { const char *e = std::getenv("SVDQ_K2_BAND_MB"); return e ? std::atof(e) : 48.0; }();
+  for (int i = 0; i < g.n; ++i) {
+    K2Params &p = g.pr[i].p;
+    const int64_t mt = (p.M + 255) / 256;
+    const double tile_bytes = 256.0 * static_cast<double>(p.K) * (p.w8 ? 1.0 : 0.5625);
+    int64_t cap = band_mb > 0 ? static_cast<int64_t>(band_mb * 1048576.0 / tile_bytes) : mt;
+    if (cap < 1) cap = 1;
+    if (p.fuse || mt <= cap) {
+      p.band = 0;
+    } else {
+      const int64_t nb = (mt + cap - 1) / cap;
+      p.band = static_cast<int>((mt + nb - 1) / nb);
+    }
+  }
   static const int force_contig = [] { const char *e = std::getenv("SVDQ_K2_CONTIG"); return e ? std::atoi(e) : 0; }();
   g.contig = (fuse || force_contig) ? 1 : 0;      // SVDQ_K2_CONTIG=1: schedule ablation
   g.npairs = static_cast<int>(pairs);
