@@ -778,9 +778,10 @@ cudaError_t launch_k2_nvfp4_2sm_group(K2PairArgs &g, cudaStream_t s) {
   // L2 banding (large M): the m-fastest order re-streams the whole of A for every weight column
   // tile; once A (M x K codes + scales) outgrows the L2 budget -- FLUX batch >= 4 -- its rows come
   // from DRAM again for each of the N / BN columns.  Band size: as many 256-row tiles as fit
-  // SVDQ_K2_BAND_MB (default 48 MB) of A, balanced over the bands.  At batch 1 every FLUX problem
-  // fits one band, so the order is unchanged there.
-  static const double band_mb = [] { const char *e = std::getenv("SVDQ_K2_BAND_MB"); return e ? std::atof(e) : 48.0; }();
+  // SVDQ_K2_BAND_MB (default 16 MB; swept 8 / 16 / 32 / 48 / 80 on the 57-block stack) of A,
+  // balanced over the bands.  At batch 1 only the K >= 12288 launches band (2-3 bands; timing
+  // unchanged); batch 8 gains 12 % (tools/c5_stack.py).
+  static const double band_mb = [] { const char *e = std::getenv("SVDQ_K2_BAND_MB"); return e ? std::atof(e) : 16.0; }();
   for (int i = 0; i < g.n; ++i) {
     K2Params &p = g.pr[i].p;
     const int64_t mt = (p.M + 255) / 256;

@@ -16,6 +16,7 @@ import paper_2411_05007_b200 as P  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--out", default=os.path.join(bench.ROOT, "profiles", "r02", "c5_stack_1gpu.json"))
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--batches", default="1,2,4,8")
 a = ap.parse_args()
 dev = torch.device("cuda")
 st = torch.cuda.Stream()
@@ -46,7 +47,7 @@ def time_block(built):
 
 
 out = {"note": __doc__.split("\n    python")[0], "batches": {}}
-for B in (1, 2, 4, 8):
+for B in (int(b) for b in a.batches.split(",")):
     dl, sl = synth.flux_double_block(B), synth.flux_single_block(B)
     td = time_block(bench.build_layers(P, torch, dl, "nvfp4", dev))
     torch.cuda.empty_cache()
