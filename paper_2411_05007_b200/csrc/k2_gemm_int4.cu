@@ -45,6 +45,13 @@
 #else
 #define SVDQ_I4_WAIT(bar, par) mbar_wait_sleep((bar), (par), SVDQ_I4_SLEEP_NS)
 #endif
+// Magic-initialized group accumulators: every int32 ring slot holds 0x4B400000 (= 1.5 * 2^23 as
+// fp32) when the MMA starts a group, the group's MMAs ACCUMULATE onto it, so the epilogue reads
+// the fp32 value 1.5 * 2^23 + acc directly (exact: |acc| <= 64 * 49 < 2^22) and saves the integer
+// add per element; it writes the constant back (tcgen05.st) before releasing the slot.
+#ifndef SVDQ_I4_MAGIC
+#define SVDQ_I4_MAGIC 1
+#endif
 #ifndef SVDQ_I4EXP
 #define SVDQ_I4EXP 0   // ablation bits: 1 no scale fetch, 2 no promotion math, 4 no unpack, 8 no MMA
 #endif
@@ -109,6 +116,14 @@ __device__ __forceinline__ float4 lds_f32x4(uint32_t addr) {
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
+// 16 columns of the constant v: four .x4 stores (a .x16 store of one repeated register still
+// needs 16 live source registers and made the epilogue spill)
+__device__ __forceinline__ void tmem_st_32x32b_x16_const(uint32_t taddr, uint32_t v) {
+#pragma unroll
+  for (int c = 0; c < 16; c += 4)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%1,%1,%1};" ::"r"(taddr + c), "r"(v) : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
   uint64_t d;
   asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
@@ -240,6 +255,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (SVDQ_I4_MAGIC && !kW8) {
+    if (warp >= 2 + kUnpackWarps) {                 // epilogue warps: their lanes and columns of every slot
+      const int ew0 = warp - 2 - kUnpackWarps;
+      const uint32_t lo0 = static_cast<uint32_t>((warp & 3) * 32) << 16;
+      for (int b = 0; b < kAcc; ++b)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) tmem_st_32x32b_x16_const(tmem + b * BN + lo0 + (ew0 >> 2) * EC + hh * 16, 0x4B400000u);
+      tmem_st_wait();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   griddep_launch_dependents();
   griddep_wait();                                   // inputs may come from the previous kernel
 
@@ -353,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int h = 0; h < ((SVDQ_I4EXP & 8) ? 0 : 2); ++h)
               mma_s8(tmem + b * BN, sdesc_kmajor_sw128(ua + 64 * j + 32 * h),
-                     sdesc_kmajor_sw128(ub + 64 * j + 32 * h), idesc_i, h);
+                     sdesc_kmajor_sw128(ub + 64 * j + 32 * h), idesc_i, SVDQ_I4_MAGIC ? 1u : static_cast<uint32_t>(h));
             tc_commit(&g_full[b]);
           }
           __syncwarp();
@@ -477,7 +505,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int c = 0; c < 8; ++c) facc[hh * 8 + c] = f2pack(__uint_as_float(r[2 * c]), __uint_as_float(r[2 * c + 1]));
+          if (SVDQ_I4_MAGIC && !kW8)                 // the slot's next user may be an int32 group
+            tmem_st_32x32b_x16_const(tmem + b * BN + lane_off + slice * EC + hh * 16, 0x4B400000u);
         }
+        if (SVDQ_I4_MAGIC && !kW8) tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&g_empty[b]);
@@ -552,6 +583,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld_32x32b_x16(tmem + b * BN + lane_off + slice * EC + hh * 16, r);
             tmem_ld_wait();
             if (hh == 1) {
+              if (SVDQ_I4_MAGIC) {                        // both halves read: restore the constant
+                tmem_st_32x32b_x16_const(tmem + b * BN + lane_off + slice * EC, 0x4B400000u);
+                tmem_st_32x32b_x16_const(tmem + b * BN + lane_off + slice * EC + 16, 0x4B400000u);
+                tmem_st_wait();
+              }
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(&g_empty[b]);   // the int32 buffer is free again
@@ -566,7 +602,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int q = 0; q < 16; q += 4)
                   if (c0 + hh * 16 + q < p.N)
-                    *reinterpret_cast<int4 *>(dst + q) = make_int4((int)r[q], (int)r[q + 1], (int)r[q + 2], (int)r[q + 3]);
+                    *reinterpret_cast<int4 *>(dst + q) = SVDQ_I4_MAGIC
+                        ? make_int4((int)(r[q] - 0x4B400000u), (int)(r[q + 1] - 0x4B400000u), (int)(r[q + 2] - 0x4B400000u),
+                                    (int)(r[q + 3] - 0x4B400000u))
+                        : make_int4((int)r[q], (int)r[q + 1], (int)r[q + 2], (int)r[q + 3]);
               }
               continue;
             }
@@ -579,8 +618,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // fl32(acc * sx) in one FMA: the magic-number float m = 1.5 * 2^23 + acc is exact
                 // (|acc| <= 64*49 < 2^22), bsx = fl32(-1.5 * 2^23 * sx) is exact (sx has 11
                 // significant bits), so fma(m, sx, bsx) = fl32((m - 1.5 * 2^23) * sx) = fl32(acc * sx)
-                const uint64_t a2 = f2pack(__int_as_float(static_cast<int>(r[e]) + 0x4B400000),
-                                           __int_as_float(static_cast<int>(r[e + 1]) + 0x4B400000));
+                const uint64_t a2 = SVDQ_I4_MAGIC
+                    ? f2pack(__uint_as_float(r[e]), __uint_as_float(r[e + 1]))
+                    : f2pack(__int_as_float(static_cast<int>(r[e]) + 0x4B400000),
+                             __int_as_float(static_cast<int>(r[e + 1]) + 0x4B400000));
                 const uint64_t t2 = fma2(a2, sx2, bsx2);
                 const int fi = hh * 8 + e / 2;
                 facc[fi] = fma2(t2, h ? f2pack(w4.z, w4.w) : f2pack(w4.x, w4.y), facc[fi]);   // + . * sw
