@@ -337,7 +337,9 @@ svdq_status svdq_quantize_act_lowrank_down(const svdq_linear *L, const void *X, 
     ++g_launches;
   }
   if (p.fmt == 2) {                    // per-token INT8 codes + fp32 scales
-    e = launch_k1_int8_rows(p, static_cast<cudaStream_t>(stream));
+    K1Params p8 = p;
+    p8.w8_amax = p.rank > 0 ? 1 : 0;   // the row-tile kernel above left each row's amax in xs
+    e = launch_k1_int8_rows(p8, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "K1 (int8 rows) launch");
     ++g_launches;
   }

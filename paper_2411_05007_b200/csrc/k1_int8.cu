@@ -1,8 +1,9 @@
 // K1 for the 8-bit setting (SVDQ_FMT_W8A8; App. D): per-token dynamic INT8 codes of
 // x_hat = fl32(x * lambda_inv) (reading Q14) with Eq. (1), q_max = 127 and one fp32 scale
-// per token.  A per-token scale needs the whole row before any code can be written, so the
-// row is read twice by the same warp: pass 1 takes amax(|x_hat|), pass 2 (served from L1 /
-// L2) encodes.  The down-projection X L1s^T of the same layer runs in the regular K1 kernel in
+// per token.  A per-token scale needs the whole row before any code can be written: the
+// row-tile kernel's down-projection pass (which reads X anyway) leaves amax(|x_hat|) per row in
+// xs (`w8_amax`), so this kernel encodes in one pass; without a low-rank branch (rank 0) it
+// takes amax itself first (pass 1, then pass 2 served from L1 / L2).  The down-projection X L1s^T of the same layer runs in the regular K1 kernel in
 // its projection-only mode (fmt 2), so the 16-bit branch is bit-identical across formats.
 //   s = fl32(amax / 127); qinv = s == 0 ? 0 : fl32(1 / s); q = clamp(rne(fl32(x_hat * qinv)), +-127)
 #include <cstdint>
@@ -32,6 +33,8 @@ __global__ void __launch_bounds__(256) k1_int8_rows_kernel(const K1Params p) {
   const uint16_t *x = static_cast<const uint16_t *>(p.X) + row * p.ldx;
   const int64_t K = p.K;
   float amax = 0.f;
+  if (p.w8_amax) amax = reinterpret_cast<const float *>(p.xs)[row];   // from the down-projection pass
+  else
   for (int64_t k = 8 * lane; k < K; k += 256) {
     const uint4 v = *reinterpret_cast<const uint4 *>(x + k);
     const float4 l0 = *reinterpret_cast<const float4 *>(p.lam_inv + k);

@@ -66,6 +66,9 @@ struct K1Params {
   // layout of the outputs: codes row pitch out_k / 2 bytes, scales of the (rows, out_k) layout
   // starting at 16-column group out_c0 (K-slice inside a full-K buffer); defaults out_k = K, 0
   int64_t out_k, out_c0;
+  // W8A8: xs already holds every row's amax |x_hat| (fp32), written by the row-tile kernel's
+  // down-projection pass, so the INT8 kernel encodes in one pass
+  int w8_amax;
 };
 cudaError_t launch_k1_int8_rows(const K1Params &p, cudaStream_t s);   // W8A8 per-token INT8 codes
 // Grouped K1: up to kMaxGroup1 problems (same fmt, scale dtype and rank) in one launch; the

@@ -176,7 +176,7 @@ K1RowLayout k1_row_layout(int rt, int rank, bool x16) {
   L.stages = s > kMaxXStages ? kMaxXStages : (s < 2 ? 2 : s);
   L.w_off = static_cast<size_t>(L.stages) * L.stage_bytes;
   L.bar_off = L.w_off + static_cast<size_t>(L.wstages) * L.l1_bytes;
-  L.smem = L.bar_off + 512 + 1024 + 1024;            // barriers, 256-entry qinv table, alignment slack
+  L.smem = L.bar_off + 512 + 1024 + 512 + 1024;      // barriers, 256-entry qinv table, W8A8 row amax, slack
   return L;
 }
 
@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
   uint64_t *dfull = wempty + kMaxWStages;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dfull + 1);
   float *qinv_lut = reinterpret_cast<float *>(smem + Ly.bar_off + 512);
+  uint32_t *rowmax = reinterpret_cast<uint32_t *>(smem + Ly.bar_off + 512 + 1024);   // W8A8: [RT] amax bits
   uint8_t *wring = smem + Ly.w_off;
 
   const int warp = threadIdx.x >> 5;
@@ -237,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
     const float sfd = e4m3_to_f32(code & 0x7F);
     qinv_lut[code] = sfd == 0.f ? 0.f : __frcp_rn(__fmul_rn(sfd, p.gs_x));
   }
+  if (kFmt == 2 && threadIdx.x < RT) rowmax[threadIdx.x] = 0u;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -501,19 +503,21 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
       }
     };
 
-    if (kFmt == 2 && !kX16) {                                   // W8A8: the MMA warp alone uses the tile
-      for (int i = team; i < nsteps; i += 2) {
-        const int s = qs;
-        mbar_wait(&full[s], qph);
-        next_slot();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-      }
-    } else {
+    {
+      float w8max[2] = {0.f, 0.f};                              // W8A8: running amax |x_hat| of both rows
       for (int i = team; i < nsteps; i += 2) {
         uint64_t xh[2][8];
         load_stage(i, xh);
-        if (kFmt == 2) continue;                                // W8A8 (fp16 X): conversion only
+        if (kFmt == 2) {                                        // W8A8: amax for the INT8 kernel (+ fp16 conversion)
+          if (i * Q + qb < nkb) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                w8max[h] = fmaxf(w8max[h], fmaxf(fabsf(lo32(xh[h][j])), fabsf(hi32(xh[h][j]))));
+          }
+          continue;
+        }
         if (SVDQ_K1REXP & 1) {
           if (xh[0][0] == 12345ull || xh[1][0] == 12345ull) p.xq[0] = 1;   // keep the loads alive
           continue;
@@ -521,6 +525,15 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
         quant_store(i, 0, xh[0]);
         quant_store(i, 1, xh[1]);
         if (lane == 0 && (i >> 1) == (nsteps >> 2)) RTRACE(420 + qw);
+      }
+      if (kFmt == 2) {                                          // combine the 4 groups of a row, then the CTA
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float v = w8max[h];
+          v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 1));
+          v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 2));
+          if (q4 == 0) atomicMax(&rowmax[mh[h]], __float_as_uint(v));   // non-negative: bit order = value order
+        }
       }
     }
   }
@@ -537,6 +550,8 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
   // the row stores the 8 columns.  The barrier first: the ring is no longer read by anyone.
   __syncthreads();
   if (threadIdx.x == 32 * kQ0) RTRACE(102);
+  if (kFmt == 2 && threadIdx.x < RT && row0 + threadIdx.x < p.M)   // every row's amax -> xs (fp32)
+    reinterpret_cast<float *>(p.xs)[row0 + threadIdx.x] = __uint_as_float(rowmax[threadIdx.x]);
   if (warp >= kQ0) {
     const int qd = warp & 3;                                   // TMEM lane quadrant of this warp
     const int qq = (warp - kQ0) >> 2;                          // 0..3 within the quadrant

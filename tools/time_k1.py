@@ -9,7 +9,8 @@ import paper_2411_05007_b200 as P
 M, K = int(sys.argv[1]), int(sys.argv[2])
 r = int(sys.argv[3]) if len(sys.argv) > 3 else 32
 dev = torch.device("cuda")
-layer = P.QuantizedLinear.empty("nvfp4", K, 64, r, device=dev)
+fmt = os.environ.get("SVDQ_FMT", "nvfp4")
+layer = P.QuantizedLinear.empty(fmt, K, 64, r, device=dev)
 layer.lambda_inv.fill_(1.0); layer.l1s.zero_(); layer._sync_view()
 nb = max(3, int(400e6 // (M * K * 2)) + 1)
 xs = [torch.randn(M, K, device=dev).to(torch.bfloat16) for _ in range(nb)]
@@ -45,6 +46,6 @@ for i in range(10):
     tw.append(a.elapsed_time(b) * 1e3)
 tf = sum(tf) / len(tf); tw = sum(tw) / len(tw)
 B = M * K * 2.5625 + 2 * M * r
-print(f"K1 M={M} K={K} r={r} lib={os.path.basename(os.environ.get('SVDQ_LIB', 'libsvdq.so'))}: "
+print(f"K1 {fmt} M={M} K={K} r={r} lib={os.path.basename(os.environ.get('SVDQ_LIB', 'libsvdq.so'))}: "
       f"back-to-back cold {us:.2f} us ({B/us/1e3:.2f} TB/s) | single after flush {tf:.2f} us ({B/tf/1e3:.2f} TB/s) "
       f"| single L2-warm {tw:.2f} us")
