@@ -707,9 +707,9 @@ def run_svdq(args, rank, world, local_rank):
                           "k1_gbs": round(float((L.M * L.K * (2 + cbytes)
                                                  + 2 * L.M * eff_rank(L)) / k1_avg_s[j] / 1e9), 1)}
                  for j, L in enumerate(layers)}
-    traffic = None
+    traffic = None                     # ncu DRAM bytes per K2 launch: captured for the NVFP4 FLUX step only
     tpath = os.path.join(ROOT, "profiles", "k2_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and args.fmt == "nvfp4" and args.config == "flux" and args.batch == 1:
         traffic = json.load(open(tpath)).get("bytes_per_launch")
     clocks = clk.summary()
     f_sm = (clocks.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)) * 1e6
