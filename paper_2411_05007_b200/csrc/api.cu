@@ -122,15 +122,15 @@ svdq_status make_map(CUtensorMap *map, const void *base, CUtensorMapDataType dt,
   return SVDQ_OK;
 }
 
-// 3-D view of a row-major 16-bit activation X [rows][ldx]: {64 cols, K/64 blocks, rows}, box
-// {64, q, rt}, 128-byte swizzle (the row-tile K1's stage: q blocks of rt rows).
+// 3-D view of a row-major 16-bit activation X [rows][ldx]: {64 cols, rows, K/64 blocks}, box
+// {64, rt, q}, 128-byte swizzle: the row-tile K1's stage, block-major (staged row q rt + m).
 svdq_status make_x3_map(CUtensorMap *map, const void *base, CUtensorMapDataType dt, int64_t K, int64_t rows,
                         int64_t ldx_bytes, uint32_t q, uint32_t rt) {
   auto fn = encode_fn();
   if (!fn) return fail(SVDQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(K / 64), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(ldx_bytes)};
-  cuuint32_t box[3] = {64, q, rt};
+  cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(K / 64)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ldx_bytes), 128};
+  cuuint32_t box[3] = {64, rt, q};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, dt, 3, const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

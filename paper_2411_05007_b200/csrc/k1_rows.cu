@@ -49,8 +49,12 @@ __device__ __forceinline__ unsigned long long k1r_gtime() {
 }
 #define RTRACE(slot) \
   do { if (blockIdx.x == 0) svdq::g_k1r_trace[(slot)] = k1r_gtime(); } while (0)
+// SM-clock stamps of the tail (slots 500-503), consistent within the CTA
+#define CTRACE(slot) \
+  do { if (blockIdx.x == 0) svdq::g_k1r_trace[(slot)] = clock64(); } while (0)
 #else
 #define RTRACE(slot) do {} while (0)
+#define CTRACE(slot) do {} while (0)
 #endif
 
 namespace svdq {
@@ -93,6 +97,9 @@ static_assert(SVDQ_K1_SW >= 2 && SVDQ_K1_SW <= kMaxWStages, "L1s ring depth");
 #define SVDQ_K1_LAMPRE 2                               // ring slots whose lambda tile goes out before griddepcontrol.wait
 #endif
 
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
@@ -202,6 +209,9 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dfull + 1);
   float *qinv_lut = reinterpret_cast<float *>(smem + Ly.bar_off + 512);
   uint32_t *rowmax = reinterpret_cast<uint32_t *>(smem + Ly.bar_off + 512 + 1024);   // W8A8: [RT] amax bits
+  // the tail's output parameters, staged in smem at setup: read from the (dynamically indexed)
+  // parameter space at the end of the kernel they cost a few hundred cycles of constant-cache miss
+  int64_t *tailp = reinterpret_cast<int64_t *>(smem + Ly.bar_off + 384);   // {xl1, xl1_f32, M}
   uint8_t *wring = smem + Ly.w_off;
 
   const int warp = threadIdx.x >> 5;
@@ -239,6 +249,11 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
     qinv_lut[code] = sfd == 0.f ? 0.f : __frcp_rn(__fmul_rn(sfd, p.gs_x));
   }
   if (kFmt == 2 && threadIdx.x < RT) rowmax[threadIdx.x] = 0u;
+  if (threadIdx.x == 64) {
+    tailp[0] = reinterpret_cast<int64_t>(p.xl1);
+    tailp[1] = reinterpret_cast<int64_t>(p.xl1_f32);
+    tailp[2] = p.M;
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -264,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
       // (~1.6 us) with the previous kernel's tail.  Safe while that kernel may still write X:
       // L2 is the coherence point and the TMA loads below are issued after the wait.
       for (int i = 0; i < nsteps && i < (SVDQ_K1_XPRE < S ? SVDQ_K1_XPRE : S); ++i)
-        tma_prefetch_3d(&tmX, 0, i * Q, static_cast<int32_t>(row0));
+        tma_prefetch_3d(&tmX, 0, static_cast<int32_t>(row0), i * Q);
       griddep_wait();
       int s = 0;
       uint32_t ph = 0;                                          // ring round parity of slot s
@@ -275,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
         }
         if (i < 64) RTRACE(2 + i);
         // X box {64 cols, Q blocks, RT rows}
-        tma_load_3d(smem + s * Ly.stage_bytes, &tmX, &full[s], 0, i * Q, static_cast<int32_t>(row0));
+        tma_load_3d(smem + s * Ly.stage_bytes, &tmX, &full[s], 0, static_cast<int32_t>(row0), i * Q);
         if (i + npre < S && i + npre < nsteps) load_lam(i + npre, i + npre);   // rest of the first ring
         if (++s == S) { s = 0; ph ^= 1; }
       }
@@ -351,10 +366,14 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
     // load latency.
     const int qw = warp - kQ0;
     const int team = qw >> 3;
-    const int R = (qw & 7) * 8 + (lane >> 2);                   // staged tile rows R and R + 64
+    // block-major stage: staged row R = q RT + m (block q of tile row m).  Pair index pidx (64 per
+    // team) -> block qb and rows m, m + RT / 2 of that block (same K block: one set of lambda loads)
+    const int half = RT / 2;
+    const int pidx = (qw & 7) * 8 + (lane >> 2);
+    const int R = (pidx / half) * RT + pidx % half;             // staged tile rows R and R + RT / 2
     const int q4 = lane & 3;                                    // 16-element group within the block
-    const int qb = R % Q;                                       // K block within the stage (both rows)
-    const int mh[2] = {R / Q, (R + 64) / Q};                    // rows within the tile
+    const int qb = pidx / half;                                 // K block within the stage (both rows)
+    const int mh[2] = {pidx % half, pidx % half + half};        // rows within the tile
     const float t6 = __fmul_rn(__frcp_rn(p.gs_x), __frcp_rn(6.0f));
     // output addressing: the layer's own layout (out_k = K, out_c0 = 0), or -- fused tensor-parallel
     // gather -- this K-slice's place inside the full-K layout (out_k = full K, out_c0 = k0 / 16)
@@ -370,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
       sf_base[h] = p.xs + sf_offset(row, p.out_c0, p.out_k) + static_cast<int64_t>(qb) * 512 + q4;
       s16_base[h] = p.xs + 2 * (row * (p.out_k / 64) + p.out_c0 / 4 + qb);
     }
-    const uint32_t swz = static_cast<uint32_t>(R & 7);          // == (R + 64) & 7
+    const uint32_t swz = static_cast<uint32_t>(R & 7);          // == (R + RT / 2) & 7 (RT / 2 % 8 == 0)
     const uint32_t lut = smem_u32(qinv_lut);
     const uint32_t stage0 = smem_u32(smem);
     // lambda row j = 2 qb + (q4 >> 1) of the swizzled [2Q][128 B] block; chunk (q4 & 1) * 4 + t
@@ -405,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
         lds_v2x64(sbase + lam_off[2 * c + 1], l2, l3);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const uint32_t xaddr = sbase + x_off[c] + h * 8192;   // row R + 64 h
+          const uint32_t xaddr = sbase + x_off[c] + h * half * 128;   // row R + (RT / 2) h
           const uint4 v = lds128(xaddr);
           const uint64_t x0 = x2_to_f32x2<kX16>(v.x), x1 = x2_to_f32x2<kX16>(v.y);
           const uint64_t x2 = x2_to_f32x2<kX16>(v.z), x3 = x2_to_f32x2<kX16>(v.w);
@@ -542,63 +561,94 @@ __global__ void __launch_bounds__(kThreads, 1) k1_rows_kernel(const __grid_const
   if (warp >= kQ0 && lane == 0) RTRACE(400 + warp - kQ0);
   if (r == 0) return;
   // ---------------------------------------------------------------------- xl1 = sum_q diag blocks
-  // No shared-memory round trip: a warp's 32 TMEM lanes are rows d = m Q + q of whole m (32 % Q == 0).
-  // The 16 quantizer warps split xl1's r columns into 8-column chunks (4 warps per lane quadrant,
-  // chunks qq, qq + 4, ...); for a chunk a warp loads it from every block q' (all loads, then one
-  // wait), each lane keeps the one of its own q (the diagonal), a butterfly over the Q lanes of a row
-  // sums them in a fixed order ((q0 + q1) + (q2 + q3) at Q = 4: deterministic), and lane q = 0 of
-  // the row stores the 8 columns.  The barrier first: the ring is no longer read by anyone.
+  // Block-major stage: TMEM lane d = q RT + m holds row m's partial over the K blocks of index q in
+  // columns [q r, q r + r) (the diagonal block).  A warp's 32 lanes span 32 / RT blocks (one when
+  // RT >= 32), so it reads only those columns -- a quarter of the Q r-column accumulator at Q = 4
+  // (TMEM reads run at 64 B / clk: reading all of it cost ~1 us per launch).  The 16 quantizer warps
+  // split xl1's r columns into 8-column chunks (4 warps per lane quadrant, chunks qq, qq + 4, ...),
+  // park the partials in the (now idle) ring as part[q][m][r + 4], and after a barrier of the
+  // quantizer warps each (row, chunk) is summed over q in the fixed pairwise order
+  // ((p0 + p1) + (p2 + p3) at Q = 4: deterministic, and the order of the former warp butterfly).
   __syncthreads();
-  if (threadIdx.x == 32 * kQ0) RTRACE(102);
+  if (threadIdx.x == 32 * kQ0) { RTRACE(102); CTRACE(500); }
   if (kFmt == 2 && threadIdx.x < RT && row0 + threadIdx.x < p.M)   // every row's amax -> xs (fp32)
     reinterpret_cast<float *>(p.xs)[row0 + threadIdx.x] = __uint_as_float(rowmax[threadIdx.x]);
   if (warp >= kQ0) {
     const int qd = warp & 3;                                   // TMEM lane quadrant of this warp
     const int qq = (warp - kQ0) >> 2;                          // 0..3 within the quadrant
-    const int d = 32 * qd + lane;                              // D row = m * Q + q
-    const int q = d % Q, mm = d / Q;
-    const int64_t row = row0 + mm;
+    const int d = 32 * qd + lane;                              // D row = q RT + m
+    const int q = d / RT, m = d % RT;
     const int nc8 = r / 8;
+    const int pst = r + 4;                                     // part row stride (floats), padded
+    float *part = reinterpret_cast<float *>(smem);
     if (qq < nc8) {
       q_wait(dfull, 0);
       tc_fence_after();
     }
-    if (threadIdx.x == 32 * kQ0) RTRACE(103);
-    for (int c8 = qq; c8 < nc8; c8 += 4) {
-      float val[8];
-      for (int q0 = 0; q0 < Q; q0 += 4) {
-        uint32_t v[4][8];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (q0 + u < Q) tmem_ld_32x32b_x8(tmem + (static_cast<uint32_t>(32 * qd) << 16) + (q0 + u) * r + 8 * c8, v[u]);
-        tmem_ld_wait();
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (q0 + u == q) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) val[j] = __uint_as_float(v[u][j]);
-          }
+    if (threadIdx.x == 32 * kQ0) { RTRACE(103); CTRACE(501); }
+    const int qa = (32 * qd) / RT;                             // first block in this quadrant
+    const int nbq = RT >= 32 ? 1 : 32 / RT;                    // blocks in this quadrant (2 at RT = 16)
+    for (int c8 = qq; c8 < ((SVDQ_K1REXP & 64) ? 0 : nc8); c8 += 4) {   // 64: ablation, no drain
+      uint32_t v[2][8];
+      tmem_ld_32x32b_x8(tmem + (static_cast<uint32_t>(32 * qd) << 16) + qa * r + 8 * c8, v[0]);
+      if (nbq > 1) tmem_ld_32x32b_x8(tmem + (static_cast<uint32_t>(32 * qd) << 16) + (qa + 1) * r + 8 * c8, v[1]);
+      tmem_ld_wait();
+      if (threadIdx.x == 32 * kQ0) CTRACE(503);
+      const int u = q - qa;
+      float *dst = part + (static_cast<int64_t>(q) * RT + m) * pst + 8 * c8;
+      if (u == 0) {
+        reinterpret_cast<float4 *>(dst)[0] = make_float4(__uint_as_float(v[0][0]), __uint_as_float(v[0][1]),
+                                                         __uint_as_float(v[0][2]), __uint_as_float(v[0][3]));
+        reinterpret_cast<float4 *>(dst)[1] = make_float4(__uint_as_float(v[0][4]), __uint_as_float(v[0][5]),
+                                                         __uint_as_float(v[0][6]), __uint_as_float(v[0][7]));
+      } else {
+        reinterpret_cast<float4 *>(dst)[0] = make_float4(__uint_as_float(v[1][0]), __uint_as_float(v[1][1]),
+                                                         __uint_as_float(v[1][2]), __uint_as_float(v[1][3]));
+        reinterpret_cast<float4 *>(dst)[1] = make_float4(__uint_as_float(v[1][4]), __uint_as_float(v[1][5]),
+                                                         __uint_as_float(v[1][6]), __uint_as_float(v[1][7]));
       }
-      for (int off = 1; off < Q; off <<= 1) {
+    }
+    named_bar_sync(1, 32 * kQuantWarps);                      // every partial parked
+    // (row m, chunk c8) items over the 512 quantizer threads
+    for (int it = threadIdx.x - 32 * kQ0; it < ((SVDQ_K1REXP & 64) ? 0 : RT * nc8); it += 32 * kQuantWarps) {
+      const int mm = it / nc8, c8 = it % nc8;
+      const int64_t row = row0 + mm;
+      if (row >= tailp[2]) continue;
+      float pv[8][8];                                          // [q][j], Q <= 8
 #pragma unroll
-        for (int j = 0; j < 8; ++j) val[j] += __shfl_xor_sync(0xffffffffu, val[j], off);
-      }
-      if (q == 0 && row < p.M) {
-        const int64_t c = row * r + 8 * c8;
-        if (p.xl1_f32) {
-          for (int j = 0; j < p.ndst; ++j) {
-            float4 *dst = reinterpret_cast<float4 *>(reinterpret_cast<uint8_t *>(p.xl1_f32 + c) + p.dst_delta[j]);
-            dst[0] = make_float4(val[0], val[1], val[2], val[3]);
-            dst[1] = make_float4(val[4], val[5], val[6], val[7]);
-          }
-        } else {
-          *reinterpret_cast<uint4 *>(p.xl1 + c) = make_uint4(pack_bf16x2(val[0], val[1]), pack_bf16x2(val[2], val[3]),
-                                                             pack_bf16x2(val[4], val[5]), pack_bf16x2(val[6], val[7]));
+      for (int qv = 0; qv < 8; ++qv) {
+        if (qv < Q) {
+          const float4 *src = reinterpret_cast<const float4 *>(part + (static_cast<int64_t>(qv) * RT + mm) * pst + 8 * c8);
+          const float4 a0 = src[0], a1 = src[1];
+          pv[qv][0] = a0.x; pv[qv][1] = a0.y; pv[qv][2] = a0.z; pv[qv][3] = a0.w;
+          pv[qv][4] = a1.x; pv[qv][5] = a1.y; pv[qv][6] = a1.z; pv[qv][7] = a1.w;
         }
+      }
+      float val[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {                            // pairwise tree over q
+        float t0 = pv[0][j];
+        if (Q == 2) t0 = pv[0][j] + pv[1][j];
+        else if (Q == 4) t0 = (pv[0][j] + pv[1][j]) + (pv[2][j] + pv[3][j]);
+        else if (Q == 8) t0 = ((pv[0][j] + pv[1][j]) + (pv[2][j] + pv[3][j])) + ((pv[4][j] + pv[5][j]) + (pv[6][j] + pv[7][j]));
+        val[j] = t0;
+      }
+      const int64_t c = row * r + 8 * c8;
+      if (tailp[1] && !(SVDQ_K1REXP & 512)) {
+        for (int j = 0; j < p.ndst; ++j) {
+          float4 *o = reinterpret_cast<float4 *>(reinterpret_cast<uint8_t *>(reinterpret_cast<float *>(tailp[1]) + c) +
+                                                 p.dst_delta[j]);
+          o[0] = make_float4(val[0], val[1], val[2], val[3]);
+          o[1] = make_float4(val[4], val[5], val[6], val[7]);
+        }
+      } else if (!(SVDQ_K1REXP & 512)) {
+        *reinterpret_cast<uint4 *>(reinterpret_cast<uint16_t *>(tailp[0]) + c) = make_uint4(
+            pack_bf16x2(val[0], val[1]), pack_bf16x2(val[2], val[3]), pack_bf16x2(val[4], val[5]),
+            pack_bf16x2(val[6], val[7]));
       }
     }
   }
-  if (threadIdx.x == 32 * kQ0) RTRACE(104);
+  if (threadIdx.x == 32 * kQ0) { RTRACE(104); CTRACE(502); }
   tc_fence_before();
   __syncthreads();                                             // every tcgen05.ld is done
   if (warp == 1) tmem_dealloc_n(tmem, tcols);

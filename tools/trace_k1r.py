@@ -32,3 +32,4 @@ print("quantizer warps at stage nsteps/2:", " ".join(f"{rel(420 + i):.2f}" for i
 print("quantizer warps done:", " ".join(f"{rel(400 + i):.2f}" for i in range(16)))
 print(f"tail: sync1 {rel(102):.2f}  dfull {rel(103):.2f}  drained {rel(104):.2f}  sync2 {rel(105):.2f}  stored {rel(101):.2f}")
 print(f"quantizer 0 done {rel(100):.2f}  xl1 stored {rel(101):.2f}")
+print(f"tail in SM cycles: sync1 -> dfull {t[501] - t[500]}  dfull -> tmem loads done {t[503] - t[501]}  -> drained {t[502] - t[503]}")
