@@ -121,3 +121,22 @@ def test_k1_grouped_equals_single(fmt, dt, shapes):
         qa = S.quantize_activation(x, ops)
         ref_q = F.pack_nibbles(qa.codes if fmt == "nvfp4" else F.int4_to_nibble(qa.codes))
         np.testing.assert_array_equal(sq.cpu().numpy().reshape(M, K // 2), ref_q)
+
+
+# Every row tile of the row-tile kernel (RT = 16 / 32 / 64 / 128, i.e. Q = 8 / 4 / 2 / 1 K-blocks per
+# block-major stage, quantizer rows m and m + RT/2 of one block) -- the tile is the smallest whose
+# CTA count fits one wave, so M selects it; ragged M (a partial last tile) and fp16 X included.
+@pytest.mark.parametrize("M,dt", [(1000, "bf16"), (2500, "fp16"), (9000, "bf16"), (9700, "fp16")])
+def test_k1_every_row_tile(M, dt):
+    need_cuda()
+    import paper_2411_05007_b200 as P
+    rt = P.svdq_k1_row_tile((M + 127) // 128 * 128, 32)
+    assert rt in (16, 32, 64, 128)
+    run_k1("nvfp4", M, 576, 64, 32, dt=dt, seed=M)
+
+
+def test_k1_row_tiles_all_reached():
+    need_cuda()
+    import paper_2411_05007_b200 as P
+    got = {P.svdq_k1_row_tile((M + 127) // 128 * 128, 32) for M in (1000, 2500, 9000, 9700)}
+    assert got == {16, 32, 64, 128}, got
