@@ -1,6 +1,6 @@
 """K2's L2-banded tile order (large M) covers every output tile exactly once: the same launch with
 banding forced on (SVDQ_K2_BAND_MB tiny, so a few 256-row tiles per band, ragged last band,
-ragged M / N) and off (SVDQ_K2_BAND_MB=0) gives bit-identical Y, single and grouped.  The
+ragged M / N) and off (SVDQ_K2_BAND_MB=0) gives bit-identical Y, single, grouped and W8A8.  The
 unbanded path is itself oracle-checked (test_gpu_k2.py, test_gpu_step_full.py); tile order cannot
 change a tile's arithmetic, so equality is the whole contract.  The knob is read once per process,
 hence one subprocess per setting."""
@@ -35,6 +35,19 @@ for i, (M, K, N) in enumerate(shapes):
     y = P.svdq_gemm_w4a4_lowrank_up(layer, xq, xs, xl1, M)
     out[f"single{i}"] = y.view(torch.int16).cpu().numpy()
     layers.append(layer); xqs.append(xq); xss.append(xs); xl1s.append(xl1)
+# W8A8 (kind::i8 pair tiles, 1-byte operands: bands of fewer row tiles)
+g = torch.Generator(device=dev).manual_seed(7)
+M8, K8, N8 = 2600, 1024, 576
+w8 = P.QuantizedLinear.empty("w8a8", K8, N8, 16, device=dev)
+w8.w_codes.random_(0, 256, generator=g)
+w8.w_scales.view(torch.float32).uniform_(0.001, 0.01, generator=g)
+w8.l1s.random_(-3000, 3000, generator=g)
+w8.l2s.random_(-3000, 3000, generator=g)
+w8.lambda_inv.uniform_(0.5, 2.0, generator=g)
+w8._sync_view()
+x8 = torch.randn(M8, K8, device=dev, generator=g).to(torch.bfloat16)
+q8, s8, l8 = P.svdq_quantize_act_lowrank_down(w8, x8)
+out["w8a8"] = P.svdq_gemm_w4a4_lowrank_up(w8, q8, s8, l8, M8).view(torch.int16).cpu().numpy()
 ys = [torch.empty(M, N, dtype=torch.bfloat16, device=dev) for (M, K, N) in shapes]
 P.svdq_gemm_w4a4_lowrank_up_grouped(layers, xqs, xss, xl1s, [s[0] for s in shapes], ys)
 torch.cuda.synchronize()
